@@ -1,0 +1,158 @@
+/* sfxb_cuda.h — C ABI of the B200-native Paillier plugin (libsfxb_cuda.so).
+ *
+ * This is the thin layer between host code and the sm_100a kernels.  It
+ * replaces the three scalar-path virtuals of the reference's
+ * `sfxb::EncryptionPlugin` (/root/reference/proj/include/sfxb/
+ * secure_processor.hpp:112-143) as implemented by `PaillierPlugin`
+ * (proj/src/secure_processor.cpp:553-746), and the HE primitives they bottom
+ * out in (proj/src/he.cpp:87-143).  The C++ adapter that re-exposes these as an
+ * EncryptionPlugin lives in paper_2504_03909_b200/host/ (INTEGRATION.md).
+ *
+ * Conventions
+ *   - Big integers are little-endian arrays of uint32_t limbs.  A value mod n
+ *     takes `n_words` limbs, a ciphertext (mod n²) takes 2·n_words limbs.
+ *   - All pointers are caller-owned and only used for the duration of the
+ *     call.  Host-pointer entry points are synchronous.  `*_dev` entry points
+ *     take device pointers on the context's device, are ordered on the
+ *     context's stream and return after enqueueing unless stated otherwise.
+ *   - Every entry point returns SFXB_OK (0) or a negative code; the message
+ *     is in sfxb_last_error(ctx) and repeats the reference's exception text
+ *     where one exists (e.g. "not coprime", "bin index out of range in
+ *     accumulate", "decrypt requested without private key material").
+ *   - A context is used by one host thread at a time (the reference calls one
+ *     plugin instance from one thread at a time, federation.cpp:509-516);
+ *     distinct contexts may be used concurrently.
+ *   - There is no CPU fallback: without a usable sm_100 device every call
+ *     fails with SFXB_ERR_CUDA.
+ */
+#ifndef SFXB_CUDA_H
+#define SFXB_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    SFXB_OK = 0,
+    SFXB_ERR_ARG = -1,         /* bad argument / shape (reference: sfxb::Error)        */
+    SFXB_ERR_CUDA = -2,        /* CUDA runtime failure or no device                     */
+    SFXB_ERR_AUTH = -3,        /* private key required (reference: AuthorizationError) */
+    SFXB_ERR_RANGE = -4,       /* value out of range (plaintext, blinding, ciphertext)  */
+    SFXB_ERR_COPRIME = -5,     /* value not coprime to n                                */
+    SFXB_ERR_UNSUPPORTED = -6, /* key size / shape outside the built size classes      */
+};
+
+typedef struct sfxb_ctx sfxb_ctx;
+
+/* ---- key context -------------------------------------------------------
+ * Replaces make_paillier_plugin(const PaillierPublicKey&, ...) and
+ * make_paillier_plugin(const PaillierKeypair&, ...)
+ * (secure_processor.hpp:155-158, secure_processor.cpp:754-762).
+ * p, q: NULL for a public-key-only holder (passive party,
+ * federation.cpp:83-85); otherwise pq_words limbs each.  n up to 3072 bits. */
+int sfxb_ctx_create(sfxb_ctx **out, int device, const uint32_t *n, uint32_t n_words,
+                    const uint32_t *p, const uint32_t *q, uint32_t pq_words);
+void sfxb_ctx_destroy(sfxb_ctx *ctx);
+const char *sfxb_last_error(const sfxb_ctx *ctx);
+/* error text of the last failed sfxb_ctx_create on this thread */
+const char *sfxb_create_error(void);
+uint32_t sfxb_ctx_n_words(const sfxb_ctx *ctx);
+uint32_t sfxb_ctx_ct_words(const sfxb_ctx *ctx);
+int sfxb_ctx_has_private(const sfxb_ctx *ctx);
+/* key_id_of(n): FNV-1a-64 over the lower-case hex digits of n (he.cpp:30-38) */
+uint64_t sfxb_ctx_key_id(const sfxb_ctx *ctx);
+/* number of our kernels launched by this context so far (bench evidence) */
+uint64_t sfxb_ctx_launches(const sfxb_ctx *ctx);
+
+/* ---- encrypt -------------------------------------------------------------
+ * Batch of encrypt_with_r (he.cpp:87-99) as driven by PaillierPlugin::
+ * encrypt_gh (secure_processor.cpp:574-585):
+ *     c_i = ((1 + m_i·n) mod n²) · (r_i^n mod n²) mod n²
+ * with m_i = q_i mod n, q_i the fixed-point value fixed_encode_ll(x, scale)
+ * (fixed_point.hpp:13-15; encode_fixed's range checks he.cpp:125-136 are the
+ * caller's, see sfxb_encode_check).  r: count × n_words limbs, 1 < r < n.
+ * With p, q present the kernel uses CRT (mod p², q²); otherwise r^n mod n².
+ * r_flags (optional, count bytes): set to 1 where r shares a factor with n
+ * (only detectable with p, q; the call then fails with SFXB_ERR_COPRIME so the
+ * caller can re-draw per the reference's rejection rule, he.cpp:19-28). */
+int sfxb_encrypt(sfxb_ctx *ctx, const int64_t *q_fixed, const uint32_t *r, size_t count,
+                 uint32_t *out_cts, uint8_t *r_flags);
+int sfxb_encrypt_dev(sfxb_ctx *ctx, const int64_t *d_q_fixed, const uint32_t *d_r, size_t count,
+                     uint32_t *d_out_cts, uint8_t *d_r_flags);
+
+/* encode_fixed's checks (he.cpp:125-136) without the mpz work: returns
+ * SFXB_OK and q = llround(ldexp(x, scale)), or SFXB_ERR_RANGE with the
+ * reference's message. */
+int sfxb_encode_check(sfxb_ctx *ctx, double x, uint32_t scale_bits, int64_t *q_out);
+
+/* ---- ciphertext addition (add_ciphertexts, he.cpp:117-121), batched -------- */
+int sfxb_add(sfxb_ctx *ctx, const uint32_t *a, const uint32_t *b, size_t count, uint32_t *out);
+
+/* ---- encrypted histogram ---------------------------------------------------
+ * PaillierPlugin::accumulate_rows (secure_processor.cpp:587-620) for one
+ * party and one frontier:
+ *   gh_cts      2·n_samples ciphertexts, interleaved Enc(g_i), Enc(h_i)
+ *   bins        n_features columns of n_samples uint16 (column-major,
+ *               dataset.hpp:55-57), feature order = output order
+ *   node_offsets[n_nodes+1] / rows: the rows of each frontier node
+ *   out_slots   n_nodes × n_features × n_bins × 2 ciphertexts; slot
+ *               ((node·J + f)·K + b)·2 + {0:G, 1:H}; empty slots are the
+ *               literal 1 (trivial_zero, he.cpp:123)
+ *   additions   += the reference's ciphertext_additions for this call,
+ *               Σ_slots max(count − 1, 0) (fold_into, :724-732)
+ * Errors: "bin index out of range in accumulate", row index out of range. */
+int sfxb_accumulate(sfxb_ctx *ctx, const uint32_t *gh_cts, uint32_t n_samples,
+                    const uint16_t *bins, uint32_t n_features, const uint32_t *node_offsets,
+                    uint32_t n_nodes, const uint32_t *rows, uint32_t n_bins, uint32_t *out_slots,
+                    uint64_t *additions);
+
+/* Device-resident gradient ciphertexts (Montgomery form), reusable across
+ * the levels of a tree; the C++ adapter keys it on content. */
+typedef struct sfxb_gh sfxb_gh;
+int sfxb_gh_upload(sfxb_ctx *ctx, const uint32_t *gh_cts, uint32_t n_samples, sfxb_gh **out);
+int sfxb_gh_from_dev(sfxb_ctx *ctx, const uint32_t *d_gh_cts, uint32_t n_samples, sfxb_gh **out);
+void sfxb_gh_free(sfxb_gh *gh);
+
+/* Histogram over a resident gh with device-resident bins and frontier.
+ * mont_out != 0 leaves the slots in Montgomery form (partials for the
+ * multi-GPU reduce); additions is synchronous (host) and may be NULL. */
+int sfxb_accumulate_dev(sfxb_ctx *ctx, const sfxb_gh *gh, const uint16_t *d_bins,
+                        uint32_t n_features, const uint32_t *d_node_offsets, uint32_t n_nodes,
+                        const uint32_t *d_rows, uint32_t n_rows, uint32_t n_bins,
+                        uint32_t *d_out_slots, int mont_out, uint64_t *additions);
+
+/* K4: element-wise product of `parts` partial histograms (Montgomery form,
+ * each n_slots ciphertexts, contiguous) into d_out (plain form, n_slots).
+ * Used after the all-gather of per-GPU row-shard partials (homomorphic
+ * addition is a modular product, so an NCCL sum cannot combine them). */
+int sfxb_reduce_partials_dev(sfxb_ctx *ctx, const uint32_t *d_parts, uint32_t parts,
+                             size_t n_slots, uint32_t *d_out);
+
+/* ---- decrypt -----------------------------------------------------------------
+ * PaillierPlugin::decrypt_histogram / decrypt_slot (secure_processor.cpp:
+ * 679-719, :734-738) + decrypt (he.cpp:105-115) + decode_fixed (:138-143):
+ * slots equal to 1 decode to 0.0 and are not counted; others are decrypted
+ * (CRT mod p², q²; bit-identical to the reference's c^λ mod n² path) and
+ * decoded exactly like mpz_get_d (truncation) then ldexp(−scale).
+ * out_plain (optional): count × n_words decrypted plaintexts.
+ * Errors: SFXB_ERR_AUTH without p, q; "ciphertext out of range";
+ * "ciphertext not coprime to modulus". */
+int sfxb_decrypt(sfxb_ctx *ctx, const uint32_t *cts, size_t count, uint32_t scale_bits,
+                 double *out_values, uint32_t *out_plain, uint64_t *decryptions);
+int sfxb_decrypt_dev(sfxb_ctx *ctx, const uint32_t *d_cts, size_t count, uint32_t scale_bits,
+                     double *d_out_values, uint32_t *d_out_plain, uint64_t *decryptions);
+
+/* ---- stream / timing helpers (bench + tests) ---------------------------------- */
+void *sfxb_ctx_stream(sfxb_ctx *ctx); /* cudaStream_t of the context */
+int sfxb_ctx_sync(sfxb_ctx *ctx);
+/* integer-multiply peak microbenchmark: IMAD.WIDE.U32(.X) 32×32→64 products/s */
+int sfxb_imad_peak(int device, double *products_per_s, double *sm_clock_mhz);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SFXB_CUDA_H */

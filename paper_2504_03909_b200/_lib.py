@@ -1,0 +1,207 @@
+"""ctypes binding of libsfxb_cuda.so (the C ABI in include/sfxb_cuda.h).
+
+This is plumbing for the Python tests and bench.py; the product boundary is
+the C ABI itself (and the C++ EncryptionPlugin adapter in host/).  There is no
+CPU fallback: if the shared library or a B200 is missing, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "lib", "libsfxb_cuda.so")
+
+SFXB_OK = 0
+SFXB_ERR_ARG = -1
+SFXB_ERR_CUDA = -2
+SFXB_ERR_AUTH = -3
+SFXB_ERR_RANGE = -4
+SFXB_ERR_COPRIME = -5
+SFXB_ERR_UNSUPPORTED = -6
+
+
+class SfxbError(RuntimeError):
+    """Carries the C ABI error code and the reference-compatible message."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+class AuthorizationError(SfxbError):
+    """Mirrors sfxb::AuthorizationError (errors.hpp:26-28)."""
+
+
+_u32p = np.ctypeslib.ndpointer(dtype=np.uint32, flags="C_CONTIGUOUS")
+_u16p = np.ctypeslib.ndpointer(dtype=np.uint16, flags="C_CONTIGUOUS")
+_i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_u8p = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise SfxbError(SFXB_ERR_CUDA, f"{LIB_PATH} not built (run __graft_entry__.build())")
+    lib = C.CDLL(LIB_PATH)
+    vp, sz = C.c_void_p, C.c_size_t
+    sig = {
+        "sfxb_ctx_create": (C.c_int, [C.POINTER(vp), C.c_int, _u32p, C.c_uint32, vp, vp, C.c_uint32]),
+        "sfxb_ctx_destroy": (None, [vp]),
+        "sfxb_last_error": (C.c_char_p, [vp]),
+        "sfxb_create_error": (C.c_char_p, []),
+        "sfxb_ctx_n_words": (C.c_uint32, [vp]),
+        "sfxb_ctx_ct_words": (C.c_uint32, [vp]),
+        "sfxb_ctx_has_private": (C.c_int, [vp]),
+        "sfxb_ctx_key_id": (C.c_uint64, [vp]),
+        "sfxb_ctx_launches": (C.c_uint64, [vp]),
+        "sfxb_ctx_stream": (vp, [vp]),
+        "sfxb_ctx_sync": (C.c_int, [vp]),
+        "sfxb_encrypt": (C.c_int, [vp, _i64p, _u32p, sz, _u32p, vp]),
+        "sfxb_encrypt_dev": (C.c_int, [vp, vp, vp, sz, vp, vp]),
+        "sfxb_encode_check": (C.c_int, [vp, C.c_double, C.c_uint32, C.POINTER(C.c_int64)]),
+        "sfxb_add": (C.c_int, [vp, _u32p, _u32p, sz, _u32p]),
+        "sfxb_accumulate": (C.c_int, [vp, _u32p, C.c_uint32, _u16p, C.c_uint32, _u32p, C.c_uint32, _u32p,
+                                      C.c_uint32, _u32p, C.POINTER(C.c_uint64)]),
+        "sfxb_gh_upload": (C.c_int, [vp, _u32p, C.c_uint32, C.POINTER(vp)]),
+        "sfxb_gh_from_dev": (C.c_int, [vp, vp, C.c_uint32, C.POINTER(vp)]),
+        "sfxb_gh_free": (None, [vp]),
+        "sfxb_accumulate_dev": (C.c_int, [vp, vp, vp, C.c_uint32, vp, C.c_uint32, vp, C.c_uint32, C.c_uint32,
+                                          vp, C.c_int, C.POINTER(C.c_uint64)]),
+        "sfxb_reduce_partials_dev": (C.c_int, [vp, vp, C.c_uint32, sz, vp]),
+        "sfxb_decrypt": (C.c_int, [vp, _u32p, sz, C.c_uint32, _f64p, vp, C.POINTER(C.c_uint64)]),
+        "sfxb_decrypt_dev": (C.c_int, [vp, vp, sz, C.c_uint32, vp, vp, C.POINTER(C.c_uint64)]),
+        "sfxb_imad_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name, None)
+        if fn is None:
+            continue
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def exported_symbols() -> list[str]:
+    """Names declared in include/sfxb_cuda.h (checked against the .so by the CPU tests)."""
+    import re
+
+    hdr = os.path.join(os.path.dirname(PKG), "include", "sfxb_cuda.h")
+    text = open(hdr).read()
+    return sorted(set(re.findall(r"\b(sfxb_[a-z0-9_]+)\s*\(", text)))
+
+
+def to_words(x: int, words: int) -> np.ndarray:
+    return np.frombuffer(int(x).to_bytes(4 * words, "little"), dtype=np.uint32).copy()
+
+
+def from_words(w) -> int:
+    return int.from_bytes(np.ascontiguousarray(w, dtype=np.uint32).tobytes(), "little")
+
+
+class Context:
+    """One Paillier key on one device (sfxb_ctx)."""
+
+    def __init__(self, n: int, p: int | None = None, q: int | None = None, device: int = 0):
+        lib = load()
+        self.lib = lib
+        self.n = n
+        self.nw = (n.bit_length() + 31) // 32
+        h = C.c_void_p()
+        nw_arr = to_words(n, self.nw)
+        if p is not None:
+            pw = max((p.bit_length() + 31) // 32, (q.bit_length() + 31) // 32)
+            pa, qa = to_words(p, pw), to_words(q, pw)
+            rc = lib.sfxb_ctx_create(C.byref(h), device, nw_arr, self.nw, pa.ctypes.data, qa.ctypes.data, pw)
+        else:
+            rc = lib.sfxb_ctx_create(C.byref(h), device, nw_arr, self.nw, None, None, 0)
+        if rc != SFXB_OK:
+            raise SfxbError(rc, lib.sfxb_create_error().decode())
+        self.h = h
+        self.ct_words = lib.sfxb_ctx_ct_words(h)
+        self.key_id = lib.sfxb_ctx_key_id(h)
+        self.has_private = bool(lib.sfxb_ctx_has_private(h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.sfxb_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != SFXB_OK:
+            msg = self.lib.sfxb_last_error(self.h).decode()
+            if rc == SFXB_ERR_AUTH:
+                raise AuthorizationError(rc, msg)
+            raise SfxbError(rc, msg)
+
+    @property
+    def launches(self) -> int:
+        return self.lib.sfxb_ctx_launches(self.h)
+
+    def encode_check(self, x: float, scale: int = 40) -> int:
+        q = C.c_int64()
+        self._check(self.lib.sfxb_encode_check(self.h, float(x), scale, C.byref(q)))
+        return q.value
+
+    def encrypt(self, q_fixed, r):
+        """q_fixed: int64[count]; r: uint32[count, n_words] -> uint32[count, ct_words]."""
+        q_fixed = np.ascontiguousarray(q_fixed, dtype=np.int64)
+        r = np.ascontiguousarray(r, dtype=np.uint32)
+        count = q_fixed.shape[0]
+        out = np.zeros((count, self.ct_words), np.uint32)
+        flags = np.zeros(count, np.uint8)
+        self._check(self.lib.sfxb_encrypt(self.h, q_fixed, r.reshape(-1), count, out, flags.ctypes.data))
+        return out
+
+    def add(self, a, b):
+        a = np.ascontiguousarray(a, dtype=np.uint32)
+        b = np.ascontiguousarray(b, dtype=np.uint32)
+        out = np.zeros_like(a)
+        self._check(self.lib.sfxb_add(self.h, a.reshape(-1), b.reshape(-1), a.shape[0], out.reshape(-1)))
+        return out
+
+    def accumulate(self, gh_cts, bins, node_offsets, rows, n_bins):
+        gh_cts = np.ascontiguousarray(gh_cts, dtype=np.uint32)
+        bins = np.ascontiguousarray(bins, dtype=np.uint16)
+        J, n_samples = bins.shape
+        n_nodes = len(node_offsets) - 1
+        out = np.zeros((n_nodes * J * n_bins * 2, self.ct_words), np.uint32)
+        adds = C.c_uint64(0)
+        self._check(self.lib.sfxb_accumulate(
+            self.h, gh_cts.reshape(-1), n_samples, bins.reshape(-1), J,
+            np.ascontiguousarray(node_offsets, dtype=np.uint32), n_nodes,
+            np.ascontiguousarray(rows, dtype=np.uint32), n_bins, out.reshape(-1), C.byref(adds)))
+        return out, adds.value
+
+    def decrypt(self, cts, scale: int = 40, want_plain: bool = False):
+        cts = np.ascontiguousarray(cts, dtype=np.uint32)
+        count = cts.shape[0]
+        vals = np.zeros(count, np.float64)
+        plain = np.zeros((count, self.nw), np.uint32) if want_plain else None
+        decs = C.c_uint64(0)
+        self._check(self.lib.sfxb_decrypt(self.h, cts.reshape(-1), count, scale, vals,
+                                          plain.ctypes.data if want_plain else None, C.byref(decs)))
+        return (vals, decs.value, plain) if want_plain else (vals, decs.value)
+
+
+def imad_peak(device: int = 0):
+    lib = load()
+    p, clk = C.c_double(), C.c_double()
+    rc = lib.sfxb_imad_peak(device, C.byref(p), C.byref(clk))
+    if rc != SFXB_OK:
+        raise SfxbError(rc, "imad peak microbenchmark failed")
+    return p.value, clk.value

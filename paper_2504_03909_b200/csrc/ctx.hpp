@@ -1,0 +1,70 @@
+// Host-side key context shared by the translation units of libsfxb_cuda.so.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "bignum_host.hpp"
+
+namespace sfxb {
+
+// Device copy of a Montgomery modulus: 4·S words [m | R mod m | R² | R³].
+struct DevMod {
+    uint32_t *w = nullptr;
+    uint32_t np = 0;
+    int S = 0;
+};
+
+// Size class: s = limbs of a prime; mod-p² and mod-n values use 2s limbs,
+// ciphertexts (mod n²) 4s limbs.  s ∈ {4 (n ≤ 256 bits, tests), 8 (512),
+// 16 (1024), 32 (2048), 48 (3072)}.
+struct Buf {
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+
+struct CtxState {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int sms = 148;
+    int s = 0;          // size class
+    uint32_t nw = 0;    // exact limbs of n as given
+    bool has_priv = false;
+    uint64_t key_id = 0;
+    uint64_t launches = 0;
+    std::string err;
+
+    host::Big n, p, q, n2;
+    DevMod mod_n2, mod_n, mod_pq[2], mod_pq2[2];
+    // device constants (each padded to its modulus size)
+    uint32_t *d_n = nullptr;          // n, 2s limbs
+    uint32_t *d_n4 = nullptr;         // n, 4s limbs
+    uint32_t *d_n2w = nullptr;        // n², 4s limbs
+    uint32_t *d_nR_n2 = nullptr;      // n·R mod n²            (4s)
+    uint32_t *d_q2R_n2 = nullptr;     // q²·R mod n²           (4s)
+    uint32_t *d_qq_inv_m = nullptr;   // (q²)^-1·R mod p²      (2s)
+    uint32_t *d_pinv[2] = {nullptr, nullptr};  // p^-1 mod 2^(32s), q^-1 mod 2^(32s)   (s)
+    uint32_t *d_hR[2] = {nullptr, nullptr};    // h_p·R mod p, h_q·R mod q            (s)
+    uint32_t *d_qinvR_p = nullptr;    // q^-1·R mod p          (s)
+    uint32_t *d_qR_n = nullptr;       // q·R mod n             (2s)
+    // exponent window digits (device) and their counts
+    uint8_t *d_dig_n = nullptr;
+    int nd_n = 0;
+    uint8_t *d_dig_e1[2] = {nullptr, nullptr}; // q mod (p−1), p mod (q−1)
+    int nd_e1[2] = {0, 0};
+    uint8_t *d_dig_pq[2] = {nullptr, nullptr}; // p, q
+    int nd_pq[2] = {0, 0};
+    uint8_t *d_dig_m1[2] = {nullptr, nullptr}; // p−1, q−1
+    int nd_m1[2] = {0, 0};
+
+    // scratch (grown on demand, freed with the context)
+    Buf scratch_table, tmp[4], host_pinned[2];
+    std::vector<void *> owned; // device allocations of constants
+};
+
+constexpr int kWindow = 5; // fixed exponent window for the 1024-bit CRT exponents
+constexpr int kWindowN = 5;
+
+} // namespace sfxb

@@ -1,0 +1,373 @@
+// Warp-cooperative CIOS Montgomery arithmetic on 32-bit limbs for sm_100a.
+//
+// One big-integer "instance" (an S-limb value mod M, S = 32·k bits / 32) is
+// spread over TPI consecutive lanes of a warp; lane t owns limbs
+// [t·L, t·L+L), L = S/TPI (even).  The multiply
+//     MontMul(a, b) = a·b·2^(−32S) mod M        (a, b < M, result < M)
+// is CIOS (coarsely integrated operand scanning): S iterations, each adds
+// a·b_i and q_i·M (q_i = acc_0·(−M⁻¹) mod 2^32) and shifts the accumulator
+// down one limb.
+//
+// Instruction shape: every 32×32 product is ONE
+// IMAD.WIDE.U32(.X) — the PTX pair `mad{c}.lo.cc / madc.hi.cc` on the same
+// operands with a 64-bit addend in an aligned register pair fuses into one
+// wide multiply-add with carry-in/carry-out predicate on sm_100a.  To keep the
+// addend pairs aligned the accumulator is held as two arrays (sppark-style):
+// E (pairs at even limb positions) and O (pairs at odd positions); a limb
+// shift turns O into the next E, and the old E becomes the next O by a MAD
+// that reads its addend two registers up (the shift costs no moves).  Carries
+// that leave a lane's window are kept in one word Z and folded into the lane's
+// top limb one step later; the one-limb shift across lanes is two
+// __shfl_down_sync per iteration, q_i is one __shfl_sync.  Operand b is read
+// limb-pair by limb-pair (LDS.64) from shared memory.
+//
+// Exactness: with a, b < M the CIOS accumulator stays < 2M, so after the last
+// iteration one cross-lane carry resolution (ballot carry-lookahead) and one
+// conditional subtraction give the canonical residue in [0, M) — the residues
+// are unique, so results are bit-identical to GMP's `a*b % M` path.
+#pragma once
+#include <cstdint>
+
+namespace sfxb {
+namespace dev {
+
+// ---------------------------------------------------------------- PTX carry primitives
+
+__device__ __forceinline__ uint32_t add_cc(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t addc_cc(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm volatile("addc.cc.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t addc(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm volatile("addc.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t sub_cc(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm volatile("sub.cc.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t subc_cc(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm volatile("subc.cc.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t subc(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm volatile("subc.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+// (d0,d1) = a·b + (c0,c1), carry out          -> IMAD.WIDE.U32 (P out)
+__device__ __forceinline__ void mad_w_cc(uint32_t &d0, uint32_t &d1, uint32_t a, uint32_t b,
+                                         uint32_t c0, uint32_t c1) {
+    asm volatile("mad.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.cc.u32 %1, %2, %3, %5;"
+                 : "=r"(d0), "=r"(d1)
+                 : "r"(a), "r"(b), "r"(c0), "r"(c1));
+}
+// (d0,d1) = a·b + (c0,c1) + carry in, carry out -> IMAD.WIDE.U32.X (P in/out)
+__device__ __forceinline__ void madc_w_cc(uint32_t &d0, uint32_t &d1, uint32_t a, uint32_t b,
+                                          uint32_t c0, uint32_t c1) {
+    asm volatile("madc.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.cc.u32 %1, %2, %3, %5;"
+                 : "=r"(d0), "=r"(d1)
+                 : "r"(a), "r"(b), "r"(c0), "r"(c1));
+}
+// (d0,d1) = a·b (no carries)
+__device__ __forceinline__ void mul_w(uint32_t &d0, uint32_t &d1, uint32_t a, uint32_t b) {
+    uint64_t p = (uint64_t)a * b;
+    d0 = (uint32_t)p;
+    d1 = (uint32_t)(p >> 32);
+}
+
+// ---------------------------------------------------------------- instance geometry
+
+template <int S_, int TPI_>
+struct Geom {
+    static constexpr int S = S_;
+    static constexpr int TPI = TPI_;
+    static constexpr int L = S / TPI;
+    static_assert(S % TPI == 0, "TPI must divide S");
+    static_assert(L % 2 == 0 && L >= 2, "limbs per lane must be even");
+    static_assert(TPI == 1 || TPI == 2 || TPI == 4 || TPI == 8 || TPI == 16 || TPI == 32, "TPI");
+};
+
+// Lane index inside the instance and the instance's base lane in the warp.
+template <int TPI>
+__device__ __forceinline__ int inst_lane() {
+    return (int)(threadIdx.x & 31) & (TPI - 1);
+}
+template <int TPI>
+__device__ __forceinline__ uint32_t inst_mask_shift() {
+    return (threadIdx.x & 31) & ~(uint32_t)(TPI - 1);
+}
+
+// broadcast from lane `src` of the instance
+template <int TPI>
+__device__ __forceinline__ uint32_t inst_bcast(uint32_t v, int src) {
+    if constexpr (TPI == 1) return v;
+    else return __shfl_sync(0xffffffffu, v, src, TPI);
+}
+// value of lane t+1 (0 for the top lane)
+template <int TPI>
+__device__ __forceinline__ uint32_t from_above(uint32_t v) {
+    if constexpr (TPI == 1) return 0u;
+    else {
+        uint32_t r = __shfl_down_sync(0xffffffffu, v, 1, TPI);
+        return inst_lane<TPI>() == TPI - 1 ? 0u : r;
+    }
+}
+// value of lane t−1 (0 for lane 0)
+template <int TPI>
+__device__ __forceinline__ uint32_t from_below(uint32_t v) {
+    if constexpr (TPI == 1) return 0u;
+    else {
+        uint32_t r = __shfl_up_sync(0xffffffffu, v, 1, TPI);
+        return inst_lane<TPI>() == 0 ? 0u : r;
+    }
+}
+// per-instance bit masks of a warp-wide predicate (bit t = lane t of this instance)
+template <int TPI>
+__device__ __forceinline__ uint32_t inst_ballot(bool pred) {
+    if constexpr (TPI == 1) return pred ? 1u : 0u;
+    else {
+        uint32_t b = __ballot_sync(0xffffffffu, pred);
+        return (b >> inst_mask_shift<TPI>()) & ((TPI == 32) ? 0xffffffffu : ((1u << TPI) - 1u));
+    }
+}
+
+// ---------------------------------------------------------------- shared-memory operand b
+//
+// Operand b of an instance lives in shared memory as S/2 limb pairs, pair i
+// of instance k at sB[i * NI + k] (uint2), NI = instances per block; the
+// TPI lanes of an instance read the same pair (broadcast) and the instances
+// of a warp read consecutive 8-byte words (conflict-free LDS.64).
+
+template <int S, int TPI>
+__device__ __forceinline__ void store_b(uint2 *sB, int NI, int inst, const uint32_t (&v)[S / TPI]) {
+    constexpr int L = S / TPI;
+    const int t = inst_lane<TPI>();
+#pragma unroll
+    for (int j = 0; j < L / 2; ++j) sB[(t * (L / 2) + j) * NI + inst] = make_uint2(v[2 * j], v[2 * j + 1]);
+}
+
+// ---------------------------------------------------------------- CIOS core
+
+// One CIOS step for limb pair (b_lo at iteration i, b_hi at i+1) is written
+// as two calls of `step` with the E/O roles swapped.
+template <int L, int TPI>
+__device__ __forceinline__ void cios_step(uint32_t (&E)[L], uint32_t (&Q)[L], uint32_t &Z,
+                                          const uint32_t (&A)[L], const uint32_t (&N)[L],
+                                          uint32_t bi, uint32_t np, bool first) {
+    const int t = inst_lane<TPI>();
+    uint32_t Zn;
+    if (first) {
+        // E = A_even·b_i, O(Q) = A_odd·b_i
+#pragma unroll
+        for (int k = 0; k < L / 2; ++k) {
+            mul_w(Q[2 * k], Q[2 * k + 1], A[2 * k + 1], bi);
+            mul_w(E[2 * k], E[2 * k + 1], A[2 * k], bi);
+        }
+        Zn = 0;
+    } else {
+        // The one-limb shift of the previous step: the old E (now in Q) moves
+        // down; its two lowest words belong to lane t−1's window.
+        const uint32_t u0 = from_above<TPI>(Q[0]);
+        const uint32_t u1 = from_above<TPI>(Q[1]);
+        const uint32_t x = (t == 0) ? Q[1] : 0u; // lane 0: limb 0 of the new window
+        E[0] = add_cc(E[0], x);
+        // O = A_odd·b_i + (old E >> 2 limbs): fused shift, carry chain from E[0]
+#pragma unroll
+        for (int k = 0; k < L / 2 - 1; ++k)
+            madc_w_cc(Q[2 * k], Q[2 * k + 1], A[2 * k + 1], bi, Q[2 * k + 2], Q[2 * k + 3]);
+        madc_w_cc(Q[L - 2], Q[L - 1], A[L - 1], bi, u0, u1);
+        Zn = addc(0u, 0u);
+        Q[L - 1] = add_cc(Q[L - 1], Z); // old Z now sits at the top of the window
+        Zn = addc(Zn, 0u);
+        // E += A_even·b_i
+        mad_w_cc(E[0], E[1], A[0], bi, E[0], E[1]);
+#pragma unroll
+        for (int k = 1; k < L / 2; ++k) madc_w_cc(E[2 * k], E[2 * k + 1], A[2 * k], bi, E[2 * k], E[2 * k + 1]);
+        Q[L - 1] = addc_cc(Q[L - 1], 0u);
+        Zn = addc(Zn, 0u);
+    }
+    // q_i from limb 0 (lane 0 only holds it), broadcast to the instance
+    const uint32_t q = inst_bcast<TPI>(E[0] * np, 0);
+    // O += N_odd·q
+    mad_w_cc(Q[0], Q[1], N[1], q, Q[0], Q[1]);
+#pragma unroll
+    for (int k = 1; k < L / 2; ++k) madc_w_cc(Q[2 * k], Q[2 * k + 1], N[2 * k + 1], q, Q[2 * k], Q[2 * k + 1]);
+    Zn = addc(Zn, 0u);
+    // E += N_even·q   (limb 0 of lane 0 becomes 0)
+    mad_w_cc(E[0], E[1], N[0], q, E[0], E[1]);
+#pragma unroll
+    for (int k = 1; k < L / 2; ++k) madc_w_cc(E[2 * k], E[2 * k + 1], N[2 * k], q, E[2 * k], E[2 * k + 1]);
+    Q[L - 1] = addc_cc(Q[L - 1], 0u);
+    Z = addc(Zn, 0u);
+}
+
+// Carry-lookahead across the instance's lanes: lane t adds 1 if a carry
+// reaches it.  g = lane generates a carry out, p = lane propagates (all ones).
+// Returns the carry out of the top lane.
+template <int L, int TPI>
+__device__ __forceinline__ uint32_t resolve_carries(uint32_t (&R)[L], uint32_t g) {
+    if constexpr (TPI == 1) {
+        return g;
+    } else {
+        bool all_ones = true;
+#pragma unroll
+        for (int k = 0; k < L; ++k) all_ones &= (R[k] == 0xffffffffu);
+        const uint32_t G = inst_ballot<TPI>(g != 0);
+        const uint32_t P = inst_ballot<TPI>(all_ones);
+        const uint64_t sum = (uint64_t)P + ((uint64_t)G << 1);
+        const uint32_t cin = (uint32_t)(sum ^ P);
+        if ((cin >> inst_lane<TPI>()) & 1u) {
+            R[0] = add_cc(R[0], 1u);
+#pragma unroll
+            for (int k = 1; k < L; ++k) R[k] = addc_cc(R[k], 0u);
+        }
+        return (uint32_t)(sum >> TPI) & 1u;
+    }
+}
+
+// Canonicalise: V = R + over·2^(32S) with V < 2M; return V mod M in R.
+template <int L, int TPI>
+__device__ __forceinline__ void final_sub(uint32_t (&R)[L], uint32_t over, const uint32_t (&N)[L]) {
+    uint32_t D[L];
+    D[0] = sub_cc(R[0], N[0]);
+#pragma unroll
+    for (int k = 1; k < L; ++k) D[k] = subc_cc(R[k], N[k]);
+    uint32_t bout = subc(0u, 0u) & 1u; // 1 when this lane borrowed
+    uint32_t top_borrow;
+    if constexpr (TPI == 1) {
+        top_borrow = bout;
+    } else {
+        bool zero = true;
+#pragma unroll
+        for (int k = 0; k < L; ++k) zero &= (D[k] == 0u);
+        const uint32_t G = inst_ballot<TPI>(bout != 0);
+        const uint32_t P = inst_ballot<TPI>(zero);
+        const uint64_t sum = (uint64_t)P + ((uint64_t)G << 1);
+        const uint32_t bin = (uint32_t)(sum ^ P);
+        if ((bin >> inst_lane<TPI>()) & 1u) {
+            D[0] = sub_cc(D[0], 1u);
+#pragma unroll
+            for (int k = 1; k < L; ++k) D[k] = subc_cc(D[k], 0u);
+        }
+        top_borrow = (uint32_t)(sum >> TPI) & 1u;
+    }
+    // V >= M  <=>  overflow word set, or R − N did not borrow out of the top
+    const bool ge = over != 0 || top_borrow == 0;
+#pragma unroll
+    for (int k = 0; k < L; ++k) R[k] = ge ? D[k] : R[k];
+}
+
+// r = A·B·2^(−32S) mod M.  A, N: this lane's L limbs; B: instance operand in
+// shared memory (store_b layout); np = −M⁻¹ mod 2^32.  r may alias A.
+template <int S, int TPI>
+__device__ __forceinline__ void mont_mul(uint32_t (&r)[S / TPI], const uint32_t (&A)[S / TPI],
+                                         const uint2 *sB, int NI, int inst,
+                                         const uint32_t (&N)[S / TPI], uint32_t np) {
+    constexpr int L = S / TPI;
+    uint32_t X[L], Y[L], Z = 0;
+    // pair 0: iteration 0 (E=X, fresh) and 1 (E=Y)
+    uint2 b = sB[inst];
+    cios_step<L, TPI>(X, Y, Z, A, N, b.x, np, true);
+    cios_step<L, TPI>(Y, X, Z, A, N, b.y, np, false);
+#pragma unroll 1
+    for (int i = 1; i < S / 2; ++i) {
+        b = sB[i * NI + inst];
+        cios_step<L, TPI>(X, Y, Z, A, N, b.x, np, false);
+        cios_step<L, TPI>(Y, X, Z, A, N, b.y, np, false);
+    }
+    // After the last step E = Y, raw = X.  Apply the final shift and merge:
+    // window limb k = X... no: E (=Y) is the old even array -> it shifts down,
+    // O (=X) becomes the even-aligned array.
+    const uint32_t u0 = from_above<TPI>(Y[0]);
+    uint32_t R[L];
+    R[0] = add_cc(X[0], Y[1]);
+#pragma unroll
+    for (int k = 1; k < L - 1; ++k) R[k] = addc_cc(X[k], Y[k + 1]);
+    R[L - 1] = addc_cc(X[L - 1], u0);
+    uint32_t C = addc(Z, 0u); // carry word at position t·L+L (into lane t+1)
+    uint32_t over;
+    if constexpr (TPI == 1) {
+        over = C;
+    } else {
+        const uint32_t cin = from_below<TPI>(C);
+        const uint32_t ctop = inst_bcast<TPI>(C, TPI - 1);
+        R[0] = add_cc(R[0], cin);
+#pragma unroll
+        for (int k = 1; k < L; ++k) R[k] = addc_cc(R[k], 0u);
+        uint32_t c2 = addc(0u, 0u);
+        uint32_t ripple = resolve_carries<L, TPI>(R, c2);
+        over = ctop + ripple;
+    }
+    final_sub<L, TPI>(R, over, N);
+#pragma unroll
+    for (int k = 0; k < L; ++k) r[k] = R[k];
+}
+
+// ---------------------------------------------------------------- global <-> lane limbs
+
+template <int S, int TPI>
+__device__ __forceinline__ void load_lane(uint32_t (&v)[S / TPI], const uint32_t *g) {
+    constexpr int L = S / TPI;
+    const uint32_t *p = g + inst_lane<TPI>() * L;
+    if constexpr (L % 4 == 0) {
+#pragma unroll
+        for (int k = 0; k < L / 4; ++k) {
+            uint4 w = reinterpret_cast<const uint4 *>(p)[k];
+            v[4 * k] = w.x;
+            v[4 * k + 1] = w.y;
+            v[4 * k + 2] = w.z;
+            v[4 * k + 3] = w.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < L / 2; ++k) {
+            uint2 w = reinterpret_cast<const uint2 *>(p)[k];
+            v[2 * k] = w.x;
+            v[2 * k + 1] = w.y;
+        }
+    }
+}
+
+template <int S, int TPI>
+__device__ __forceinline__ void store_lane(uint32_t *g, const uint32_t (&v)[S / TPI]) {
+    constexpr int L = S / TPI;
+    uint32_t *p = g + inst_lane<TPI>() * L;
+    if constexpr (L % 4 == 0) {
+#pragma unroll
+        for (int k = 0; k < L / 4; ++k)
+            reinterpret_cast<uint4 *>(p)[k] = make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < L / 2; ++k) reinterpret_cast<uint2 *>(p)[k] = make_uint2(v[2 * k], v[2 * k + 1]);
+    }
+}
+
+// lane limbs of a small constant (value v at limb 0)
+template <int L, int TPI>
+__device__ __forceinline__ void set_small(uint32_t (&r)[L], uint32_t v) {
+#pragma unroll
+    for (int k = 0; k < L; ++k) r[k] = 0;
+    if (inst_lane<TPI>() == 0) r[0] = v;
+}
+
+// instance-wide equality with a small constant
+template <int L, int TPI>
+__device__ __forceinline__ bool eq_small(const uint32_t (&r)[L], uint32_t v) {
+    bool ok = true;
+    const bool l0 = inst_lane<TPI>() == 0;
+#pragma unroll
+    for (int k = 0; k < L; ++k) ok &= (r[k] == ((l0 && k == 0) ? v : 0u));
+    return inst_ballot<TPI>(!ok) == 0;
+}
+
+} // namespace dev
+} // namespace sfxb

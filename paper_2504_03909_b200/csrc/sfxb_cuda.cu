@@ -1,0 +1,611 @@
+// libsfxb_cuda.so: key contexts, launch logic and the C ABI (include/sfxb_cuda.h).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/sfxb_cuda.h"
+#include "bignum_host.hpp"
+#include "ctx.hpp"
+#include "kernels.cuh"
+
+using namespace sfxb;
+using sfxb::host::Big;
+
+struct sfxb_ctx : CtxState {};
+struct sfxb_gh {
+    sfxb_ctx *ctx = nullptr;
+    uint32_t *d = nullptr; // 2·n_samples × 4s limbs, Montgomery form
+    uint32_t n_samples = 0;
+};
+
+namespace {
+
+thread_local std::string g_create_err;
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ApiError : std::runtime_error {
+    int code;
+    ApiError(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(x)                                                                                      \
+    do {                                                                                           \
+        cudaError_t e_ = (x);                                                                      \
+        if (e_ != cudaSuccess)                                                                     \
+            throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));                      \
+    } while (0)
+
+template <typename F>
+int guard(sfxb_ctx *ctx, F &&f) {
+    try {
+        f();
+        return SFXB_OK;
+    } catch (const ApiError &e) {
+        if (ctx) ctx->err = e.what();
+        return e.code;
+    } catch (const CudaError &e) {
+        if (ctx) ctx->err = e.what();
+        return SFXB_ERR_CUDA;
+    } catch (const std::exception &e) {
+        if (ctx) ctx->err = e.what();
+        return SFXB_ERR_ARG;
+    }
+}
+
+// --------------------------------------------------------------- device memory helpers
+
+template <typename T>
+T *dev_upload(CtxState &c, const T *h, size_t n) {
+    T *d = nullptr;
+    CK(cudaMalloc(&d, n * sizeof(T) + 16));
+    CK(cudaMemcpy(d, h, n * sizeof(T), cudaMemcpyHostToDevice));
+    c.owned.push_back(d);
+    return d;
+}
+uint32_t *dev_big(CtxState &c, const Big &v, size_t words) {
+    Big p = host::pad(v, words);
+    return dev_upload(c, p.data(), words);
+}
+DevMod dev_mod(CtxState &c, const Big &m, int S) {
+    host::MontHost mh(m, S);
+    std::vector<uint32_t> w(4 * (size_t)S);
+    std::copy(mh.m.begin(), mh.m.end(), w.begin());
+    std::copy(mh.r1.begin(), mh.r1.end(), w.begin() + S);
+    std::copy(mh.r2.begin(), mh.r2.end(), w.begin() + 2 * S);
+    std::copy(mh.r3.begin(), mh.r3.end(), w.begin() + 3 * S);
+    DevMod d;
+    d.w = dev_upload(c, w.data(), w.size());
+    d.np = mh.np;
+    d.S = S;
+    return d;
+}
+uint8_t *dev_digits(CtxState &c, const Big &e, int w, int &nd) {
+    std::vector<uint8_t> d = host::window_digits(e, w);
+    nd = (int)d.size();
+    return dev_upload(c, d.data(), d.size());
+}
+void *grow(Buf &b, size_t bytes) {
+    if (b.bytes < bytes) {
+        if (b.p) CK(cudaFree(b.p));
+        b.p = nullptr;
+        CK(cudaMalloc(&b.p, bytes));
+        b.bytes = bytes;
+    }
+    return b.p;
+}
+void *grow_pinned(Buf &b, size_t bytes) {
+    if (b.bytes < bytes) {
+        if (b.p) CK(cudaFreeHost(b.p));
+        b.p = nullptr;
+        CK(cudaMallocHost(&b.p, bytes));
+        b.bytes = bytes;
+    }
+    return b.p;
+}
+
+dev::ModArg arg(const DevMod &m) { return dev::ModArg{m.w, m.np}; }
+
+// --------------------------------------------------------------- size classes
+//
+// Tuned TPI (lanes per instance) per kernel and class.  S = limbs of the
+// modulus of that kernel: step1 s, step2 2s, histogram / ct-add 4s.
+template <int s>
+struct Cls;
+template <>
+struct Cls<4> {
+    static constexpr int T1 = 1, T2 = 1, TC = 1, TD = 1, TE = 1, TH = 1, TN = 1;
+};
+template <>
+struct Cls<8> {
+    static constexpr int T1 = 1, T2 = 1, TC = 2, TD = 1, TE = 2, TH = 2, TN = 2;
+};
+template <>
+struct Cls<16> {
+    static constexpr int T1 = 1, T2 = 2, TC = 2, TD = 2, TE = 2, TH = 2, TN = 2;
+};
+template <>
+struct Cls<32> {
+    static constexpr int T1 = 2, T2 = 2, TC = 4, TD = 2, TE = 4, TH = 4, TN = 4;
+};
+template <>
+struct Cls<48> {
+    static constexpr int T1 = 2, T2 = 4, TC = 8, TD = 4, TE = 8, TH = 8, TN = 8;
+};
+
+// grid.x for `items` work items spread over `rows` block rows (grid.y)
+template <typename K>
+int occupancy_grid(CtxState &c, K kernel, size_t items, int NI, int rows = 1) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, dev::kBlock, 0));
+    if (per_sm < 1) per_sm = 1;
+    size_t want = (items + (size_t)NI * rows - 1) / ((size_t)NI * rows);
+    size_t cap = std::max<size_t>(1, (size_t)c.sms * per_sm / rows);
+    if (want < 1) want = 1;
+    return (int)std::min(want, cap);
+}
+
+template <typename Fn>
+void dispatch_class(int s, Fn &&fn) {
+    switch (s) {
+    case 4: fn(std::integral_constant<int, 4>{}); break;
+    case 8: fn(std::integral_constant<int, 8>{}); break;
+    case 16: fn(std::integral_constant<int, 16>{}); break;
+    case 32: fn(std::integral_constant<int, 32>{}); break;
+    case 48: fn(std::integral_constant<int, 48>{}); break;
+    default: throw ApiError(SFXB_ERR_UNSUPPORTED, "unsupported key size class");
+    }
+}
+
+void check_launch(CtxState &c) {
+    CK(cudaGetLastError());
+    c.launches++;
+}
+
+// --------------------------------------------------------------- encrypt
+
+void encrypt_dev(sfxb_ctx *c, const int64_t *d_q, const uint32_t *d_r, size_t count,
+                 uint32_t *d_out, uint8_t *d_flags) {
+    if (count == 0) return;
+    const int s = c->s;
+    const size_t S2 = 2 * (size_t)s, S4 = 4 * (size_t)s;
+    dev::EncArgs a{};
+    a.r = d_r;
+    a.qfix = d_q;
+    a.count = count;
+    a.mod_n2 = arg(c->mod_n2);
+    a.dig_n = c->d_dig_n;
+    a.nd_n = c->nd_n;
+    a.n4 = c->d_n4;
+    a.nR_n2 = c->d_nR_n2;
+    a.out = d_out;
+    a.flags = d_flags;
+    uint32_t *status = (uint32_t *)grow(c->tmp[3], 64);
+    CK(cudaMemsetAsync(status, 0, 4, c->stream));
+    a.status = status;
+    if (c->has_priv) {
+        for (int i = 0; i < 2; ++i) {
+            a.mod_pq[i] = arg(c->mod_pq[i]);
+            a.mod_pq2[i] = arg(c->mod_pq2[i]);
+            a.dig_e1[i] = c->d_dig_e1[i];
+            a.nd_e1[i] = c->nd_e1[i];
+            a.dig_pq[i] = c->d_dig_pq[i];
+            a.nd_pq[i] = c->nd_pq[i];
+        }
+        a.q2R_n2 = c->d_q2R_n2;
+        a.qq_inv_m = c->d_qq_inv_m;
+        a.x = (uint32_t *)grow(c->tmp[0], count * 2 * S2 * 4);
+        a.y = (uint32_t *)grow(c->tmp[1], count * 2 * S2 * 4);
+    } else {
+        a.y = (uint32_t *)grow(c->tmp[1], count * S4 * 4);
+    }
+    dispatch_class(s, [&](auto sc) {
+        constexpr int cs = decltype(sc)::value;
+        using C = Cls<cs>;
+        if (c->has_priv) {
+            {
+                auto k = dev::k_enc_step1<cs, C::T1, kWindow>;
+                constexpr int NI = dev::kBlock / C::T1;
+                int grid = occupancy_grid(*c, k, 2 * count, NI, 2);
+                a.scratch = (uint32_t *)grow(c->scratch_table, 2 * (size_t)grid * NI * ((size_t)cs << kWindow) * 4);
+                k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(a);
+                check_launch(*c);
+            }
+            {
+                auto k = dev::k_enc_step2<2 * cs, C::T2, kWindow>;
+                constexpr int NI = dev::kBlock / C::T2;
+                int grid = occupancy_grid(*c, k, 2 * count, NI, 2);
+                a.scratch = (uint32_t *)grow(c->scratch_table, 2 * (size_t)grid * NI * ((size_t)(2 * cs) << kWindow) * 4);
+                k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(a);
+                check_launch(*c);
+            }
+        } else {
+            auto k = dev::k_pow_n2<4 * cs, C::TN, kWindowN>;
+            constexpr int NI = dev::kBlock / C::TN;
+            int grid = occupancy_grid(*c, k, count, NI);
+            a.scratch = (uint32_t *)grow(c->scratch_table, (size_t)grid * NI * ((size_t)(4 * cs) << kWindowN) * 4);
+            k<<<grid, dev::kBlock, 0, c->stream>>>(a);
+            check_launch(*c);
+        }
+        {
+            auto k = dev::k_enc_combine<cs, C::TC>;
+            constexpr int NI = dev::kBlock / C::TC;
+            int grid = occupancy_grid(*c, k, count, NI);
+            k<<<grid, dev::kBlock, 0, c->stream>>>(a, c->has_priv ? 1 : 0);
+            check_launch(*c);
+        }
+    });
+    uint32_t st = 0;
+    CK(cudaMemcpyAsync(&st, status, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (st & 1u) throw ApiError(SFXB_ERR_COPRIME, "encrypt: blinding factor not coprime to modulus");
+}
+
+// --------------------------------------------------------------- decrypt
+
+void decrypt_dev(sfxb_ctx *c, const uint32_t *d_cts, size_t count, uint32_t scale, double *d_values,
+                 uint32_t *d_plain, uint64_t *decryptions) {
+    if (!c->has_priv) throw ApiError(SFXB_ERR_AUTH, "decrypt requested without private key material");
+    if (count == 0) return;
+    if (count > 0xffffffffull) throw ApiError(SFXB_ERR_ARG, "decrypt: too many slots in one call");
+    const int s = c->s;
+    dev::DecArgs a{};
+    a.cts = d_cts;
+    a.count = count;
+    a.idx = (uint32_t *)grow(c->tmp[2], count * 4 + 64);
+    uint32_t *misc = (uint32_t *)grow(c->tmp[3], 64);
+    a.n_idx = misc + 1;
+    a.status = misc;
+    CK(cudaMemsetAsync(misc, 0, 8, c->stream));
+    for (int i = 0; i < 2; ++i) {
+        a.mod_pq[i] = arg(c->mod_pq[i]);
+        a.mod_pq2[i] = arg(c->mod_pq2[i]);
+        a.dig_m1[i] = c->d_dig_m1[i];
+        a.nd_m1[i] = c->nd_m1[i];
+        a.pinv[i] = c->d_pinv[i];
+        a.hR[i] = c->d_hR[i];
+    }
+    a.mod_n = arg(c->mod_n);
+    a.qinvR_p = c->d_qinvR_p;
+    a.qR_n = c->d_qR_n;
+    a.n2w = c->d_n2w;
+    a.nw = c->d_n;
+    a.mpq = (uint32_t *)grow(c->tmp[0], count * 2 * (size_t)s * 4);
+    a.values = d_values;
+    a.plain = d_plain;
+    a.scale = scale;
+    dispatch_class(s, [&](auto sc) {
+        constexpr int cs = decltype(sc)::value;
+        using C = Cls<cs>;
+        {
+            int grid = (int)std::min<size_t>((count + 255) / 256, (size_t)c->sms * 8);
+            dev::k_dec_scan<4 * cs><<<grid, 256, 0, c->stream>>>(a);
+            check_launch(*c);
+        }
+        uint32_t hst[2];
+        CK(cudaMemcpyAsync(hst, misc, 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (hst[0] & 2u) throw ApiError(SFXB_ERR_RANGE, "decrypt: ciphertext out of range");
+        const uint32_t n_items = hst[1];
+        if (decryptions) *decryptions += n_items;
+        if (n_items == 0) return;
+        {
+            auto k = dev::k_dec_step<cs, C::TD, kWindow>;
+            constexpr int NI = dev::kBlock / C::TD;
+            int grid = occupancy_grid(*c, k, 2 * (size_t)n_items, NI, 2);
+            a.scratch = (uint32_t *)grow(c->scratch_table, 2 * (size_t)grid * NI * ((size_t)(2 * cs) << kWindow) * 4);
+            k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(a, n_items);
+            check_launch(*c);
+        }
+        {
+            auto k = dev::k_dec_combine<cs, C::TE>;
+            constexpr int NI = dev::kBlock / C::TE;
+            int grid = occupancy_grid(*c, k, n_items, NI);
+            k<<<grid, dev::kBlock, 0, c->stream>>>(a, n_items);
+            check_launch(*c);
+        }
+        CK(cudaMemcpyAsync(hst, misc, 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (hst[0] & 4u) throw ApiError(SFXB_ERR_COPRIME, "decrypt: ciphertext not coprime to modulus");
+    });
+}
+
+// --------------------------------------------------------------- ct add
+
+void add_dev(sfxb_ctx *c, const uint32_t *d_a, const uint32_t *d_b, size_t count, uint32_t *d_out) {
+    if (count == 0) return;
+    dispatch_class(c->s, [&](auto sc) {
+        constexpr int cs = decltype(sc)::value;
+        using C = Cls<cs>;
+        auto k = dev::k_mulmod<4 * cs, C::TH>;
+        constexpr int NI = dev::kBlock / C::TH;
+        int grid = occupancy_grid(*c, k, count, NI);
+        k<<<grid, dev::kBlock, 0, c->stream>>>(arg(c->mod_n2), d_a, d_b, d_out, count);
+        check_launch(*c);
+    });
+}
+
+// --------------------------------------------------------------- host <-> padded layouts
+
+// copy `count` values of `words` limbs into a padded device layout of `stride`
+void h2d_padded(sfxb_ctx *c, uint32_t *d, const uint32_t *h, size_t count, size_t words, size_t stride) {
+    if (words == stride) {
+        CK(cudaMemcpyAsync(d, h, count * words * 4, cudaMemcpyHostToDevice, c->stream));
+        return;
+    }
+    std::vector<uint32_t> tmp(count * stride, 0u);
+    for (size_t i = 0; i < count; ++i) std::memcpy(&tmp[i * stride], h + i * words, words * 4);
+    CK(cudaMemcpyAsync(d, tmp.data(), tmp.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+}
+void d2h_padded(sfxb_ctx *c, uint32_t *h, const uint32_t *d, size_t count, size_t words, size_t stride) {
+    if (words == stride) {
+        CK(cudaMemcpyAsync(h, d, count * words * 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return;
+    }
+    std::vector<uint32_t> tmp(count * stride);
+    CK(cudaMemcpyAsync(tmp.data(), d, tmp.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < count; ++i) std::memcpy(h + i * words, &tmp[i * stride], words * 4);
+}
+
+template <typename T>
+struct DevBuf {
+    T *p = nullptr;
+    explicit DevBuf(size_t n) { CK(cudaMalloc(&p, n * sizeof(T) + 16)); }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+};
+
+} // namespace
+
+// =================================================================== C ABI
+
+extern "C" {
+
+const char *sfxb_create_error(void) { return g_create_err.c_str(); }
+
+int sfxb_ctx_create(sfxb_ctx **out, int device, const uint32_t *n, uint32_t n_words, const uint32_t *p,
+                    const uint32_t *q, uint32_t pq_words) {
+    if (!out || !n || n_words == 0) {
+        g_create_err = "sfxb_ctx_create: bad arguments";
+        return SFXB_ERR_ARG;
+    }
+    auto c = std::make_unique<sfxb_ctx>();
+    int rc = guard(c.get(), [&] {
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        if (device < 0 || device >= ndev) throw ApiError(SFXB_ERR_CUDA, "no such CUDA device");
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10) throw ApiError(SFXB_ERR_CUDA, "libsfxb_cuda is built for sm_100a only");
+        CK(cudaSetDevice(device));
+        c->device = device;
+        c->sms = prop.multiProcessorCount;
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+
+        Big N = host::from_words(n, n_words);
+        if ((N[0] & 1u) == 0 || host::bit_length(N) < 3) throw ApiError(SFXB_ERR_ARG, "modulus must be odd and > 4");
+        const uint32_t nw = (uint32_t)((host::bit_length(N) + 31) / 32);
+        int s = nw <= 8 ? 4 : nw <= 16 ? 8 : nw <= 32 ? 16 : nw <= 64 ? 32 : nw <= 96 ? 48 : 0;
+        if (!s) throw ApiError(SFXB_ERR_UNSUPPORTED, "modulus wider than 3072 bits");
+        c->s = s;
+        c->nw = nw;
+        c->n = N;
+        c->n2 = host::mul(N, N);
+        // key_id_of(n): FNV-1a over lower-case hex (he.cpp:30-38)
+        {
+            static const char *hex = "0123456789abcdef";
+            std::string digits;
+            size_t nb = host::bit_length(N);
+            for (size_t i = (nb + 3) / 4; i-- > 0;) {
+                uint32_t v = (N[i / 8] >> (4 * (i % 8))) & 0xf;
+                digits.push_back(hex[v]);
+            }
+            uint64_t h = 14695981039346656037ULL;
+            for (unsigned char ch : digits) {
+                h ^= ch;
+                h *= 1099511628211ULL;
+            }
+            c->key_id = h;
+        }
+        c->mod_n2 = dev_mod(*c, c->n2, 4 * s);
+        c->mod_n = dev_mod(*c, N, 2 * s);
+        c->d_n = dev_big(*c, N, 2 * s);
+        c->d_n4 = dev_big(*c, N, 4 * s);
+        c->d_n2w = dev_big(*c, c->n2, 4 * s);
+        host::MontHost mn2(c->n2, 4 * s);
+        c->d_nR_n2 = dev_big(*c, mn2.to_mont(N), 4 * s);
+        c->d_dig_n = dev_digits(*c, N, kWindowN, c->nd_n);
+        if (p && q && pq_words) {
+            Big P = host::from_words(p, pq_words), Q = host::from_words(q, pq_words);
+            if (host::cmp(host::mul(P, Q), N) != 0) throw ApiError(SFXB_ERR_ARG, "private key inconsistent: p·q != n");
+            if (host::cmp(P, Q) == 0) throw ApiError(SFXB_ERR_ARG, "primes must be distinct");
+            if ((P[0] & 1u) == 0 || (Q[0] & 1u) == 0) throw ApiError(SFXB_ERR_ARG, "primes must be odd");
+            if (host::bit_length(P) > 32u * s || host::bit_length(Q) > 32u * s)
+                throw ApiError(SFXB_ERR_UNSUPPORTED, "unbalanced primes are outside the CRT size class");
+            // q < 2p and p < 2q keep the single conditional subtractions of the CRT combine exact
+            if (host::cmp(Q, host::add(P, P)) >= 0 || host::cmp(P, host::add(Q, Q)) >= 0)
+                throw ApiError(SFXB_ERR_UNSUPPORTED, "primes differ by more than a factor of two");
+            c->has_priv = true;
+            c->p = P;
+            c->q = Q;
+            const Big PQ[2] = {P, Q};
+            for (int i = 0; i < 2; ++i) {
+                const Big &pr = PQ[i], &ot = PQ[1 - i];
+                Big pr2 = host::mul(pr, pr);
+                c->mod_pq[i] = dev_mod(*c, pr, s);
+                c->mod_pq2[i] = dev_mod(*c, pr2, 2 * s);
+                Big pm1 = host::sub(pr, host::from_u64(1));
+                c->d_dig_e1[i] = dev_digits(*c, host::mod(ot, pm1), kWindow, c->nd_e1[i]);
+                c->d_dig_pq[i] = dev_digits(*c, pr, kWindow, c->nd_pq[i]);
+                c->d_dig_m1[i] = dev_digits(*c, pm1, kWindow, c->nd_m1[i]);
+                c->d_pinv[i] = dev_big(*c, host::inv_pow2(pr, s), s);
+                // h = (−other mod prime)^-1 mod prime, in Montgomery form
+                Big negot = host::sub(pr, host::mod(ot, pr));
+                Big h = host::inv_mod_prime(negot, pr, s);
+                host::MontHost mp(pr, s);
+                c->d_hR[i] = dev_big(*c, mp.to_mont(h), s);
+            }
+            host::MontHost mp(P, s), mp2(host::mul(P, P), 2 * s), mn(N, 2 * s);
+            Big P2 = host::mul(P, P), Q2 = host::mul(Q, Q);
+            // (q²)^-1 mod p² = q²^(p(p−1)−1) mod p²  (Euler)
+            Big phi = host::mul(P, host::sub(P, host::from_u64(1)));
+            Big qq_inv = mp2.pow(host::mod(Q2, P2), host::sub(phi, host::from_u64(1)));
+            c->d_qq_inv_m = dev_big(*c, mp2.to_mont(qq_inv), 2 * s);
+            c->d_q2R_n2 = dev_big(*c, mn2.to_mont(Q2), 4 * s);
+            Big qinv = host::inv_mod_prime(host::mod(Q, P), P, s);
+            c->d_qinvR_p = dev_big(*c, mp.to_mont(qinv), s);
+            c->d_qR_n = dev_big(*c, mn.to_mont(Q), 2 * s);
+        }
+        CK(cudaDeviceSynchronize());
+    });
+    if (rc != SFXB_OK) {
+        g_create_err = c->err;
+        for (void *d : c->owned) cudaFree(d);
+        if (c->stream) cudaStreamDestroy(c->stream);
+        return rc;
+    }
+    *out = c.release();
+    return SFXB_OK;
+}
+
+void sfxb_ctx_destroy(sfxb_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (void *d : c->owned) cudaFree(d);
+    if (c->scratch_table.p) cudaFree(c->scratch_table.p);
+    for (auto &b : c->tmp)
+        if (b.p) cudaFree(b.p);
+    for (auto &b : c->host_pinned)
+        if (b.p) cudaFreeHost(b.p);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char *sfxb_last_error(const sfxb_ctx *c) { return c ? c->err.c_str() : "null context"; }
+uint32_t sfxb_ctx_n_words(const sfxb_ctx *c) { return c->nw; }
+uint32_t sfxb_ctx_ct_words(const sfxb_ctx *c) { return 2 * c->nw; }
+int sfxb_ctx_has_private(const sfxb_ctx *c) { return c->has_priv ? 1 : 0; }
+uint64_t sfxb_ctx_key_id(const sfxb_ctx *c) { return c->key_id; }
+uint64_t sfxb_ctx_launches(const sfxb_ctx *c) { return c->launches; }
+void *sfxb_ctx_stream(sfxb_ctx *c) { return (void *)c->stream; }
+int sfxb_ctx_sync(sfxb_ctx *c) {
+    return guard(c, [&] { CK(cudaStreamSynchronize(c->stream)); });
+}
+
+int sfxb_encode_check(sfxb_ctx *c, double x, uint32_t scale, int64_t *q_out) {
+    return guard(c, [&] {
+        // encode_fixed (he.cpp:125-136) + fixed_encode_ll (fixed_point.hpp:13-15)
+        if (!std::isfinite(x)) throw ApiError(SFXB_ERR_RANGE, "encode_fixed: value must be finite");
+        if (std::abs(x) >= std::ldexp(1.0, (int)(62 - scale)))
+            throw ApiError(SFXB_ERR_RANGE, "encode_fixed: value too large for the fixed-point grid");
+        int64_t qv = std::llround(std::ldexp(x, (int)scale));
+        uint64_t mag = qv < 0 ? (uint64_t)(-(qv + 1)) + 1u : (uint64_t)qv;
+        Big twice = host::add(host::from_u64(mag), host::from_u64(mag));
+        if (host::cmp(twice, c->n) >= 0)
+            throw ApiError(SFXB_ERR_RANGE, "encode_fixed: |x|·2^scale_bits must stay below n/2");
+        *q_out = qv;
+    });
+}
+
+int sfxb_encrypt_dev(sfxb_ctx *c, const int64_t *d_q, const uint32_t *d_r, size_t count, uint32_t *d_out,
+                     uint8_t *d_flags) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        encrypt_dev(c, d_q, d_r, count, d_out, d_flags);
+    });
+}
+
+int sfxb_encrypt(sfxb_ctx *c, const int64_t *q_fixed, const uint32_t *r, size_t count, uint32_t *out_cts,
+                 uint8_t *r_flags) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (count == 0) return;
+        const size_t Sn = 2 * (size_t)c->s, S4 = 4 * (size_t)c->s;
+        // range checks of encrypt_with_r (he.cpp:88-89) on the blinding factors
+        for (size_t i = 0; i < count; ++i) {
+            const uint32_t *ri = r + i * c->nw;
+            bool small = true;
+            for (uint32_t k = 1; k < c->nw; ++k) small &= ri[k] == 0;
+            if (small && ri[0] < 1) throw ApiError(SFXB_ERR_RANGE, "encrypt: blinding factor out of range");
+            if (host::cmp(host::from_words(ri, c->nw), c->n) >= 0)
+                throw ApiError(SFXB_ERR_RANGE, "encrypt: blinding factor out of range");
+        }
+        DevBuf<int64_t> dq(count);
+        DevBuf<uint32_t> dr(count * Sn), dout(count * S4);
+        DevBuf<uint8_t> dflags(count);
+        CK(cudaMemsetAsync(dflags.p, 0, count, c->stream));
+        CK(cudaMemcpyAsync(dq.p, q_fixed, count * 8, cudaMemcpyHostToDevice, c->stream));
+        h2d_padded(c, dr.p, r, count, c->nw, Sn);
+        int st = SFXB_OK;
+        try {
+            encrypt_dev(c, dq.p, dr.p, count, dout.p, dflags.p);
+        } catch (const ApiError &e) {
+            if (e.code != SFXB_ERR_COPRIME) throw;
+            st = e.code;
+            c->err = e.what();
+        }
+        if (r_flags) {
+            CK(cudaMemcpyAsync(r_flags, dflags.p, count, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+        }
+        if (st != SFXB_OK) throw ApiError(st, c->err);
+        d2h_padded(c, out_cts, dout.p, count, 2 * c->nw, S4);
+    });
+}
+
+int sfxb_add(sfxb_ctx *c, const uint32_t *a, const uint32_t *b, size_t count, uint32_t *out) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (count == 0) return;
+        const size_t S4 = 4 * (size_t)c->s, cw = 2 * c->nw;
+        for (size_t i = 0; i < count; ++i)
+            if (host::cmp(host::from_words(a + i * cw, cw), c->n2) >= 0 ||
+                host::cmp(host::from_words(b + i * cw, cw), c->n2) >= 0)
+                throw ApiError(SFXB_ERR_RANGE, "add_ciphertexts: ciphertext out of range");
+        DevBuf<uint32_t> da(count * S4), db(count * S4), dout(count * S4);
+        h2d_padded(c, da.p, a, count, cw, S4);
+        h2d_padded(c, db.p, b, count, cw, S4);
+        add_dev(c, da.p, db.p, count, dout.p);
+        d2h_padded(c, out, dout.p, count, cw, S4);
+    });
+}
+
+int sfxb_decrypt_dev(sfxb_ctx *c, const uint32_t *d_cts, size_t count, uint32_t scale, double *d_values,
+                     uint32_t *d_plain, uint64_t *decryptions) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        decrypt_dev(c, d_cts, count, scale, d_values, d_plain, decryptions);
+    });
+}
+
+int sfxb_decrypt(sfxb_ctx *c, const uint32_t *cts, size_t count, uint32_t scale, double *out_values,
+                 uint32_t *out_plain, uint64_t *decryptions) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (!c->has_priv) throw ApiError(SFXB_ERR_AUTH, "decrypt requested without private key material");
+        if (count == 0) return;
+        const size_t Sn = 2 * (size_t)c->s, S4 = 4 * (size_t)c->s;
+        DevBuf<uint32_t> dc(count * S4), dplain(out_plain ? count * Sn : 1);
+        DevBuf<double> dv(count);
+        h2d_padded(c, dc.p, cts, count, 2 * c->nw, S4);
+        decrypt_dev(c, dc.p, count, scale, dv.p, out_plain ? dplain.p : nullptr, decryptions);
+        CK(cudaMemcpyAsync(out_values, dv.p, count * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (out_plain) d2h_padded(c, out_plain, dplain.p, count, c->nw, Sn);
+    });
+}
+
+} // extern "C"

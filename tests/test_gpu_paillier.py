@@ -1,0 +1,158 @@
+"""GPU parity: encrypt / ct-add / decrypt through the C ABI against the oracle
+and the reference's golden vectors (bit-exact; decrypted doubles compared
+bitwise).  Reference behaviour pinned: he.cpp:87-143, test_he.cpp:22-41."""
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+from keys import key
+from paper_2504_03909_b200 import _lib
+from py_oracle import Oracle, OracleKey, from_words, ints_to_words, words_to_ints
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def golden(name):
+    with open(os.path.join(HERE, "golden", f"plugin_{name}.json")) as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    return Oracle()
+
+
+def ctx_for(name, private=True):
+    n, p, q = key(name)
+    return _lib.Context(n, p, q) if private else _lib.Context(n)
+
+
+def test_toy_known_answers():
+    # test_he.cpp:22-41: n=35, Enc(0, r=2) = 18, Dec(Enc(3,4)·Enc(4,9)) = 7
+    ctx = _lib.Context(35, 5, 7)
+    c = ctx.encrypt(np.array([0], np.int64), np.array([[2]], np.uint32))
+    assert from_words(c[0]) == 18
+    c3 = ctx.encrypt(np.array([3], np.int64), np.array([[4]], np.uint32))
+    c4 = ctx.encrypt(np.array([4], np.int64), np.array([[9]], np.uint32))
+    s = ctx.add(c3, c4)
+    assert from_words(s[0]) == (from_words(c3[0]) * from_words(c4[0])) % 1225
+    vals, decs, plain = ctx.decrypt(s, scale=0, want_plain=True)
+    assert from_words(plain[0]) == 7 and vals[0] == 7.0 and decs == 1
+    # Dec(trivial zero) = 0, not counted (secure_processor.cpp:734-738)
+    vals, decs = ctx.decrypt(np.array([[1, 0]], np.uint32))
+    assert vals[0] == 0.0 and decs == 0
+    with pytest.raises(_lib.SfxbError, match="not coprime"):
+        ctx.encrypt(np.array([3], np.int64), np.array([[5]], np.uint32))
+    with pytest.raises(_lib.SfxbError, match="out of range"):
+        ctx.encrypt(np.array([3], np.int64), np.array([[35]], np.uint32))
+
+
+@pytest.mark.parametrize("kname", ["k512_c0ffee", "k2048_7"])
+def test_encrypt_matches_reference_golden(kname):
+    g = golden(kname)
+    n, p, q = key(kname)
+    ctx = _lib.Context(n, p, q)
+    nw = ctx.nw
+    r = ints_to_words([int(x, 16) for x in g["r_stream"]], nw)
+    gh = np.array(g["fixture4"]["inputs"]["gh"], np.float64).reshape(-1)
+    qf = np.array([ctx.encode_check(x) for x in gh], np.int64)
+    cts = ctx.encrypt(qf, r[: len(qf)])
+    want = [int(x, 16) for x in g["fixture4"]["cts"]]
+    assert words_to_ints(cts) == want
+
+
+@pytest.mark.parametrize("kname", ["k512_c0ffee", "k1024_7", "k2048_7", "k3072_7"])
+def test_encrypt_random_matches_oracle(oracle, kname):
+    n, p, q = key(kname)
+    ok = OracleKey(oracle, n, p, q)
+    rng = random.Random(kname)
+    count = 24
+    qs = [rng.randrange(-(1 << 62), 1 << 62) for _ in range(count)]
+    qs[:4] = [0, 1, -1, -(1 << 62)]
+    rs = [rng.randrange(2, n) for _ in range(count)]
+    for pub_only in (False, True):
+        ctx = _lib.Context(n) if pub_only else _lib.Context(n, p, q)
+        cts = ctx.encrypt(np.array(qs, np.int64), ints_to_words(rs, ctx.nw))
+        got = words_to_ints(cts)
+        for i in range(count):
+            m = qs[i] % n
+            assert got[i] == ok.encrypt_with_r(m, rs[i]), (kname, pub_only, i)
+
+
+@pytest.mark.parametrize("kname", ["k512_c0ffee", "k2048_7"])
+def test_add_matches_python(kname):
+    n, p, q = key(kname)
+    ctx = _lib.Context(n)
+    rng = random.Random(5)
+    a = [rng.randrange(1, n * n) for _ in range(40)]
+    b = [rng.randrange(1, n * n) for _ in range(40)]
+    out = ctx.add(ints_to_words(a, ctx.ct_words), ints_to_words(b, ctx.ct_words))
+    assert words_to_ints(out) == [(x * y) % (n * n) for x, y in zip(a, b)]
+
+
+@pytest.mark.parametrize("kname", ["k512_c0ffee", "k1024_7", "k2048_7", "k3072_7"])
+def test_decrypt_random_matches_oracle(oracle, kname):
+    n, p, q = key(kname)
+    ok = OracleKey(oracle, n, p, q)
+    ctx = _lib.Context(n, p, q)
+    rng = random.Random(kname + "dec")
+    cts = []
+    for i in range(20):
+        while True:
+            c = rng.randrange(2, n * n)
+            if c % p and c % q:
+                break
+        cts.append(c)
+    vals, decs, plain = ctx.decrypt(ints_to_words(cts, ctx.ct_words), want_plain=True)
+    assert decs == len(cts)
+    want_m = [ok.decrypt(c) for c in cts]
+    assert words_to_ints(plain) == want_m
+    for i, m in enumerate(want_m):
+        w = ok.decode_fixed(m)
+        assert vals[i] == w or (np.isnan(w) and np.isnan(vals[i])), (i, vals[i], w)
+
+
+@pytest.mark.parametrize("kname", ["k512_c0ffee", "k2048_7"])
+def test_decrypt_golden_slots(kname):
+    g = golden(kname)
+    n, p, q = key(kname)
+    ctx = _lib.Context(n, p, q)
+    for fx in ("fixture4", "random50"):
+        slots = ints_to_words([int(x, 16) for x in g[fx]["slots"]], ctx.ct_words)
+        vals, decs = ctx.decrypt(slots)
+        want = np.array([float.fromhex(x) for x in g[fx]["values"]])
+        assert np.array_equal(vals, want)
+        assert decs == g[fx]["counters"][2] - g[fx]["counters_after_accumulate"][2]
+
+
+def test_decrypt_errors():
+    n, p, q = key("k512_c0ffee")
+    pub = _lib.Context(n)
+    with pytest.raises(_lib.AuthorizationError, match="without private key material"):
+        pub.decrypt(np.zeros((1, pub.ct_words), np.uint32))
+    ctx = _lib.Context(n, p, q)
+    with pytest.raises(_lib.SfxbError, match="out of range"):
+        ctx.decrypt(np.zeros((1, ctx.ct_words), np.uint32))
+    with pytest.raises(_lib.SfxbError, match="not coprime"):
+        ctx.decrypt(_lib.to_words(n, ctx.ct_words)[None, :])
+
+
+def test_decode_truncates_like_mpz_get_d(oracle):
+    # decode_fixed (he.cpp:138-143): mpz_get_d truncates toward zero
+    n, p, q = key("k2048_7")
+    ok = OracleKey(oracle, n, p, q)
+    ctx = _lib.Context(n, p, q)
+    rng = random.Random(3)
+    ms = [(1 << 60) + 255, n - ((1 << 60) + 255), 0, 1, n - 1, (n - 1) // 2, (n + 1) // 2,
+          (1 << 64) - 1, (1 << 64), (1 << 64) + 1, rng.randrange(n), (1 << 200) + 12345]
+    rs = [rng.randrange(2, n) for _ in ms]
+    cts = [ok.encrypt_with_r(m, r) for m, r in zip(ms, rs)]
+    vals, _, plain = ctx.decrypt(ints_to_words(cts, ctx.ct_words), want_plain=True)
+    assert words_to_ints(plain) == ms
+    for m, v in zip(ms, vals):
+        w = ok.decode_fixed(m)
+        assert v == w or (np.isinf(v) and np.isinf(w) and (v > 0) == (w > 0)), (m, v, w)
