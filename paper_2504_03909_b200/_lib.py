@@ -198,6 +198,97 @@ class Context:
         return (vals, decs.value, plain) if want_plain else (vals, decs.value)
 
 
+class GhHandle:
+    """Device-resident gradient ciphertexts (sfxb_gh, Montgomery form)."""
+
+    def __init__(self, ctx: "Context", h):
+        self.ctx, self.h = ctx, h
+
+    def free(self):
+        if self.h:
+            self.ctx.lib.sfxb_gh_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _ptr(t) -> int:
+    """Device pointer of a torch tensor (plumbing only)."""
+    return int(t.data_ptr())
+
+
+class DeviceOps:
+    """Device-pointer entry points (`*_dev`) driven with torch tensors.
+
+    torch provides device memory and the stream order; every call syncs torch's
+    stream before enqueueing on the context stream and returns after the
+    context stream drained (tests/bench time their own regions)."""
+
+    def __init__(self, ctx: Context):
+        self.ctx = ctx
+        import torch
+
+        self.torch = torch
+
+    def _pre(self):
+        self.torch.cuda.synchronize()
+
+    def _post(self):
+        self.ctx._check(self.ctx.lib.sfxb_ctx_sync(self.ctx.h))
+
+    def gh_from_dev(self, d_gh, n_samples: int) -> GhHandle:
+        self._pre()
+        h = C.c_void_p()
+        self.ctx._check(self.ctx.lib.sfxb_gh_from_dev(self.ctx.h, _ptr(d_gh), n_samples, C.byref(h)))
+        return GhHandle(self.ctx, h)
+
+    def gh_upload(self, gh_cts) -> GhHandle:
+        gh_cts = np.ascontiguousarray(gh_cts, dtype=np.uint32)
+        h = C.c_void_p()
+        self.ctx._check(self.ctx.lib.sfxb_gh_upload(self.ctx.h, gh_cts.reshape(-1), gh_cts.shape[0] // 2, C.byref(h)))
+        return GhHandle(self.ctx, h)
+
+    def accumulate(self, gh: GhHandle, d_bins, n_features: int, d_offsets, n_nodes: int, d_rows, n_rows: int,
+                   n_bins: int, d_out, mont_out: bool = False, sync: bool = True) -> int:
+        if sync:
+            self._pre()
+        adds = C.c_uint64(0)
+        self.ctx._check(self.ctx.lib.sfxb_accumulate_dev(
+            self.ctx.h, gh.h, _ptr(d_bins), n_features, _ptr(d_offsets), n_nodes, _ptr(d_rows), n_rows, n_bins,
+            _ptr(d_out), 1 if mont_out else 0, C.byref(adds)))
+        if sync:
+            self._post()
+        return adds.value
+
+    def reduce_partials(self, d_parts, parts: int, n_slots: int, d_out, sync: bool = True):
+        if sync:
+            self._pre()
+        self.ctx._check(self.ctx.lib.sfxb_reduce_partials_dev(self.ctx.h, _ptr(d_parts), parts, n_slots, _ptr(d_out)))
+        if sync:
+            self._post()
+
+    def encrypt(self, d_q, d_r, count: int, d_out, sync: bool = True):
+        if sync:
+            self._pre()
+        self.ctx._check(self.ctx.lib.sfxb_encrypt_dev(self.ctx.h, _ptr(d_q), _ptr(d_r), count, _ptr(d_out), None))
+        if sync:
+            self._post()
+
+    def decrypt(self, d_cts, count: int, d_values, scale: int = 40, sync: bool = True) -> int:
+        if sync:
+            self._pre()
+        decs = C.c_uint64(0)
+        self.ctx._check(self.ctx.lib.sfxb_decrypt_dev(self.ctx.h, _ptr(d_cts), count, scale, _ptr(d_values), None,
+                                                      C.byref(decs)))
+        if sync:
+            self._post()
+        return decs.value
+
+
 def imad_peak(device: int = 0):
     lib = load()
     p, clk = C.c_double(), C.c_double()

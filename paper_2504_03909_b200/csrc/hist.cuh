@@ -1,0 +1,231 @@
+// K2: encrypted histogram (PaillierPlugin::accumulate_rows,
+// secure_processor.cpp:587-620) as a segmented modular product.
+//
+//   1. key(i, f) = (node(i)·J + f)·K + bins[f][rows[i]]   (slot pair index)
+//      counting sort of the frontier's (row, feature) items by key
+//   2. pass 1: every key's rows are cut into pieces of ≤ C items; one
+//      instance multiplies a piece (Montgomery form, gathered from the
+//      resident gh ciphertexts), for G and H separately
+//   3. pass k>1: the same over the previous pass's partials until each key
+//      has one partial
+//   4. finalize: plain form (or Montgomery for multi-GPU partials); empty
+//      slots are the literal 1 (trivial_zero, he.cpp:123)
+// Products mod n² are unique residues, so any grouping/order is bit-exact.
+#pragma once
+#include "kernels.cuh"
+
+namespace sfxb {
+namespace dev {
+
+// position -> frontier node (one block per node)
+__global__ void k_node_of(const uint32_t *offsets, uint32_t *node_of) {
+    const uint32_t nd = blockIdx.x;
+    for (uint32_t i = offsets[nd] + threadIdx.x; i < offsets[nd + 1]; i += blockDim.x) node_of[i] = nd;
+}
+
+// per (gh row) flags: bit0 = Enc(g) == 1, bit1 = Enc(h) == 1 (trivial zeros are
+// skipped by fold_into and not counted, secure_processor.cpp:724-732)
+template <int S4>
+__global__ void k_gh_flags(const uint32_t *gh_plain, uint32_t n_samples, int ct_words, uint8_t *flags) {
+    for (size_t r = (size_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_samples; r += (size_t)gridDim.x * blockDim.x) {
+        uint8_t f = 0;
+        for (int g = 0; g < 2; ++g) {
+            const uint32_t *c = gh_plain + (2 * r + g) * S4;
+            bool one = c[0] == 1u;
+            for (int k = 1; k < ct_words; ++k) one &= c[k] == 0u;
+            f |= one ? (uint8_t)(1u << g) : (uint8_t)0;
+        }
+        flags[r] = f;
+    }
+}
+
+struct HistArgs {
+    const uint32_t *rows;
+    uint32_t n_rows;
+    const uint32_t *node_of;
+    const uint16_t *bins;
+    uint32_t n_samples;
+    uint32_t J, K;
+    const uint8_t *gh_flags; // may be null
+    uint32_t *count;         // N·J·K
+    uint32_t *ones;          // N·J·K·2 (may be null)
+    uint32_t *cursor;        // N·J·K
+    const uint32_t *seg_start;
+    uint32_t *sorted;        // n_rows·J
+    uint32_t *status;        // bit0 bin out of range, bit1 row out of range
+};
+
+__global__ void k_hist_count(HistArgs a) {
+    const size_t total = (size_t)a.n_rows * a.J;
+    for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t f = (uint32_t)(t / a.n_rows), i = (uint32_t)(t % a.n_rows);
+        const uint32_t row = a.rows[i];
+        if (row >= a.n_samples) {
+            atomicOr(a.status, 2u);
+            continue;
+        }
+        const uint32_t b = a.bins[(size_t)f * a.n_samples + row];
+        if (b >= a.K) {
+            atomicOr(a.status, 1u);
+            continue;
+        }
+        const size_t key = ((size_t)a.node_of[i] * a.J + f) * a.K + b;
+        atomicAdd(a.count + key, 1u);
+        if (a.gh_flags) {
+            const uint8_t fl = a.gh_flags[row];
+            if (fl & 1u) atomicAdd(a.ones + 2 * key, 1u);
+            if (fl & 2u) atomicAdd(a.ones + 2 * key + 1, 1u);
+        }
+    }
+}
+
+__global__ void k_hist_scatter(HistArgs a) {
+    const size_t total = (size_t)a.n_rows * a.J;
+    for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t f = (uint32_t)(t / a.n_rows), i = (uint32_t)(t % a.n_rows);
+        const uint32_t row = a.rows[i];
+        const uint32_t b = a.bins[(size_t)f * a.n_samples + row];
+        const size_t key = ((size_t)a.node_of[i] * a.J + f) * a.K + b;
+        const uint32_t pos = a.seg_start[key] + atomicAdd(a.cursor + key, 1u);
+        a.sorted[pos] = row;
+    }
+}
+
+// Σ_keys,g max(count − ones − 1, 0)
+__global__ void k_hist_adds(const uint32_t *count, const uint32_t *ones, size_t nkeys,
+                            unsigned long long *adds) {
+    unsigned long long local = 0;
+    for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < nkeys; k += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t c = count[k];
+        for (int g = 0; g < 2; ++g) {
+            const uint32_t real = c - (ones ? ones[2 * k + g] : 0u);
+            local += real > 0 ? real - 1 : 0;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(adds, local);
+}
+
+// pieces of ≤ C items per segment: npieces[k] = ceil(len[k] / C)
+__global__ void k_npieces(const uint32_t *seg_len, size_t nkeys, uint32_t C, uint32_t *np) {
+    for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < nkeys; k += (size_t)gridDim.x * blockDim.x)
+        np[k] = (seg_len[k] + C - 1) / C;
+}
+
+struct Piece {
+    uint32_t start, len;
+};
+
+__global__ void k_emit_pieces(const uint32_t *seg_start, const uint32_t *seg_len, const uint32_t *piece_start,
+                              size_t nkeys, uint32_t C, Piece *pieces) {
+    for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < nkeys; k += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t len = seg_len[k], s0 = seg_start[k], p0 = piece_start[k];
+        for (uint32_t j = 0; j * C < len; ++j) pieces[p0 + j] = Piece{s0 + j * C, min(C, len - j * C)};
+    }
+}
+
+// Segmented product pass.  Job j = 2·piece + gh.  Item k of a piece is
+//   pass 1: gh[(2·sorted[start+k] + gh)·S]      (gather by row id)
+//   pass>1: prev[(start+k)·2 + gh]·S            (contiguous partials)
+// Every instance of a warp runs the same number of Montgomery products
+// (shorter pieces keep their accumulator), exiting when the warp is done.
+template <int S, int TPI, int C>
+__global__ void __launch_bounds__(kBlock) k_seg_prod(ModArg M, const Piece *pieces, size_t n_pieces,
+                                                     const uint32_t *sorted, const uint32_t *src,
+                                                     uint32_t *dst) {
+    constexpr int L = S / TPI, NI = kBlock / TPI;
+    __shared__ uint2 sB[S / 2 * NI];
+    const Stage st = make_stage<TPI>(sB);
+    const ModRef mr = M.ref();
+    uint32_t N[L];
+    load_const<S, TPI>(N, mr, kMod);
+    SFXB_UNIFORM_LOOP(job, active, 2 * n_pieces) {
+        const Piece pc = pieces[job >> 1];
+        const uint32_t g = (uint32_t)(job & 1);
+        auto item_ptr = [&](uint32_t k) -> const uint32_t * {
+            const size_t idx = sorted ? (2 * (size_t)sorted[pc.start + k] + g) : (2 * (size_t)(pc.start + k) + g);
+            return src + idx * S;
+        };
+        uint32_t acc[L], x[L];
+        load_lane<S, TPI>(acc, item_ptr(0));
+        for (int k = 1; k < C; ++k) {
+            const bool more = active && (uint32_t)k < pc.len;
+            if (!__any_sync(0xffffffffu, more)) break; // warp-uniform exit
+            load_lane<S, TPI>(x, item_ptr(more ? (uint32_t)k : 0u));
+            uint32_t r[L];
+            mmul<S, TPI>(r, acc, x, st, N, M.np);
+#pragma unroll
+            for (int w = 0; w < L; ++w) acc[w] = more ? r[w] : acc[w];
+        }
+        if (active) store_lane<S, TPI>(dst + job * S, acc);
+    }
+}
+
+// Output slot (key, gh): count == 0 -> literal 1 (or Montgomery one for
+// partials); else from_mont of the key's single final partial.
+template <int S, int TPI>
+__global__ void __launch_bounds__(kBlock) k_hist_finalize(ModArg M, const uint32_t *count, const uint32_t *final_idx,
+                                                          size_t nkeys, const uint32_t *partial, uint32_t *out,
+                                                          int mont_out) {
+    constexpr int L = S / TPI, NI = kBlock / TPI;
+    __shared__ uint2 sB[S / 2 * NI];
+    const Stage st = make_stage<TPI>(sB);
+    const ModRef mr = M.ref();
+    uint32_t N[L], one_m[L];
+    load_const<S, TPI>(N, mr, kMod);
+    load_const<S, TPI>(one_m, mr, kOne);
+    SFXB_UNIFORM_LOOP(slot, active, 2 * nkeys) {
+        const size_t key = slot >> 1;
+        const uint32_t g = (uint32_t)(slot & 1);
+        const bool empty = count[key] == 0;
+        uint32_t v[L];
+        if (!empty) load_lane<S, TPI>(v, partial + (2 * (size_t)final_idx[key] + g) * S);
+        else
+#pragma unroll
+            for (int w = 0; w < L; ++w) v[w] = one_m[w];
+        if (!mont_out) from_mont<S, TPI>(v, v, st, N, M.np); // Montgomery one -> 1
+        if (active) store_lane<S, TPI>(out + slot * S, v);
+    }
+}
+
+// x -> x·R mod M (any x < R)
+template <int S, int TPI>
+__global__ void __launch_bounds__(kBlock) k_to_mont(ModArg M, uint32_t *x, size_t count) {
+    constexpr int L = S / TPI, NI = kBlock / TPI;
+    __shared__ uint2 sB[S / 2 * NI];
+    const Stage st = make_stage<TPI>(sB);
+    const ModRef mr = M.ref();
+    uint32_t N[L];
+    load_const<S, TPI>(N, mr, kMod);
+    SFXB_UNIFORM_LOOP(e, active, count) {
+        uint32_t v[L];
+        load_lane<S, TPI>(v, x + e * S);
+        to_mont<S, TPI>(v, v, mr, st, N);
+        if (active) store_lane<S, TPI>(x + e * S, v);
+    }
+}
+
+// K4: out[i] = from_mont(∏_p parts[p][i]) for Montgomery-form partials
+template <int S, int TPI>
+__global__ void __launch_bounds__(kBlock) k_reduce_parts(ModArg M, const uint32_t *parts, uint32_t n_parts,
+                                                         size_t n_slots, uint32_t *out) {
+    constexpr int L = S / TPI, NI = kBlock / TPI;
+    __shared__ uint2 sB[S / 2 * NI];
+    const Stage st = make_stage<TPI>(sB);
+    const ModRef mr = M.ref();
+    uint32_t N[L];
+    load_const<S, TPI>(N, mr, kMod);
+    SFXB_UNIFORM_LOOP(e, active, n_slots) {
+        uint32_t acc[L], x[L];
+        load_lane<S, TPI>(acc, parts + e * S);
+        for (uint32_t p = 1; p < n_parts; ++p) {
+            load_lane<S, TPI>(x, parts + ((size_t)p * n_slots + e) * S);
+            mmul<S, TPI>(acc, acc, x, st, N, M.np);
+        }
+        from_mont<S, TPI>(acc, acc, st, N, M.np);
+        if (active) store_lane<S, TPI>(out + e * S, acc);
+    }
+}
+
+} // namespace dev
+} // namespace sfxb

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -11,7 +12,10 @@
 #include "../../include/sfxb_cuda.h"
 #include "bignum_host.hpp"
 #include "ctx.hpp"
+#include "hist.cuh"
 #include "kernels.cuh"
+
+#include <cub/cub.cuh>
 
 using namespace sfxb;
 using sfxb::host::Big;
@@ -19,7 +23,8 @@ using sfxb::host::Big;
 struct sfxb_ctx : CtxState {};
 struct sfxb_gh {
     sfxb_ctx *ctx = nullptr;
-    uint32_t *d = nullptr; // 2·n_samples × 4s limbs, Montgomery form
+    uint32_t *d = nullptr;     // 2·n_samples × 4s limbs, Montgomery form
+    uint8_t *flags = nullptr;  // per row: bit0 Enc(g) == 1, bit1 Enc(h) == 1
     uint32_t n_samples = 0;
 };
 
@@ -331,6 +336,193 @@ void add_dev(sfxb_ctx *c, const uint32_t *d_a, const uint32_t *d_b, size_t count
     });
 }
 
+
+// --------------------------------------------------------------- histogram (K2)
+
+constexpr int kPiece = 16; // items per segmented-product piece
+
+struct HistBufs {
+    Buf node_of, count, ones, cursor, seg_start, sorted, np, piece_start, pieces, part[2], cub, misc;
+};
+HistBufs &hist_bufs(sfxb_ctx *c) {
+    static thread_local std::map<sfxb_ctx *, HistBufs> m; // per context, per thread
+    return m[c];
+}
+
+void gh_prepare(sfxb_ctx *c, sfxb_gh *g) {
+    const size_t S4 = 4 * (size_t)c->s, n2 = 2 * (size_t)g->n_samples;
+    dispatch_class(c->s, [&](auto sc) {
+        constexpr int cs = decltype(sc)::value;
+        using C = Cls<cs>;
+        if (g->n_samples) {
+            int grid = (int)std::min<size_t>((g->n_samples + 255) / 256, (size_t)c->sms * 8);
+            dev::k_gh_flags<4 * cs><<<grid, 256, 0, c->stream>>>(g->d, g->n_samples, 2 * c->nw, g->flags);
+            check_launch(*c);
+            auto k = dev::k_to_mont<4 * cs, C::TH>;
+            constexpr int NI = dev::kBlock / C::TH;
+            int grid2 = occupancy_grid(*c, k, n2, NI);
+            k<<<grid2, dev::kBlock, 0, c->stream>>>(arg(c->mod_n2), g->d, n2);
+            check_launch(*c);
+        }
+    });
+    (void)S4;
+}
+
+sfxb_gh *gh_alloc(sfxb_ctx *c, uint32_t n_samples) {
+    auto g = std::make_unique<sfxb_gh>();
+    g->ctx = c;
+    g->n_samples = n_samples;
+    CK(cudaMalloc(&g->d, (size_t)n_samples * 2 * 4 * c->s * 4 + 16));
+    CK(cudaMalloc(&g->flags, (size_t)n_samples + 16));
+    return g.release();
+}
+
+template <typename T>
+T *bget(Buf &b, size_t n) {
+    return (T *)grow(b, n * sizeof(T) + 64);
+}
+
+void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint32_t J, const uint32_t *d_offsets,
+                    uint32_t N, const uint32_t *d_rows, uint32_t R, uint32_t K, uint32_t *d_out, int mont_out,
+                    uint64_t *additions) {
+    if (!g || g->ctx != c) throw ApiError(SFXB_ERR_ARG, "accumulate: gradient handle belongs to another context");
+    if (K == 0 || K > 65536) throw ApiError(SFXB_ERR_ARG, "accumulate: n_bins out of range");
+    const size_t nkeys = (size_t)N * J * K;
+    if (nkeys == 0) return;
+    if (nkeys >= 0xffffffffull || (size_t)R * J >= 0xffffffffull)
+        throw ApiError(SFXB_ERR_ARG, "accumulate: frontier too large for one call");
+    HistBufs &B = hist_bufs(c);
+    cudaStream_t st = c->stream;
+    uint32_t *count = bget<uint32_t>(B.count, nkeys), *ones = bget<uint32_t>(B.ones, 2 * nkeys);
+    uint32_t *cursor = bget<uint32_t>(B.cursor, nkeys), *seg_start = bget<uint32_t>(B.seg_start, nkeys);
+    uint32_t *misc = bget<uint32_t>(B.misc, 16);
+    CK(cudaMemsetAsync(count, 0, nkeys * 4, st));
+    CK(cudaMemsetAsync(ones, 0, 2 * nkeys * 4, st));
+    CK(cudaMemsetAsync(cursor, 0, nkeys * 4, st));
+    CK(cudaMemsetAsync(misc, 0, 64, st));
+    dev::HistArgs a{};
+    a.rows = d_rows;
+    a.n_rows = R;
+    a.bins = d_bins;
+    a.n_samples = g->n_samples;
+    a.J = J;
+    a.K = K;
+    a.gh_flags = g->flags;
+    a.count = count;
+    a.ones = ones;
+    a.cursor = cursor;
+    a.seg_start = seg_start;
+    a.status = misc;
+    if (R > 0) {
+        uint32_t *node_of = bget<uint32_t>(B.node_of, R);
+        a.node_of = node_of;
+        dev::k_node_of<<<N, 256, 0, st>>>(d_offsets, node_of);
+        check_launch(*c);
+        const size_t items = (size_t)R * J;
+        int grid = (int)std::min<size_t>((items + 255) / 256, (size_t)c->sms * 16);
+        dev::k_hist_count<<<grid, 256, 0, st>>>(a);
+        check_launch(*c);
+        uint32_t status = 0;
+        CK(cudaMemcpyAsync(&status, misc, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (status & 2u) throw ApiError(SFXB_ERR_ARG, "row index out of range in accumulate");
+        if (status & 1u) throw ApiError(SFXB_ERR_ARG, "bin index out of range in accumulate");
+    }
+    // scan counts -> segment starts; max count -> number of passes
+    size_t tmp_bytes = 0, tmp2 = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, count, seg_start, (int)nkeys, st));
+    CK(cub::DeviceReduce::Max(nullptr, tmp2, count, misc + 4, (int)nkeys, st));
+    void *cubtmp = grow(B.cub, std::max(tmp_bytes, tmp2) + 256);
+    CK(cub::DeviceScan::ExclusiveSum(cubtmp, tmp_bytes, count, seg_start, (int)nkeys, st));
+    CK(cub::DeviceReduce::Max(cubtmp, tmp2, count, misc + 4, (int)nkeys, st));
+    unsigned long long *adds_d = reinterpret_cast<unsigned long long *>(misc + 8);
+    {
+        int grid = (int)std::min<size_t>((nkeys + 255) / 256, (size_t)c->sms * 8);
+        dev::k_hist_adds<<<grid, 256, 0, st>>>(count, ones, nkeys, adds_d);
+        check_launch(*c);
+    }
+    if (R > 0) {
+        const size_t items = (size_t)R * J;
+        uint32_t *sorted = bget<uint32_t>(B.sorted, items);
+        a.sorted = sorted;
+        int grid = (int)std::min<size_t>((items + 255) / 256, (size_t)c->sms * 16);
+        dev::k_hist_scatter<<<grid, 256, 0, st>>>(a);
+        check_launch(*c);
+    }
+    uint32_t maxc = 0;
+    unsigned long long adds_h = 0;
+    CK(cudaMemcpyAsync(&maxc, misc + 4, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&adds_h, adds_d, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (additions) *additions += adds_h;
+
+    // Passes of the segmented product.  Pass i reads segments (starts S_i,
+    // lengths L_i) and writes per-key piece counts np and piece starts ps;
+    // then S_{i+1} = ps, L_{i+1} = np.  Two (np, ps) and two partial buffers
+    // alternate.
+    uint32_t *npb[2] = {bget<uint32_t>(B.np, 2 * nkeys), nullptr};
+    npb[1] = npb[0] + nkeys;
+    uint32_t *psb[2] = {bget<uint32_t>(B.piece_start, 2 * nkeys), nullptr};
+    psb[1] = psb[0] + nkeys;
+    const uint32_t *cur_start = seg_start, *cur_len = count;
+    const uint32_t *src = g->d;
+    const uint32_t *sorted = R ? (const uint32_t *)B.sorted.p : nullptr;
+    const uint32_t *final_idx = seg_start, *final_part = g->d;
+    dispatch_class(c->s, [&](auto sc) {
+        constexpr int cs = decltype(sc)::value;
+        using C = Cls<cs>;
+        constexpr int S4 = 4 * cs;
+        const int g1 = (int)std::min<size_t>((nkeys + 255) / 256, (size_t)c->sms * 8);
+        uint32_t m = maxc;
+        for (int pass = 0; m > 0; ++pass) {
+            uint32_t *np = npb[pass & 1], *ps = psb[pass & 1];
+            dev::k_npieces<<<g1, 256, 0, st>>>(cur_len, nkeys, kPiece, np);
+            check_launch(*c);
+            CK(cub::DeviceScan::ExclusiveSum(cubtmp, tmp_bytes, np, ps, (int)nkeys, st));
+            uint32_t tail[2];
+            CK(cudaMemcpyAsync(&tail[0], ps + nkeys - 1, 4, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(&tail[1], np + nkeys - 1, 4, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            const size_t P = (size_t)tail[0] + tail[1];
+            dev::Piece *pieces = bget<dev::Piece>(B.pieces, P);
+            dev::k_emit_pieces<<<g1, 256, 0, st>>>(cur_start, cur_len, ps, nkeys, kPiece, pieces);
+            check_launch(*c);
+            uint32_t *dst = bget<uint32_t>(B.part[pass & 1], P * 2 * S4);
+            auto k = dev::k_seg_prod<S4, C::TH, kPiece>;
+            constexpr int NI = dev::kBlock / C::TH;
+            const int grid = occupancy_grid(*c, k, 2 * P, NI);
+            k<<<grid, dev::kBlock, 0, st>>>(arg(c->mod_n2), pieces, P, pass == 0 ? sorted : nullptr, src, dst);
+            check_launch(*c);
+            final_idx = ps;
+            final_part = dst;
+            cur_start = ps;
+            cur_len = np;
+            src = dst;
+            if (m <= (uint32_t)kPiece) break;
+            m = (m + kPiece - 1) / kPiece;
+        }
+        auto kf = dev::k_hist_finalize<S4, C::TH>;
+        constexpr int NI = dev::kBlock / C::TH;
+        const int grid = occupancy_grid(*c, kf, 2 * nkeys, NI);
+        kf<<<grid, dev::kBlock, 0, st>>>(arg(c->mod_n2), count, final_idx, nkeys, final_part, d_out, mont_out);
+        check_launch(*c);
+    });
+}
+
+void reduce_parts_dev(sfxb_ctx *c, const uint32_t *d_parts, uint32_t parts, size_t n_slots, uint32_t *d_out) {
+    if (n_slots == 0) return;
+    if (parts == 0) throw ApiError(SFXB_ERR_ARG, "reduce_partials: no inputs");
+    dispatch_class(c->s, [&](auto sc) {
+        constexpr int cs = decltype(sc)::value;
+        using C = Cls<cs>;
+        auto k = dev::k_reduce_parts<4 * cs, C::TH>;
+        constexpr int NI = dev::kBlock / C::TH;
+        const int grid = occupancy_grid(*c, k, n_slots, NI);
+        k<<<grid, dev::kBlock, 0, c->stream>>>(arg(c->mod_n2), d_parts, parts, n_slots, d_out);
+        check_launch(*c);
+    });
+}
+
 // --------------------------------------------------------------- host <-> padded layouts
 
 // copy `count` values of `words` limbs into a padded device layout of `stride`
@@ -605,6 +797,85 @@ int sfxb_decrypt(sfxb_ctx *c, const uint32_t *cts, size_t count, uint32_t scale,
         CK(cudaMemcpyAsync(out_values, dv.p, count * 8, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         if (out_plain) d2h_padded(c, out_plain, dplain.p, count, c->nw, Sn);
+    });
+}
+
+
+int sfxb_gh_upload(sfxb_ctx *c, const uint32_t *gh_cts, uint32_t n_samples, sfxb_gh **out) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        std::unique_ptr<sfxb_gh> g(gh_alloc(c, n_samples));
+        const size_t S4 = 4 * (size_t)c->s;
+        if (n_samples) h2d_padded(c, g->d, gh_cts, 2 * (size_t)n_samples, 2 * c->nw, S4);
+        gh_prepare(c, g.get());
+        CK(cudaStreamSynchronize(c->stream));
+        *out = g.release();
+    });
+}
+
+int sfxb_gh_from_dev(sfxb_ctx *c, const uint32_t *d_gh, uint32_t n_samples, sfxb_gh **out) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        std::unique_ptr<sfxb_gh> g(gh_alloc(c, n_samples));
+        const size_t S4 = 4 * (size_t)c->s;
+        CK(cudaMemcpyAsync(g->d, d_gh, 2 * (size_t)n_samples * S4 * 4, cudaMemcpyDeviceToDevice, c->stream));
+        gh_prepare(c, g.get());
+        CK(cudaStreamSynchronize(c->stream));
+        *out = g.release();
+    });
+}
+
+void sfxb_gh_free(sfxb_gh *g) {
+    if (!g) return;
+    cudaSetDevice(g->ctx->device);
+    cudaStreamSynchronize(g->ctx->stream);
+    cudaFree(g->d);
+    cudaFree(g->flags);
+    delete g;
+}
+
+int sfxb_accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint32_t n_features,
+                        const uint32_t *d_node_offsets, uint32_t n_nodes, const uint32_t *d_rows, uint32_t n_rows,
+                        uint32_t n_bins, uint32_t *d_out, int mont_out, uint64_t *additions) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        accumulate_dev(c, g, d_bins, n_features, d_node_offsets, n_nodes, d_rows, n_rows, n_bins, d_out, mont_out,
+                       additions);
+    });
+}
+
+int sfxb_accumulate(sfxb_ctx *c, const uint32_t *gh_cts, uint32_t n_samples, const uint16_t *bins, uint32_t J,
+                    const uint32_t *node_offsets, uint32_t N, const uint32_t *rows, uint32_t K, uint32_t *out_slots,
+                    uint64_t *additions) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        for (uint32_t i = 0; i < N; ++i)
+            if (node_offsets[i + 1] < node_offsets[i]) throw ApiError(SFXB_ERR_ARG, "accumulate: node offsets decrease");
+        const uint32_t R = N ? node_offsets[N] - node_offsets[0] : 0;
+        if (N && node_offsets[0] != 0) throw ApiError(SFXB_ERR_ARG, "accumulate: node offsets must start at 0");
+        std::unique_ptr<sfxb_gh, void (*)(sfxb_gh *)> g(nullptr, sfxb_gh_free);
+        {
+            sfxb_gh *gp = nullptr;
+            int rc = sfxb_gh_upload(c, gh_cts, n_samples, &gp);
+            if (rc != SFXB_OK) throw ApiError(rc, c->err);
+            g.reset(gp);
+        }
+        const size_t S4 = 4 * (size_t)c->s, nslots = 2ull * N * J * K;
+        DevBuf<uint16_t> db((size_t)J * n_samples);
+        DevBuf<uint32_t> doff((size_t)N + 1), drows(R ? R : 1), dout(nslots * S4);
+        if ((size_t)J * n_samples)
+            CK(cudaMemcpyAsync(db.p, bins, (size_t)J * n_samples * 2, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(doff.p, node_offsets, ((size_t)N + 1) * 4, cudaMemcpyHostToDevice, c->stream));
+        if (R) CK(cudaMemcpyAsync(drows.p, rows, (size_t)R * 4, cudaMemcpyHostToDevice, c->stream));
+        accumulate_dev(c, g.get(), db.p, J, doff.p, N, drows.p, R, K, dout.p, 0, additions);
+        d2h_padded(c, out_slots, dout.p, nslots, 2 * c->nw, S4);
+    });
+}
+
+int sfxb_reduce_partials_dev(sfxb_ctx *c, const uint32_t *d_parts, uint32_t parts, size_t n_slots, uint32_t *d_out) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        reduce_parts_dev(c, d_parts, parts, n_slots, d_out);
     });
 }
 

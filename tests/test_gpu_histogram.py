@@ -1,0 +1,125 @@
+"""GPU parity for the encrypted histogram (accumulate_rows,
+secure_processor.cpp:587-620) and the multi-GPU partial reduce (K4):
+residues bit-exact against the reference's golden slots and the oracle,
+ciphertext_additions equal to the reference counter law
+(test_processor.cpp:442-486)."""
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+from keys import key
+from paper_2504_03909_b200 import _lib
+from py_oracle import Oracle, OracleKey, ints_to_words, words_to_ints
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def golden(name):
+    with open(os.path.join(HERE, "golden", f"plugin_{name}.json")) as f:
+        return json.load(f)
+
+
+def frontier(nodes):
+    offs = np.cumsum([0] + [len(x) for x in nodes]).astype(np.uint32)
+    rows = np.array([r for nd in nodes for r in nd], np.uint32)
+    return offs, rows
+
+
+@pytest.mark.parametrize("kname", ["k512_c0ffee", "k2048_7"])
+@pytest.mark.parametrize("fx", ["fixture4", "random50"])
+def test_accumulate_matches_reference_golden(kname, fx):
+    g = golden(kname)[fx]
+    n, p, q = key(kname)
+    ctx = _lib.Context(n)  # passive party: public key only (federation.cpp:83-85)
+    cts = ints_to_words([int(x, 16) for x in g["cts"]], ctx.ct_words)
+    bins = np.array(g["inputs"]["bins"], np.uint16)
+    offs, rows = frontier(g["inputs"]["nodes"])
+    slots, adds = ctx.accumulate(cts, bins, offs, rows, g["inputs"]["n_bins"])
+    assert words_to_ints(slots) == [int(x, 16) for x in g["slots"]]
+    assert adds == g["counters_after_accumulate"][1]
+
+
+def random_case(rng, n, n_samples, J, K, n_nodes, ones_frac=0.0):
+    cts = [rng.randrange(2, n * n) for _ in range(2 * n_samples)]
+    for i in range(len(cts)):
+        if rng.random() < ones_frac:
+            cts[i] = 1
+    bins = np.array([[rng.randrange(K) for _ in range(n_samples)] for _ in range(J)], np.uint16)
+    perm = list(range(n_samples))
+    rng.shuffle(perm)
+    cut = sorted(rng.sample(range(1, n_samples), n_nodes - 1)) if n_nodes > 1 else []
+    nodes, prev = [], 0
+    for c in cut + [n_samples]:
+        nodes.append(sorted(perm[prev:c]))
+        prev = c
+    nodes[-1] = nodes[-1][: max(0, len(nodes[-1]) - 7)]  # some rows in no frontier node (leaves)
+    return cts, bins, nodes
+
+
+@pytest.mark.parametrize("shape", [(300, 3, 8, 3, 0.0), (257, 2, 64, 5, 0.02), (5000, 1, 2, 1, 0.0)])
+def test_accumulate_random_matches_oracle(shape):
+    n_samples, J, K, n_nodes, ones = shape
+    n, p, q = key("k512_c0ffee")
+    ok = OracleKey(Oracle(), n)
+    rng = random.Random(str(shape))
+    cts, bins, nodes = random_case(rng, n, n_samples, J, K, n_nodes, ones)
+    ctx = _lib.Context(n)
+    cw = ints_to_words(cts, ctx.ct_words)
+    offs, rows = frontier(nodes)
+    slots, adds = ctx.accumulate(cw, bins, offs, rows, K)
+    want, want_adds = ok.accumulate(cw, bins, offs, rows, K)
+    assert np.array_equal(slots, want)
+    assert adds == want_adds
+
+
+def test_accumulate_empty_bins_and_errors():
+    # test_processor.cpp:417-440: empty bins stay the literal 1
+    n, p, q = key("k512_c0ffee")
+    ctx = _lib.Context(n, p, q)
+    rng = random.Random(1)
+    cts = ints_to_words([rng.randrange(2, n * n) for _ in range(2)], ctx.ct_words)
+    slots, adds = ctx.accumulate(cts, np.array([[1], [0]], np.uint16), np.array([0, 1], np.uint32),
+                                 np.array([0], np.uint32), 3)
+    ints = words_to_ints(slots)
+    assert sum(1 for x in ints if x == 1) == 8 and adds == 0
+    with pytest.raises(_lib.SfxbError, match="bin index out of range in accumulate"):
+        ctx.accumulate(cts, np.array([[3]], np.uint16), np.array([0, 1], np.uint32), np.array([0], np.uint32), 3)
+    # empty frontier -> every slot trivial
+    slots, adds = ctx.accumulate(cts, np.array([[0]], np.uint16), np.array([0, 0], np.uint32),
+                                 np.array([], np.uint32), 2)
+    assert words_to_ints(slots) == [1] * 4 and adds == 0
+
+
+def test_partial_reduce_equals_full_histogram():
+    """Row-sharded partials (Montgomery form) combined by K4 == one-shot histogram."""
+    import torch
+
+    n, p, q = key("k512_c0ffee")
+    ctx = _lib.Context(n)
+    ops = _lib.DeviceOps(ctx)
+    rng = random.Random(7)
+    n_samples, J, K = 400, 3, 16
+    cts, bins, nodes = random_case(rng, n, n_samples, J, K, 4)
+    cw = ints_to_words(cts, ctx.ct_words)
+    offs, rows = frontier(nodes)
+    full, _ = ctx.accumulate(cw, bins, offs, rows, K)
+    gh = ops.gh_upload(cw)
+    dev = torch.device("cuda:0")
+    d_bins = torch.from_numpy(bins.astype(np.int16).copy()).to(dev)
+    n_slots = len(nodes) * J * K * 2
+    parts = torch.zeros((2, n_slots, ctx.ct_words), dtype=torch.int32, device=dev)
+    # shard: rows with even / odd ids
+    for s in range(2):
+        sub = [[r for r in nd if r % 2 == s] for nd in nodes]
+        so, sr = frontier(sub)
+        d_off = torch.from_numpy(so.astype(np.int32)).to(dev)
+        d_rows = torch.from_numpy(sr.astype(np.int32)).to(dev) if len(sr) else torch.zeros(1, dtype=torch.int32, device=dev)
+        ops.accumulate(gh, d_bins, J, d_off, len(sub), d_rows, len(sr), K, parts[s], mont_out=True)
+    out = torch.zeros((n_slots, ctx.ct_words), dtype=torch.int32, device=dev)
+    ops.reduce_partials(parts, 2, n_slots, out)
+    got = out.cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, full)
