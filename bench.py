@@ -1,0 +1,504 @@
+#!/usr/bin/env python
+"""bench.py — encrypted-histogram s/tree + Paillier enc/s on B200 (BASELINE.json).
+
+Workload (BASELINE.json configs[1]): vertical 2-party HIGGS-shaped synthetic
+data, 1M rows × 28 features (14 per party), 256 bins, depth 6 (histograms at
+depths 0-5), 2048-bit key keygen(2048, 7).  One STEP = one tree's encrypted
+histogram build: accumulate_rows for every level × party (12 calls), each row
+of the frontier folded into its (node, feature, bin) slot for G and H.
+Synthetic inputs: uniform bins, balanced binary frontiers (every row stays in
+the frontier to depth 5), random ciphertexts < n² (the kernel cost does not
+depend on the plaintexts).  The gradient ciphertexts (1 GB) exceed L2.
+
+Reported (one JSON line, rank 0):
+  value       device-resident s/tree (CUDA events on the kernels' stream,
+              max over ranks); lower is better
+  e2e         the same through the C ABI with HOST buffers: per tree the gh
+              ciphertexts are uploaded once (sfxb_gh_upload), every level ×
+              party uploads bins + frontier and downloads its slots
+              (sfxb_accumulate_gh) — the C++ adapter's call pattern
+  enc_per_s / dec_per_s / adds_per_s: Paillier encrypt (CRT), decrypt (CRT)
+              and ciphertext-add throughput, each from its own timed sample
+  roofline    dominant kernel K2 (segmented Montgomery product): algorithmic
+              products = reference ciphertext_additions × (2s²+s) with
+              s = 128 limbs, ÷ its CUDA-event time; peak = the IMAD.WIDE.U32
+              carry-chain microbenchmark run in this process
+  cpu_baseline the reference PaillierPlugin (oracle/_ref, built from the
+              unmodified sources) on one host core, bounded sample,
+              extrapolated with the exact per-tree addition count
+
+Multi-GPU (torchrun): rows are sharded contiguously; partial histograms are
+exchanged with all_to_all and reduced by the K4 kernel (strong scaling).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "encrypted-histogram s/tree + Paillier enc/s, 1M×28, 2048-bit n, 1/2/4/8 B200"
+UNIT = "s/tree"
+S_LIMBS = 128  # 2048-bit n: ciphertexts mod n² are 128 u32 limbs
+PRODUCTS_PER_ADD = 2 * S_LIMBS * S_LIMBS + S_LIMBS  # Montgomery modmul mod n²
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rows", type=int, default=1_000_000)
+    ap.add_argument("--feats", type=int, default=14, help="features per party")
+    ap.add_argument("--parties", type=int, default=2)
+    ap.add_argument("--bins", type=int, default=256)
+    ap.add_argument("--depth", type=int, default=6)
+    ap.add_argument("--key", default="k2048_7")
+    ap.add_argument("--enc-sample", type=int, default=1 << 17)
+    ap.add_argument("--dec-sample", type=int, default=1 << 17)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-sample-rows", type=int, default=12000, help="per host thread (reference arm)")
+    ap.add_argument("--cpu-rows", type=int, default=40000, help="single-core cpu_baseline sample")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def config(a, world):
+    return {
+        "workload": f"vertical {a.parties}-party HIGGS-shaped synthetic {a.rows}x{a.feats * a.parties}, "
+                    f"{a.bins} bins, depth {a.depth}, 2048-bit n (configs[1])",
+        "rows": a.rows, "features": a.feats * a.parties, "parties": a.parties, "bins": a.bins,
+        "depth": a.depth, "key": "keygen(2048, 7)", "parallelism": f"row-shard x{world}",
+        "l2": "inputs > L2 (gh ciphertexts 1 GB)",
+    }
+
+
+# ------------------------------------------------------------------ clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for name, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ synthetic frontier
+
+
+def frontiers(n_rows: int, depth: int, seed: int):
+    """Balanced binary frontiers: node(depth d) = top d bits of a per-row key;
+    rows ascending inside a node (the reference's NodeRows order)."""
+    rng = np.random.default_rng(seed)
+    keys = rng.integers(0, 2**32, n_rows, dtype=np.uint64)
+    out = []
+    for d in range(depth):
+        node = (keys >> np.uint64(32 - d)).astype(np.int64) if d else np.zeros(n_rows, np.int64)
+        order = np.argsort(node, kind="stable").astype(np.uint32)
+        counts = np.bincount(node, minlength=1 << d)
+        offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.uint32)
+        out.append((offs, order))
+    return out
+
+
+def adds_per_tree(bins_per_party, fronts, K):
+    """The reference's ciphertext_additions for one tree (fold_into law)."""
+    total = 0
+    for offs, rows in fronts:
+        N = len(offs) - 1
+        node_of = np.repeat(np.arange(N), np.diff(offs))
+        for bins in bins_per_party:
+            for f in range(bins.shape[0]):
+                key = node_of * K + bins[f][rows].astype(np.int64)
+                c = np.bincount(key, minlength=N * K)
+                total += 2 * int(np.maximum(c - 1, 0).sum())
+    return total
+
+
+def rand_words(rng, count, words, top_mask=0x3FFFFFFF):
+    x = rng.integers(0, 2**32, (count, words), dtype=np.uint64).astype(np.uint32)
+    x[:, -1] &= np.uint32(top_mask)  # < 2^(32·words − 2) <= n² (n has exactly 2048 bits)
+    return x
+
+
+# ------------------------------------------------------------------ CPU baseline
+
+
+def cpu_baseline(a, n, nw, adds_tree, threads: int = 1):
+    """Reference PaillierPlugin::accumulate_rows on a bounded level-0 sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import py_oracle as po
+
+    S = min(a.cpu_rows if threads <= 1 else a.cpu_sample_rows * threads, a.rows)
+    rng = np.random.default_rng(11)
+    cts = rand_words(rng, 2 * S, 2 * nw)
+    bins = rng.integers(0, a.bins, (a.feats, S), dtype=np.uint16)
+    offs = np.array([0, S], np.uint32)
+    rows = np.arange(S, dtype=np.uint32)
+    if po.reference_available():
+        ref = po.Reference()
+        t0 = time.perf_counter()
+        if threads <= 1:
+            plug = po.RefPlugin(ref, n, nw)
+            plug.accumulate(cts, bins, offs, rows, a.bins)
+            adds = plug.counters()[1]
+        else:
+            import ctypes as C
+
+            out = C.c_uint64(0)
+            ref._check(ref.lib.ref_accumulate_threaded(
+                po.to_words(n, nw), nw, cts.reshape(-1), S, bins.reshape(-1), a.feats, offs, 1, rows, a.bins,
+                threads, C.byref(out)))
+            adds = out.value
+        dt = time.perf_counter() - t0
+        kind = "reference"
+    else:  # oracle port (C restatement)
+        ok = po.OracleKey(po.Oracle(), n)
+        t0 = time.perf_counter()
+        _, adds = ok.accumulate(cts, bins, offs, rows, a.bins)
+        dt = time.perf_counter() - t0
+        kind, threads = "port", 1
+    rate = adds / dt
+    return {
+        "value": adds_tree / rate, "unit": UNIT, "cores": threads, "kind": kind,
+        "sample": f"accumulate_rows level-0, {S} rows x {a.feats} features x {a.bins} bins, 2048-bit n: "
+                  f"{adds} ciphertext additions in {dt:.2f} s ({rate:.3e} adds/s), extrapolated to "
+                  f"{adds_tree} additions/tree",
+        "adds_per_s": rate,
+    }
+
+
+# ------------------------------------------------------------------ reference arm
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from keys import key
+
+    n, p, q = key(a.key)
+    nw = (n.bit_length() + 31) // 32
+    fronts = frontiers(a.rows, a.depth, seed=5)
+    rng = np.random.default_rng(3)
+    bins_pp = [rng.integers(0, a.bins, (a.feats, a.rows), dtype=np.uint16) for _ in range(a.parties)]
+    adds_tree = adds_per_tree(bins_pp, fronts, a.bins)
+    threads = os.cpu_count() or 1
+    vals = []
+    last = None
+    for i in range(a.warmup + a.steps):
+        last = cpu_baseline(a, n, nw, adds_tree, threads=threads)
+        if i >= a.warmup:
+            vals.append(last["value"])
+    v = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic", "config": config(a, world),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": last["kind"],
+                         "sample": last["sample"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "adds_per_s": last["adds_per_s"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    from keys import key
+    from paper_2504_03909_b200 import _lib
+    from paper_2504_03909_b200 import dist as pdist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    peak, peak_clk = _lib.imad_peak(local)
+    n, p, q = key(a.key)
+    ctxs = [_lib.Context(n, p, q, device=local)] + [_lib.Context(n, device=local) for _ in range(a.parties - 1)]
+    ops = [_lib.DeviceOps(c) for c in ctxs]
+    nw, cw = ctxs[0].nw, ctxs[0].ct_words
+    lo, hi = pdist.row_shard(a.rows, world, rank)
+    R = hi - lo
+    K, J, D = a.bins, a.feats, a.depth
+
+    # ---- synthetic inputs (identical on every rank; each keeps its rows)
+    fronts_full = frontiers(a.rows, D, seed=5)
+    rng = np.random.default_rng(3)
+    bins_pp = [rng.integers(0, K, (J, a.rows), dtype=np.uint16) for _ in range(a.parties)]
+    adds_tree_ref = adds_per_tree(bins_pp, fronts_full, K) if rank == 0 else 0
+    fronts = []
+    for offs, rows in fronts_full:
+        # local frontier: rows of this shard, renumbered, node order kept
+        N = len(offs) - 1
+        node_of = np.repeat(np.arange(N), np.diff(offs))
+        keep = (rows >= lo) & (rows < hi)
+        lrows = (rows[keep] - lo).astype(np.uint32)
+        lcount = np.bincount(node_of[keep], minlength=N)
+        loffs = np.concatenate([[0], np.cumsum(lcount)]).astype(np.uint32)
+        fronts.append((loffs, lrows))
+    d_bins = [torch.from_numpy(b[:, lo:hi].astype(np.int16).copy()).to(dev) for b in bins_pp]
+    d_front = [(torch.from_numpy(o.astype(np.int32)).to(dev), torch.from_numpy(r.astype(np.int32)).to(dev))
+               for o, r in fronts]
+    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
+    gh_dev = torch.randint(-(2**31), 2**31 - 1, (2 * R, cw), dtype=torch.int32, device=dev, generator=gen)
+    gh_dev[:, -1] &= 0x3FFFFFFF
+    gh = [ops[pi].gh_from_dev(gh_dev, R) for pi in range(a.parties)]
+    gh_host = torch.empty((2 * R, cw), dtype=torch.int32, pin_memory=True)
+    gh_host.copy_(gh_dev)
+    del gh_dev
+    n_slots = [(1 << d) * J * K * 2 for d in range(D)]
+    pad = [pdist.padded_slots(s, world) for s in n_slots]
+    outs = [[torch.empty((pad[d], cw), dtype=torch.int32, device=dev) for _ in range(a.parties)] for d in range(D)]
+    finals = [[None] * a.parties for _ in range(D)]
+    stream = torch.cuda.ExternalStream(ctxs[0].lib.sfxb_ctx_stream(ctxs[0].h), device=dev)
+
+    def one_tree(sync_each=True):
+        adds = 0
+        for d in range(D):
+            offs, rows = d_front[d]
+            N = offs.shape[0] - 1
+            for pi in range(a.parties):
+                adds += ops[pi].accumulate(gh[pi], d_bins[pi], J, offs, N, rows, rows.shape[0], K, outs[d][pi],
+                                           mont_out=world > 1, sync=False)
+                if world > 1:
+                    ctxs[pi].lib.sfxb_ctx_sync(ctxs[pi].h)
+                    recv = pdist.exchange(outs[d][pi], world)
+                    # reduce_partials syncs torch's stream (the NCCL op) before enqueueing
+                    finals[d][pi] = pdist.reduce_slice(
+                        recv, lambda parts, k, sl, out: ops[pi].reduce_partials(parts, k, sl, out))
+        for c in ctxs:
+            c._check(c.lib.sfxb_ctx_sync(c.h))
+        return adds
+
+    # ---- warm-up
+    for _ in range(a.warmup):
+        one_tree()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    # ---- timed region (device events on the kernels' stream; all parties'
+    # contexts are drained before the end event)
+    for c in ctxs:
+        c.profile(True)
+    launches0 = sum(c.launches for c in ctxs)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    adds_timed = 0
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(a.steps):
+            adds_timed += one_tree()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = sum(c.launches for c in ctxs) - launches0
+    k2 = [c.kernel_time(0) for c in ctxs]
+    k2_launches = sum(x[0] for x in k2)
+    k2_ms = sum(x[1] for x in k2)
+    for c in ctxs:
+        c.profile(False)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    adds_t = torch.tensor([adds_timed], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(adds_t, op=dist.ReduceOp.SUM)
+    ms_step = t.item() / a.steps
+    adds_step = adds_t.item() / a.steps
+
+    # ---- e2e through the C ABI with host buffers
+    h_bins = [torch.from_numpy(b[:, lo:hi].copy()).pin_memory().numpy() for b in bins_pp]
+    h_front = [(o, torch.from_numpy(r.astype(np.int32)).pin_memory().numpy().view(np.uint32)) for o, r in fronts]
+    h_out = [torch.empty((n_slots[d], cw), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+             for d in range(D)]
+    h2d = d2h = 0
+    e2e_times = []
+    gh_np = gh_host.numpy().view(np.uint32)
+    for it in range(1 + max(1, a.e2e_steps)):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        h2d = d2h = 0
+        for pi in range(a.parties):
+            g = ops[pi].gh_upload(gh_np)
+            h2d += gh_np.nbytes
+            for d in range(D):
+                offs, rows = h_front[d]
+                if world > 1:
+                    outp = outs[d][pi]
+                    ops[pi].accumulate(g, d_bins[pi], J, d_front[d][0], len(offs) - 1, d_front[d][1],
+                                       len(rows), K, outp, mont_out=True)
+                    recv = pdist.exchange(outp, world)
+                    fin = pdist.reduce_slice(recv, lambda parts, k, sl, out: ops[pi].reduce_partials(parts, k, sl, out))
+                    full = pdist.gather_slices(fin, n_slots[d], world)
+                    if rank == 0:
+                        h_out[d][:] = full.cpu().numpy().view(np.uint32)
+                    h2d += h_bins[pi].nbytes + offs.nbytes + rows.nbytes
+                    d2h += h_out[d].nbytes if rank == 0 else 0
+                else:
+                    ops[pi].accumulate_host(g, h_bins[pi], offs, rows, K, out=h_out[d])
+                    h2d += h_bins[pi].nbytes + offs.nbytes + rows.nbytes
+                    d2h += h_out[d].nbytes
+            g.free()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if it > 0:  # first iteration is a warm-up
+            e2e_times.append(dt)
+    e2e = torch.tensor([statistics.median(e2e_times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+
+    # ---- enc/s and dec/s samples (per GPU, rank-local; whole-job = × world)
+    E = a.enc_sample
+    r_dev = torch.randint(-(2**31), 2**31 - 1, (E, nw), dtype=torch.int32, device=dev, generator=gen)
+    r_dev[:, -1] &= 0x3FFFFFFF
+    q_dev = torch.randint(-(1 << 41), 1 << 41, (E,), dtype=torch.int64, device=dev, generator=gen)
+    enc_out = torch.empty((E, cw), dtype=torch.int32, device=dev)
+    ops[0].encrypt(q_dev[:4096], r_dev[:4096], 4096, enc_out)
+    ctxs[0].profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    ops[0].encrypt(q_dev, r_dev, E, enc_out, sync=False)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    enc_s = e0.elapsed_time(e1) / 1e3
+    k1 = ctxs[0].kernel_time(1)
+    Dn = min(a.dec_sample, n_slots[D - 1])
+    dec_in = outs[D - 1][0][:Dn] if world == 1 else enc_out[:Dn]
+    dec_vals = torch.empty(Dn, dtype=torch.float64, device=dev)
+    ops[0].decrypt(dec_in[:1024], 1024, dec_vals)
+    ctxs[0].profile(True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    decs = ops[0].decrypt(dec_in, Dn, dec_vals, sync=False)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dec_s = e0.elapsed_time(e1) / 1e3
+    k3 = ctxs[0].kernel_time(2)
+    ctxs[0].profile(False)
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    enc_per_s = E / enc_s * world
+    dec_per_s = decs / dec_s * world
+    achieved = (adds_timed * PRODUCTS_PER_ADD) / (k2_ms / 1e3) if k2_ms > 0 else 0.0
+    enc_products = 2 * (1259 * (2 * 32 * 32 + 32)) + 2 * (1259 * (2 * 64 * 64 + 64))  # CRT, per encryption
+    line = {
+        "metric": METRIC, "value": ms_step / 1e3, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": config(a, world),
+        "enc_per_s": enc_per_s, "dec_per_s": dec_per_s, "adds_per_s": adds_step / (ms_step / 1e3),
+        "ciphertext_additions_per_tree": adds_step,
+        "plugin_s_per_tree_extrapolated": {
+            "encrypt_2M": 2 * a.rows / enc_per_s, "histogram": ms_step / 1e3,
+            "decrypt_occupied": sum(n_slots) * a.parties / dec_per_s,
+        },
+        "e2e": {"value": e2e.item(), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches),
+        "roofline": {
+            "bound": "imad", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tproducts/s",
+            "frac": achieved / peak if peak else None, "traffic": None,
+            "kernel": "k_seg_prod (K2 segmented Montgomery product mod n^2)",
+            "work": f"{PRODUCTS_PER_ADD} 32x32->64 products per reference ciphertext addition",
+            "kernel_launches": k2_launches, "kernel_ms": k2_ms, "kernel_share_of_step": k2_ms / ms,
+            "peak_source": f"sfxb_imad_peak (IMAD.WIDE.U32.X chains, all SMs) at {peak_clk:.0f} MHz",
+        },
+        "roofline_encrypt": {"achieved": enc_products * E / (k1[1] / 1e3) / 1e12 if k1[1] else None,
+                             "peak": peak / 1e12, "unit": "Tproducts/s",
+                             "frac": enc_products * E / (k1[1] / 1e3) / peak if k1[1] else None},
+        "roofline_decrypt": {"achieved": 2 * 1234 * (2 * 64 * 64 + 64) * decs / (k3[1] / 1e3) / 1e12
+                             if k3[1] else None, "unit": "Tproducts/s"},
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not a.no_cpu:
+        try:
+            line["cpu_baseline"] = cpu_baseline(a, n, nw, adds_tree_ref, threads=1)
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"value": None, "unavailable": str(e)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -116,6 +116,13 @@ int sfxb_gh_upload(sfxb_ctx *ctx, const uint32_t *gh_cts, uint32_t n_samples, sf
 int sfxb_gh_from_dev(sfxb_ctx *ctx, const uint32_t *d_gh_cts, uint32_t n_samples, sfxb_gh **out);
 void sfxb_gh_free(sfxb_gh *gh);
 
+/* accumulate_rows with HOST bins / frontier / output over a resident gh
+ * (the C++ adapter's call: the 2·n_samples ciphertexts cross PCIe once per
+ * GhPayload, not once per tree level). */
+int sfxb_accumulate_gh(sfxb_ctx *ctx, const sfxb_gh *gh, const uint16_t *bins, uint32_t n_features,
+                       const uint32_t *node_offsets, uint32_t n_nodes, const uint32_t *rows,
+                       uint32_t n_bins, uint32_t *out_slots, uint64_t *additions);
+
 /* Histogram over a resident gh with device-resident bins and frontier.
  * mont_out != 0 leaves the slots in Montgomery form (partials for the
  * multi-GPU reduce); additions is synchronous (host) and may be NULL. */
@@ -148,6 +155,11 @@ int sfxb_decrypt_dev(sfxb_ctx *ctx, const uint32_t *d_cts, size_t count, uint32_
 /* ---- stream / timing helpers (bench + tests) ---------------------------------- */
 void *sfxb_ctx_stream(sfxb_ctx *ctx); /* cudaStream_t of the context */
 int sfxb_ctx_sync(sfxb_ctx *ctx);
+/* CUDA-event timing of the hot kernel families on the context stream
+ * (0: K2 segmented product, 1: K1 encrypt exponentiations, 2: K3 decrypt
+ * exponentiation).  Enabling resets the accumulators. */
+int sfxb_ctx_profile(sfxb_ctx *ctx, int enable);
+int sfxb_ctx_kernel_time(sfxb_ctx *ctx, int family, uint64_t *launches, double *ms);
 /* integer-multiply peak microbenchmark: IMAD.WIDE.U32(.X) 32×32→64 products/s */
 int sfxb_imad_peak(int device, double *products_per_s, double *sm_clock_mhz);
 

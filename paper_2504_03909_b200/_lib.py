@@ -75,10 +75,14 @@ def load() -> C.CDLL:
         "sfxb_gh_free": (None, [vp]),
         "sfxb_accumulate_dev": (C.c_int, [vp, vp, vp, C.c_uint32, vp, C.c_uint32, vp, C.c_uint32, C.c_uint32,
                                           vp, C.c_int, C.POINTER(C.c_uint64)]),
+        "sfxb_accumulate_gh": (C.c_int, [vp, vp, _u16p, C.c_uint32, _u32p, C.c_uint32, _u32p, C.c_uint32,
+                                         _u32p, C.POINTER(C.c_uint64)]),
         "sfxb_reduce_partials_dev": (C.c_int, [vp, vp, C.c_uint32, sz, vp]),
         "sfxb_decrypt": (C.c_int, [vp, _u32p, sz, C.c_uint32, _f64p, vp, C.POINTER(C.c_uint64)]),
         "sfxb_decrypt_dev": (C.c_int, [vp, vp, sz, C.c_uint32, vp, vp, C.POINTER(C.c_uint64)]),
         "sfxb_imad_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+        "sfxb_ctx_profile": (C.c_int, [vp, C.c_int]),
+        "sfxb_ctx_kernel_time": (C.c_int, [vp, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name, None)
@@ -147,6 +151,15 @@ class Context:
             if rc == SFXB_ERR_AUTH:
                 raise AuthorizationError(rc, msg)
             raise SfxbError(rc, msg)
+
+    def profile(self, enable: bool = True):
+        self._check(self.lib.sfxb_ctx_profile(self.h, 1 if enable else 0))
+
+    def kernel_time(self, family: int):
+        """(launches, total ms) of a hot-kernel family since profile(True)."""
+        n, ms = C.c_uint64(), C.c_double()
+        self._check(self.lib.sfxb_ctx_kernel_time(self.h, family, C.byref(n), C.byref(ms)))
+        return n.value, ms.value
 
     @property
     def launches(self) -> int:
@@ -245,6 +258,19 @@ class DeviceOps:
         h = C.c_void_p()
         self.ctx._check(self.ctx.lib.sfxb_gh_from_dev(self.ctx.h, _ptr(d_gh), n_samples, C.byref(h)))
         return GhHandle(self.ctx, h)
+
+    def accumulate_host(self, gh: GhHandle, bins, node_offsets, rows, n_bins: int, out=None):
+        """Host-buffer accumulate over a resident gh (sfxb_accumulate_gh)."""
+        bins = np.ascontiguousarray(bins, dtype=np.uint16)
+        J = bins.shape[0]
+        n_nodes = len(node_offsets) - 1
+        if out is None:
+            out = np.zeros((n_nodes * J * n_bins * 2, self.ctx.ct_words), np.uint32)
+        adds = C.c_uint64(0)
+        self.ctx._check(self.ctx.lib.sfxb_accumulate_gh(
+            self.ctx.h, gh.h, bins.reshape(-1), J, np.ascontiguousarray(node_offsets, dtype=np.uint32), n_nodes,
+            np.ascontiguousarray(rows, dtype=np.uint32), n_bins, out.reshape(-1), C.byref(adds)))
+        return out, adds.value
 
     def gh_upload(self, gh_cts) -> GhHandle:
         gh_cts = np.ascontiguousarray(gh_cts, dtype=np.uint32)

@@ -59,6 +59,15 @@ struct CtxState {
     uint8_t *d_dig_m1[2] = {nullptr, nullptr}; // p−1, q−1
     int nd_m1[2] = {0, 0};
 
+    // optional per-kernel-family CUDA-event timing (bench roofline):
+    // family 0 = K2 segmented product, 1 = K1 encrypt exps, 2 = K3 decrypt exp
+    bool profile = false;
+    struct Prof {
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+        uint64_t launches = 0;
+        double ms_done = 0;
+    } prof[4];
+
     // scratch (grown on demand, freed with the context)
     Buf scratch_table, tmp[4], host_pinned[2];
     std::vector<void *> owned; // device allocations of constants

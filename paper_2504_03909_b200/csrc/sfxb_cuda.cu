@@ -173,6 +173,25 @@ void check_launch(CtxState &c) {
     c.launches++;
 }
 
+// Brackets a launch with events on the context stream when profiling is on.
+struct ProfScope {
+    CtxState &c;
+    int fam;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(CtxState &c_, int fam_) : c(c_), fam(fam_) {
+        if (!c.profile) return;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        CK(cudaEventRecord(a, c.stream));
+    }
+    ~ProfScope() {
+        if (!c.profile || !a) return;
+        cudaEventRecord(b, c.stream);
+        c.prof[fam].ev.emplace_back(a, b);
+        c.prof[fam].launches++;
+    }
+};
+
 // --------------------------------------------------------------- encrypt
 
 void encrypt_dev(sfxb_ctx *c, const int64_t *d_q, const uint32_t *d_r, size_t count,
@@ -219,6 +238,7 @@ void encrypt_dev(sfxb_ctx *c, const int64_t *d_q, const uint32_t *d_r, size_t co
                 constexpr int NI = dev::kBlock / C::T1;
                 int grid = occupancy_grid(*c, k, 2 * count, NI, 2);
                 a.scratch = (uint32_t *)grow(c->scratch_table, 2 * (size_t)grid * NI * ((size_t)cs << kWindow) * 4);
+                ProfScope prof_(*c, 1);
                 k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(a);
                 check_launch(*c);
             }
@@ -227,6 +247,7 @@ void encrypt_dev(sfxb_ctx *c, const int64_t *d_q, const uint32_t *d_r, size_t co
                 constexpr int NI = dev::kBlock / C::T2;
                 int grid = occupancy_grid(*c, k, 2 * count, NI, 2);
                 a.scratch = (uint32_t *)grow(c->scratch_table, 2 * (size_t)grid * NI * ((size_t)(2 * cs) << kWindow) * 4);
+                ProfScope prof_(*c, 1);
                 k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(a);
                 check_launch(*c);
             }
@@ -305,6 +326,7 @@ void decrypt_dev(sfxb_ctx *c, const uint32_t *d_cts, size_t count, uint32_t scal
             constexpr int NI = dev::kBlock / C::TD;
             int grid = occupancy_grid(*c, k, 2 * (size_t)n_items, NI, 2);
             a.scratch = (uint32_t *)grow(c->scratch_table, 2 * (size_t)grid * NI * ((size_t)(2 * cs) << kWindow) * 4);
+            ProfScope prof_(*c, 2);
             k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(a, n_items);
             check_launch(*c);
         }
@@ -491,6 +513,7 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
             auto k = dev::k_seg_prod<S4, C::TH, kPiece>;
             constexpr int NI = dev::kBlock / C::TH;
             const int grid = occupancy_grid(*c, k, 2 * P, NI);
+            ProfScope prof_(*c, 0);
             k<<<grid, dev::kBlock, 0, st>>>(arg(c->mod_n2), pieces, P, pass == 0 ? sorted : nullptr, src, dst);
             check_launch(*c);
             final_idx = ps;
@@ -693,6 +716,38 @@ int sfxb_ctx_has_private(const sfxb_ctx *c) { return c->has_priv ? 1 : 0; }
 uint64_t sfxb_ctx_key_id(const sfxb_ctx *c) { return c->key_id; }
 uint64_t sfxb_ctx_launches(const sfxb_ctx *c) { return c->launches; }
 void *sfxb_ctx_stream(sfxb_ctx *c) { return (void *)c->stream; }
+int sfxb_ctx_profile(sfxb_ctx *c, int enable) {
+    return guard(c, [&] {
+        CK(cudaStreamSynchronize(c->stream));
+        for (auto &p : c->prof) {
+            for (auto &e : p.ev) {
+                cudaEventDestroy(e.first);
+                cudaEventDestroy(e.second);
+            }
+            p = CtxState::Prof{};
+        }
+        c->profile = enable != 0;
+    });
+}
+
+int sfxb_ctx_kernel_time(sfxb_ctx *c, int family, uint64_t *launches, double *ms) {
+    return guard(c, [&] {
+        if (family < 0 || family >= 4) throw ApiError(SFXB_ERR_ARG, "kernel family out of range");
+        CK(cudaStreamSynchronize(c->stream));
+        auto &p = c->prof[family];
+        for (auto &e : p.ev) {
+            float t = 0;
+            CK(cudaEventElapsedTime(&t, e.first, e.second));
+            p.ms_done += t;
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
+        p.ev.clear();
+        *launches = p.launches;
+        *ms = p.ms_done;
+    });
+}
+
 int sfxb_ctx_sync(sfxb_ctx *c) {
     return guard(c, [&] { CK(cudaStreamSynchronize(c->stream)); });
 }
@@ -868,6 +923,27 @@ int sfxb_accumulate(sfxb_ctx *c, const uint32_t *gh_cts, uint32_t n_samples, con
         CK(cudaMemcpyAsync(doff.p, node_offsets, ((size_t)N + 1) * 4, cudaMemcpyHostToDevice, c->stream));
         if (R) CK(cudaMemcpyAsync(drows.p, rows, (size_t)R * 4, cudaMemcpyHostToDevice, c->stream));
         accumulate_dev(c, g.get(), db.p, J, doff.p, N, drows.p, R, K, dout.p, 0, additions);
+        d2h_padded(c, out_slots, dout.p, nslots, 2 * c->nw, S4);
+    });
+}
+
+int sfxb_accumulate_gh(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *bins, uint32_t J, const uint32_t *node_offsets,
+                       uint32_t N, const uint32_t *rows, uint32_t K, uint32_t *out_slots, uint64_t *additions) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (!g || g->ctx != c) throw ApiError(SFXB_ERR_ARG, "accumulate: gradient handle belongs to another context");
+        for (uint32_t i = 0; i < N; ++i)
+            if (node_offsets[i + 1] < node_offsets[i]) throw ApiError(SFXB_ERR_ARG, "accumulate: node offsets decrease");
+        if (N && node_offsets[0] != 0) throw ApiError(SFXB_ERR_ARG, "accumulate: node offsets must start at 0");
+        const uint32_t R = N ? node_offsets[N] : 0;
+        const size_t S4 = 4 * (size_t)c->s, nslots = 2ull * N * J * K, n_samples = g->n_samples;
+        DevBuf<uint16_t> db((size_t)J * n_samples);
+        DevBuf<uint32_t> doff((size_t)N + 1), drows(R ? R : 1), dout(nslots * S4);
+        if ((size_t)J * n_samples)
+            CK(cudaMemcpyAsync(db.p, bins, (size_t)J * n_samples * 2, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(doff.p, node_offsets, ((size_t)N + 1) * 4, cudaMemcpyHostToDevice, c->stream));
+        if (R) CK(cudaMemcpyAsync(drows.p, rows, (size_t)R * 4, cudaMemcpyHostToDevice, c->stream));
+        accumulate_dev(c, g, db.p, J, doff.p, N, drows.p, R, K, dout.p, 0, additions);
         d2h_padded(c, out_slots, dout.p, nslots, 2 * c->nw, S4);
     });
 }

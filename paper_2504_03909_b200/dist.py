@@ -1,0 +1,68 @@
+"""Row-sharded multi-GPU encrypted histogram.
+
+One process per GPU.  Each rank holds the gradient ciphertexts and bin
+columns of a contiguous row range and builds PARTIAL histograms (Montgomery
+form, every slot a product over its own rows only).  Homomorphic addition is a
+modular product, so the partials cannot be combined by an NCCL sum; instead
+
+  1. the slot axis is cut into `world` equal slices (padded),
+  2. ``all_to_all_single`` sends slice s of every rank's partial to rank s
+     (each rank receives world × slice, moving (world−1)/world of one partial
+     instead of the (world−1) partials of an all-gather),
+  3. rank s multiplies its world slices element-wise with the K4 kernel
+     (sfxb_reduce_partials_dev) into the plain-form result for its slice.
+
+The collective and the layout logic are independent of the reduce, so the
+CPU tests drive the same functions with the gloo backend and an oracle
+reduce (tests/test_dist_cpu.py).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def row_shard(n_rows: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous row range of `rank` (sizes differ by at most one)."""
+    base, extra = divmod(n_rows, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def slice_len(n_slots: int, world: int) -> int:
+    return (n_slots + world - 1) // world
+
+
+def padded_slots(n_slots: int, world: int) -> int:
+    return slice_len(n_slots, world) * world
+
+
+def exchange(partial: torch.Tensor, world: int, group=None) -> torch.Tensor:
+    """partial: [padded_slots, ct_words] on this rank -> [world, slice, ct_words]
+    holding slice `rank` of every rank's partial (rank-major)."""
+    assert partial.shape[0] % world == 0
+    recv = torch.empty_like(partial)
+    if world == 1:
+        recv.copy_(partial)
+    else:
+        dist.all_to_all_single(recv, partial.contiguous(), group=group)
+    return recv.view(world, partial.shape[0] // world, partial.shape[1])
+
+
+def reduce_slice(recv: torch.Tensor, reduce_fn) -> torch.Tensor:
+    """Combine the world partial slices element-wise with `reduce_fn(parts,
+    n_parts, n_slots, out)` (the K4 kernel on GPU)."""
+    world, sl, cw = recv.shape
+    out = torch.empty((sl, cw), dtype=recv.dtype, device=recv.device)
+    reduce_fn(recv, world, sl, out)
+    return out
+
+
+def gather_slices(local: torch.Tensor, n_slots: int, world: int, group=None) -> torch.Tensor:
+    """All ranks' reduced slices -> the full [n_slots, ct_words] histogram
+    (what the active party collects)."""
+    if world == 1:
+        return local[:n_slots]
+    parts = [torch.empty_like(local) for _ in range(world)]
+    dist.all_gather(parts, local.contiguous(), group=group)
+    return torch.cat(parts, 0)[:n_slots]
