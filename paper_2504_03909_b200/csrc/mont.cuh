@@ -268,25 +268,30 @@ __device__ __forceinline__ void final_sub(uint32_t (&R)[L], uint32_t over, const
 
 // r = A·B·2^(−32S) mod M.  A, N: this lane's L limbs; B: instance operand in
 // shared memory (store_b layout); np = −M⁻¹ mod 2^32.  r may alias A.
+//
+// All S iterations run the same (non-peeled) step on a zero-initialised
+// accumulator, and the pair loop is unrolled by L/2: one trip of the
+// unrolled body rotates both accumulator arrays through all L/2 register
+// pairs, so the per-step limb shift is pure register renaming (no MOVs
+// competing with IMAD.WIDE for the FMA-heavy pipe).
 template <int S, int TPI>
 __device__ __forceinline__ void mont_mul(uint32_t (&r)[S / TPI], const uint32_t (&A)[S / TPI],
                                          const uint2 *sB, int NI, int inst,
                                          const uint32_t (&N)[S / TPI], uint32_t np) {
     constexpr int L = S / TPI;
+    constexpr int U = (L / 2 <= S / 2 && (S / 2) % (L / 2) == 0) ? L / 2 : 1;
     uint32_t X[L], Y[L], Z = 0;
-    // pair 0: iteration 0 (E=X, fresh) and 1 (E=Y)
-    uint2 b = sB[inst];
-    cios_step<L, TPI>(X, Y, Z, A, N, b.x, np, true);
-    cios_step<L, TPI>(Y, X, Z, A, N, b.y, np, false);
-#pragma unroll 1
-    for (int i = 1; i < S / 2; ++i) {
-        b = sB[i * NI + inst];
+#pragma unroll
+    for (int k = 0; k < L; ++k) X[k] = Y[k] = 0;
+#pragma unroll U
+    for (int i = 0; i < S / 2; ++i) {
+        const uint2 b = sB[i * NI + inst];
         cios_step<L, TPI>(X, Y, Z, A, N, b.x, np, false);
         cios_step<L, TPI>(Y, X, Z, A, N, b.y, np, false);
     }
-    // After the last step E = Y, raw = X.  Apply the final shift and merge:
-    // window limb k = X... no: E (=Y) is the old even array -> it shifts down,
-    // O (=X) becomes the even-aligned array.
+    // After the last step E = Y (the old even array, still unshifted) and X
+    // holds the odd-aligned array, which becomes the even-aligned window; Y
+    // shifts down one limb: window limb k = X[k] + Y[k+1] (+ lane t+1's Y[0]).
     const uint32_t u0 = from_above<TPI>(Y[0]);
     uint32_t R[L];
     R[0] = add_cc(X[0], Y[1]);

@@ -129,15 +129,15 @@ struct Cls<4> {
 };
 template <>
 struct Cls<8> {
-    static constexpr int T1 = 1, T2 = 1, TC = 2, TD = 1, TE = 2, TH = 2, TN = 2;
+    static constexpr int T1 = 1, T2 = 1, TC = 2, TD = 1, TE = 1, TH = 2, TN = 2;
 };
 template <>
 struct Cls<16> {
-    static constexpr int T1 = 1, T2 = 2, TC = 2, TD = 2, TE = 2, TH = 2, TN = 2;
+    static constexpr int T1 = 1, T2 = 2, TC = 4, TD = 2, TE = 2, TH = 4, TN = 4;
 };
 template <>
 struct Cls<32> {
-    static constexpr int T1 = 2, T2 = 2, TC = 4, TD = 2, TE = 4, TH = 4, TN = 4;
+    static constexpr int T1 = 2, T2 = 4, TC = 8, TD = 4, TE = 4, TH = 8, TN = 8;
 };
 template <>
 struct Cls<48> {
