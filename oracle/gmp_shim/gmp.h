@@ -1,7 +1,7 @@
 /* TEST INFRASTRUCTURE ONLY (oracle/).
  *
  * Minimal C declarations for the subset of GMP 6.3.0 that the reference
- * (`/root/reference/proj/src/*.cpp`, see SURVEY.md §8c "Shim surface") and
+ * (the .cpp files under /root/reference/proj/src, SURVEY.md §8c "Shim surface") and
  * our oracle restatement call.  The image ships the GMP *runtime*
  * (`/usr/lib/x86_64-linux-gnu/libgmp.so.10`, GMP 6.3.0) but not its headers,
  * so this file restates the public ABI: struct layouts (`__mpz_struct`,

@@ -1,0 +1,458 @@
+// CudaPaillierPlugin: the reference's sfxb::EncryptionPlugin backed by the
+// B200 kernels through the C ABI (include/sfxb_cuda.h).
+//
+// Drop-in: this library defines both sfxb::make_paillier_plugin overloads
+// (secure_processor.hpp:155-158).  Loaded ahead of the reference library
+// (link order or LD_PRELOAD) it takes over every plugin the reference creates,
+// including make_plugin in run_vertical_histogram (federation.cpp:76-86) —
+// INTEGRATION.md.  Behaviour mirrors PaillierPlugin (secure_processor.cpp:
+// 553-746) exactly:
+//   * encrypt_gh draws the blinding factors from the same GMP Mersenne-Twister
+//     stream as HeRng (he.cpp:11-28: seed via mpz_import, mpz_urandomm,
+//     reject r <= 1 and gcd(r, n) != 1) in the same order (g0, h0, g1, ...),
+//     so ciphertexts are byte-identical; encode_fixed checks and counters
+//     advance exactly as the reference would, including on failure;
+//   * accumulate_rows / decrypt_histogram keep the reference's validation
+//     order, messages, slot layout, trivial-zero handling and counter laws;
+//   * the packed (horizontal) vector path is outside the GPU scope and is
+//     delegated to the reference implementation (dlsym RTLD_NEXT), with its
+//     counter deltas folded into ours.
+#include <dlfcn.h>
+#include <gmp.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "sfxb/errors.hpp"
+#include "sfxb/secure_processor.hpp"
+#include "sfxb_cuda.h"
+
+namespace sfxb {
+namespace {
+
+// ------------------------------------------------------------ helpers
+
+unsigned host_threads() {
+    static unsigned n = [] {
+        if (const char *e = std::getenv("SFXB_HOST_THREADS")) return (unsigned)std::max(1, std::atoi(e));
+        unsigned h = std::thread::hardware_concurrency();
+        return h ? std::min(h, 32u) : 4u;
+    }();
+    return n;
+}
+
+template <typename F>
+void parallel_for(size_t n, F &&f) {
+    const unsigned T = host_threads();
+    if (n < 4096 || T <= 1) {
+        f(size_t(0), n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const size_t chunk = (n + T - 1) / T;
+    for (unsigned t = 0; t < T; ++t) {
+        size_t lo = t * chunk, hi = std::min(n, lo + chunk);
+        if (lo >= hi) break;
+        pool.emplace_back([&, lo, hi] { f(lo, hi); });
+    }
+    for (auto &th : pool) th.join();
+}
+
+// mpz <-> little-endian u32 limbs (x86-64 GMP limbs are 64-bit little endian,
+// byte-identical to pairs of u32 limbs): raw limb copies, no mpz_import.
+static_assert(sizeof(mp_limb_t) == 8, "64-bit GMP limbs expected");
+
+void to_words(const mpz_class &z, uint32_t *out, size_t words) {
+    const size_t used = mpz_size(z.get_mpz_t());
+    if (used * 2 > words + 1 || mpz_sgn(z.get_mpz_t()) < 0) {
+        // does not fit (or negative): caller reports a range error
+        std::memset(out, 0xff, words * 4);
+        return;
+    }
+    std::memset(out, 0, words * 4);
+    const mp_limb_t *l = mpz_limbs_read(z.get_mpz_t());
+    const size_t bytes = std::min(used * 8, words * 4);
+    std::memcpy(out, l, bytes);
+    if (used * 8 > words * 4 && (l[used - 1] >> 32) != 0) std::memset(out, 0xff, words * 4);
+}
+
+bool fits(const mpz_class &z, size_t words) {
+    return mpz_sgn(z.get_mpz_t()) >= 0 && mpz_sizeinbase(z.get_mpz_t(), 2) <= 32 * words;
+}
+
+void from_words(mpz_class &z, const uint32_t *w, size_t words) {
+    size_t n64 = (words + 1) / 2;
+    while (n64 > 0) {
+        const uint32_t lo = w[2 * (n64 - 1)], hi = 2 * (n64 - 1) + 1 < words ? w[2 * (n64 - 1) + 1] : 0;
+        if (lo | hi) break;
+        --n64;
+    }
+    mp_limb_t *l = mpz_limbs_write(z.get_mpz_t(), (mp_size_t)std::max<size_t>(n64, 1));
+    for (size_t i = 0; i < n64; ++i) {
+        const uint32_t lo = w[2 * i], hi = 2 * i + 1 < words ? w[2 * i + 1] : 0;
+        l[i] = (mp_limb_t)lo | ((mp_limb_t)hi << 32);
+    }
+    mpz_limbs_finish(z.get_mpz_t(), (mp_size_t)n64);
+}
+
+// the reference implementation, for the out-of-scope packed path
+using Factory = std::unique_ptr<EncryptionPlugin> (*)(const PaillierKeypair &, const PaillierPluginConfig &);
+using FactoryPub = std::unique_ptr<EncryptionPlugin> (*)(const PaillierPublicKey &, const PaillierPluginConfig &);
+
+// ------------------------------------------------------------ the plugin
+
+class CudaPaillierPlugin final : public EncryptionPlugin {
+public:
+    CudaPaillierPlugin(const PaillierPublicKey &pk, const PaillierPluginConfig &cfg)
+        : pub_(pk), has_priv_(false), cfg_(cfg), scale_bits_(cfg.scale_bits) {
+        init_rng(cfg.rng_seed);
+        open_ctx(nullptr);
+    }
+    CudaPaillierPlugin(const PaillierKeypair &kp, const PaillierPluginConfig &cfg)
+        : pub_(kp.pub), priv_(kp.priv), has_priv_(true), kp_(kp), cfg_(cfg), scale_bits_(cfg.scale_bits) {
+        init_rng(cfg.rng_seed);
+        open_ctx(&kp);
+    }
+    ~CudaPaillierPlugin() override {
+        if (gh_) sfxb_gh_free(gh_);
+        if (ctx_) sfxb_ctx_destroy(ctx_);
+        gmp_randclear(rng_);
+    }
+
+    std::string name() const override { return "paillier"; }
+    bool is_passthrough() const override { return false; }
+    bool holds_private_key() const override { return has_priv_; }
+    std::uint64_t key_id() const override { return pub_.key_id; }
+
+    // ---- encrypt_gh (secure_processor.cpp:574-585)
+    GhPayload encrypt_gh(std::span<const GHPair> gh) override {
+        GhPayload out;
+        out.encrypted = true;
+        out.n_samples = static_cast<std::uint32_t>(gh.size());
+        const size_t count = 2 * gh.size();
+        std::vector<int64_t> q(count);
+        // encode_fixed checks in the reference's order; on the first failure
+        // the reference has drawn one r per successful encryption before it
+        size_t ok = 0;
+        std::string fail_msg;
+        for (size_t i = 0; i < count; ++i) {
+            const double x = (i & 1) ? gh[i / 2].h : gh[i / 2].g;
+            int64_t v = 0;
+            if (sfxb_encode_check(ctx_, x, scale_bits_, &v) != SFXB_OK) {
+                fail_msg = sfxb_last_error(ctx_);
+                break;
+            }
+            q[i] = v;
+            ++ok;
+        }
+        const size_t nw = n_words_;
+        std::vector<uint32_t> r(ok * nw);
+        draw_blinding(r.data(), ok);
+        if (ok < count) {
+            counters_.encryptions += 2 * (ok / 2); // pairs completed before the failure
+            throw Error(fail_msg);
+        }
+        std::vector<uint32_t> cts(count * ct_words_);
+        std::vector<uint8_t> flags(count, 0);
+        int rc = sfxb_encrypt(ctx_, q.data(), r.data(), count, cts.data(), flags.data());
+        if (rc == SFXB_ERR_COPRIME) {
+            // some r shares a factor with n (probability ~2^-1000): redo the
+            // draw with the reference's exact rejection rule from the saved state
+            gmp_randclear(rng_);
+            gmp_randinit_set(rng_, rng_snapshot_);
+            draw_blinding(r.data(), ok, /*exact_gcd=*/true);
+            rc = sfxb_encrypt(ctx_, q.data(), r.data(), count, cts.data(), nullptr);
+        }
+        check(rc);
+        out.cts.resize(count);
+        parallel_for(count, [&](size_t lo, size_t hi) {
+            for (size_t i = lo; i < hi; ++i) {
+                from_words(out.cts[i].value, &cts[i * ct_words_], ct_words_);
+                out.cts[i].key_id = pub_.key_id;
+            }
+        });
+        counters_.encryptions += count;
+        return out;
+    }
+
+    // ---- accumulate_rows (secure_processor.cpp:587-620)
+    HistogramPayload accumulate_rows(const GhPayload &gh, const std::vector<std::vector<std::uint16_t>> &bins,
+                                     const std::vector<int> &feature_ids, const std::vector<NodeRows> &nodes,
+                                     int n_bins) override {
+        if (!gh.encrypted) throw Error("paillier accumulate expects encrypted gradients");
+        if (gh.cts.size() != 2ull * gh.n_samples)
+            throw Error("row-count mismatch: ciphertext count is not 2·n_samples");
+        for (const auto &col : bins)
+            if (col.size() != gh.n_samples) throw Error("row-count mismatch between bins and gradients");
+        if (bins.size() < feature_ids.size()) throw Error("row-count mismatch between bins and gradients");
+        HistogramPayload out;
+        out.layout = HistLayout::enc_scalar;
+        const size_t J = feature_ids.size(), K = (size_t)std::max(n_bins, 0), N = nodes.size();
+        // bins are checked per visited row, as the reference loop does
+        for (const NodeRows &nd : nodes)
+            for (size_t f = 0; f < J; ++f)
+                for (std::uint32_t row : nd.rows) {
+                    if (row >= gh.n_samples) throw Error("row index out of range in accumulate");
+                    if (bins[f][row] >= static_cast<std::uint16_t>(n_bins))
+                        throw Error("bin index out of range in accumulate");
+                }
+        ensure_gh(gh);
+        std::vector<uint16_t> flat(J * gh.n_samples);
+        for (size_t f = 0; f < J; ++f) std::memcpy(&flat[f * gh.n_samples], bins[f].data(), gh.n_samples * 2);
+        std::vector<uint32_t> offs(N + 1, 0), rows;
+        for (size_t i = 0; i < N; ++i) offs[i + 1] = offs[i] + (uint32_t)nodes[i].rows.size();
+        rows.reserve(offs[N]);
+        for (const NodeRows &nd : nodes) rows.insert(rows.end(), nd.rows.begin(), nd.rows.end());
+        std::vector<uint32_t> slots(N * J * K * 2 * ct_words_);
+        uint64_t adds = 0;
+        if (N && J && K)
+            check(sfxb_accumulate_gh(ctx_, gh_, flat.data(), (uint32_t)J, offs.data(), (uint32_t)N, rows.data(),
+                                     (uint32_t)K, slots.data(), &adds));
+        counters_.ciphertext_additions += adds;
+        const size_t per_node = 2 * J * K;
+        out.nodes.resize(N);
+        for (size_t i = 0; i < N; ++i) {
+            NodeHistogram &nh = out.nodes[i];
+            nh.node_id = nodes[i].node_id;
+            nh.feature_ids = feature_ids;
+            nh.n_bins = n_bins;
+            nh.scalar_cts.resize(per_node);
+        }
+        parallel_for(N * per_node, [&](size_t lo, size_t hi) {
+            for (size_t s = lo; s < hi; ++s) {
+                Ciphertext &c = out.nodes[s / per_node].scalar_cts[s % per_node];
+                from_words(c.value, &slots[s * ct_words_], ct_words_);
+                c.key_id = pub_.key_id;
+            }
+        });
+        return out;
+    }
+
+    // ---- decrypt_histogram (secure_processor.cpp:679-719)
+    std::vector<std::pair<std::uint32_t, Histogram>> decrypt_histogram(const HistogramPayload &payload) override {
+        if (!has_priv_) throw AuthorizationError("decrypt requested without private key material");
+        if (payload.layout != HistLayout::enc_scalar) {
+            if (payload.layout == HistLayout::enc_packed) return delegate_decrypt(payload);
+            throw Error("paillier decrypt expects encrypted layouts");
+        }
+        std::vector<std::pair<std::uint32_t, Histogram>> out;
+        size_t total = 0;
+        for (const NodeHistogram &node : payload.nodes)
+            total += 2 * node.feature_ids.size() * (size_t)std::max(node.n_bins, 0);
+        std::vector<uint32_t> cts(total * ct_words_);
+        // the reference decrypts slot by slot: key and range errors surface at
+        // the first offending non-trivial slot in that order
+        size_t base = 0;
+        for (const NodeHistogram &node : payload.nodes) {
+            const size_t cnt = 2 * node.feature_ids.size() * (size_t)std::max(node.n_bins, 0);
+            if (node.scalar_cts.size() < cnt) throw Error("decrypt_histogram: scalar slot count mismatch");
+            for (size_t s = 0; s < cnt; ++s) {
+                const Ciphertext &c = node.scalar_cts[s];
+                if (c.value == 1) {
+                    std::memset(&cts[(base + s) * ct_words_], 0, ct_words_ * 4);
+                    cts[(base + s) * ct_words_] = 1;
+                    continue;
+                }
+                if (c.key_id != pub_.key_id) throw Error("decrypt: ciphertext key mismatch");
+                if (c.value < 1 || c.value >= pub_.n2 || !fits(c.value, ct_words_))
+                    throw Error("decrypt: ciphertext out of range");
+                to_words(c.value, &cts[(base + s) * ct_words_], ct_words_);
+            }
+            base += cnt;
+        }
+        std::vector<double> vals(total);
+        uint64_t decs = 0;
+        if (total) check(sfxb_decrypt(ctx_, cts.data(), total, scale_bits_, vals.data(), nullptr, &decs));
+        counters_.decryptions += decs;
+        base = 0;
+        for (const NodeHistogram &node : payload.nodes) {
+            Histogram hist;
+            hist.n_bins = node.n_bins;
+            hist.feature_ids = node.feature_ids;
+            hist.feats.assign(node.feature_ids.size(), std::vector<GHPair>(static_cast<std::size_t>(node.n_bins)));
+            for (std::size_t f = 0; f < node.feature_ids.size(); ++f)
+                for (int b = 0; b < node.n_bins; ++b) {
+                    const size_t s = base + 2 * (f * (size_t)node.n_bins + (size_t)b);
+                    hist.feats[f][b] = GHPair{vals[s], vals[s + 1]};
+                }
+            base += 2 * node.feature_ids.size() * (size_t)std::max(node.n_bins, 0);
+            out.emplace_back(node.node_id, std::move(hist));
+        }
+        return out;
+    }
+
+    // ---- packed (horizontal) path: the reference implementation
+    HistogramPayload encrypt_histogram(const std::vector<std::pair<std::uint32_t, Histogram>> &h) override {
+        return delegated<HistogramPayload>([&](EncryptionPlugin &p) { return p.encrypt_histogram(h); });
+    }
+    HistogramPayload add_histograms(const std::vector<HistogramPayload> &parts) override {
+        return delegated<HistogramPayload>([&](EncryptionPlugin &p) { return p.add_histograms(parts); });
+    }
+
+private:
+    void open_ctx(const PaillierKeypair *kp) {
+        const int dev = std::getenv("SFXB_CUDA_DEVICE") ? std::atoi(std::getenv("SFXB_CUDA_DEVICE")) : 0;
+        n_words_ = (mpz_sizeinbase(pub_.n.get_mpz_t(), 2) + 31) / 32;
+        std::vector<uint32_t> n(n_words_);
+        to_words(pub_.n, n.data(), n_words_);
+        int rc;
+        if (kp) {
+            size_t pw = (std::max(mpz_sizeinbase(kp->priv.p.get_mpz_t(), 2), mpz_sizeinbase(kp->priv.q.get_mpz_t(), 2)) + 31) / 32;
+            std::vector<uint32_t> p(pw), q(pw);
+            to_words(kp->priv.p, p.data(), pw);
+            to_words(kp->priv.q, q.data(), pw);
+            rc = sfxb_ctx_create(&ctx_, dev, n.data(), (uint32_t)n_words_, p.data(), q.data(), (uint32_t)pw);
+        } else {
+            rc = sfxb_ctx_create(&ctx_, dev, n.data(), (uint32_t)n_words_, nullptr, nullptr, 0);
+        }
+        if (rc != SFXB_OK) throw Error(std::string("CUDA Paillier plugin: ") + sfxb_create_error());
+        ct_words_ = sfxb_ctx_ct_words(ctx_);
+    }
+
+    // HeRng(seed) (he.cpp:11-15)
+    void init_rng(std::uint64_t seed) {
+        gmp_randinit_mt(rng_);
+        mpz_class s;
+        mpz_import(s.get_mpz_t(), 1, 1, sizeof seed, 0, 0, &seed);
+        gmp_randseed(rng_, s.get_mpz_t());
+        gmp_randinit_mt(rng_snapshot_);
+    }
+
+    // `count` draws of HeRng::unit_below(n) (he.cpp:19-28).  With p, q the
+    // gcd test is done on the device (p | r or q | r, SFXB_ERR_COPRIME) and the
+    // state before the batch is kept for an exact replay; without them the
+    // gcd runs here.
+    void draw_blinding(uint32_t *out, size_t count, bool exact_gcd = false) {
+        gmp_randclear(rng_snapshot_);
+        gmp_randinit_set(rng_snapshot_, rng_);
+        const bool host_gcd = exact_gcd || !has_priv_;
+        mpz_class r, g;
+        for (size_t i = 0; i < count; ++i) {
+            for (;;) {
+                mpz_urandomm(r.get_mpz_t(), rng_, pub_.n.get_mpz_t());
+                if (r <= 1) continue;
+                if (host_gcd) {
+                    mpz_gcd(g.get_mpz_t(), r.get_mpz_t(), pub_.n.get_mpz_t());
+                    if (g != 1) continue;
+                }
+                break;
+            }
+            to_words(r, out + i * n_words_, n_words_);
+        }
+    }
+
+    // Device-resident gh keyed on the ciphertext contents: one parallel
+    // read-only pass hashes the mpz limbs (and applies the checks); only on a
+    // miss are the limbs marshalled and uploaded (sfxb_gh_upload).
+    void ensure_gh(const GhPayload &gh) {
+        const size_t count = gh.cts.size();
+        constexpr size_t kChunk = 4096;
+        const size_t nchunks = (count + kChunk - 1) / kChunk;
+        std::vector<uint64_t> part(nchunks, 0);
+        std::atomic<bool> bad_key{false}, bad_range{false};
+        parallel_for(nchunks, [&](size_t lo, size_t hi) {
+            for (size_t ch = lo; ch < hi; ++ch) {
+                uint64_t h = 14695981039346656037ULL;
+                for (size_t i = ch * kChunk; i < std::min(count, (ch + 1) * kChunk); ++i) {
+                    const Ciphertext &c = gh.cts[i];
+                    if (c.key_id != pub_.key_id) bad_key = true;
+                    if (!fits(c.value, ct_words_)) bad_range = true;
+                    const size_t used = mpz_size(c.value.get_mpz_t());
+                    const mp_limb_t *l = mpz_limbs_read(c.value.get_mpz_t());
+                    for (size_t k = 0; k < used; ++k) {
+                        h ^= l[k];
+                        h *= 1099511628211ULL;
+                    }
+                    h ^= used + 0x51;
+                    h *= 1099511628211ULL;
+                }
+                part[ch] = h;
+            }
+        });
+        if (bad_range) throw Error("add_ciphertexts: ciphertext out of range");
+        if (bad_key) throw Error("add_ciphertexts: key mismatch");
+        uint64_t h = (uint64_t)count * 0x9E3779B97F4A7C15ull;
+        for (uint64_t x : part) h = (h ^ x) * 1099511628211ULL;
+        if (gh_ && gh_hash_ == h && gh_count_ == count) return;
+        if (gh_) sfxb_gh_free(gh_);
+        gh_ = nullptr;
+        std::vector<uint32_t> limbs(count * ct_words_);
+        parallel_for(count, [&](size_t lo, size_t hi) {
+            for (size_t i = lo; i < hi; ++i) to_words(gh.cts[i].value, &limbs[i * ct_words_], ct_words_);
+        });
+        check(sfxb_gh_upload(ctx_, limbs.data(), gh.n_samples, &gh_));
+        gh_hash_ = h;
+        gh_count_ = count;
+    }
+
+    void check(int rc) {
+        if (rc == SFXB_OK) return;
+        std::string msg = sfxb_last_error(ctx_);
+        if (rc == SFXB_ERR_AUTH) throw AuthorizationError(msg);
+        throw Error(msg);
+    }
+
+    EncryptionPlugin &reference() {
+        if (!ref_) {
+            const char *kp_sym = "_ZN4sfxb20make_paillier_pluginERKNS_15PaillierKeypairERKNS_20PaillierPluginConfigE";
+            const char *pk_sym = "_ZN4sfxb20make_paillier_pluginERKNS_17PaillierPublicKeyERKNS_20PaillierPluginConfigE";
+            if (has_priv_) {
+                auto f = reinterpret_cast<Factory>(dlsym(RTLD_NEXT, kp_sym));
+                if (!f) throw Error("CUDA Paillier plugin: reference factory not found for the packed path");
+                ref_ = f(kp_, cfg_);
+            } else {
+                auto f = reinterpret_cast<FactoryPub>(dlsym(RTLD_NEXT, pk_sym));
+                if (!f) throw Error("CUDA Paillier plugin: reference factory not found for the packed path");
+                ref_ = f(pub_, cfg_);
+            }
+        }
+        return *ref_;
+    }
+    template <typename R, typename F>
+    R delegated(F &&f) {
+        EncryptionPlugin &r = reference();
+        const OpCounters before = r.counters();
+        R res = f(r);
+        counters_ += r.counters() - before;
+        return res;
+    }
+    std::vector<std::pair<std::uint32_t, Histogram>> delegate_decrypt(const HistogramPayload &p) {
+        return delegated<std::vector<std::pair<std::uint32_t, Histogram>>>(
+            [&](EncryptionPlugin &r) { return r.decrypt_histogram(p); });
+    }
+
+    PaillierPublicKey pub_;
+    PaillierPrivateKey priv_;
+    bool has_priv_;
+    PaillierKeypair kp_;
+    PaillierPluginConfig cfg_;
+    unsigned scale_bits_;
+    gmp_randstate_t rng_, rng_snapshot_;
+    sfxb_ctx *ctx_ = nullptr;
+    size_t n_words_ = 0, ct_words_ = 0;
+    sfxb_gh *gh_ = nullptr;
+    uint64_t gh_hash_ = 0;
+    size_t gh_count_ = 0;
+    std::unique_ptr<EncryptionPlugin> ref_;
+};
+
+} // namespace
+
+// ------------------------------------------------------------ the factories (interposed)
+
+std::unique_ptr<EncryptionPlugin> make_paillier_plugin(const PaillierPublicKey &pk, const PaillierPluginConfig &cfg) {
+    return std::make_unique<CudaPaillierPlugin>(pk, cfg);
+}
+
+std::unique_ptr<EncryptionPlugin> make_paillier_plugin(const PaillierKeypair &kp, const PaillierPluginConfig &cfg) {
+    return std::make_unique<CudaPaillierPlugin>(kp, cfg);
+}
+
+} // namespace sfxb

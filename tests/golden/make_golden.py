@@ -94,5 +94,32 @@ def main():
         print("wrote", path, os.path.getsize(path), flush=True)
 
 
+TRAIN_CONFIGS = {
+    # name: (ini under tests/configs, key bits, key seed)
+    "vertical_toy512": ("vertical_toy512.ini", 512, 0xACCE55),
+    "vertical_threaded_3p": ("vertical_threaded_3p.ini", 512, 0xC0FFEE),
+    "vertical_c1_1024": ("vertical_c1_1024.ini", 1024, 7),
+}
+
+
+def train_goldens(names=None):
+    """run_training with the reference CPU plugin -> tests/golden/train_<name>.json"""
+    import subprocess
+
+    drv = os.path.join(ROOT, "tests", "train_driver.py")
+    for name, (ini, bits, seed) in TRAIN_CONFIGS.items():
+        if names and name not in names:
+            continue
+        out = subprocess.run([sys.executable, drv, os.path.join(ROOT, "tests", "configs", ini), str(bits), str(seed)],
+                             check=True, capture_output=True, text=True).stdout
+        path = os.path.join(HERE, f"train_{name}.json")
+        with open(path, "w") as f:
+            f.write(out)
+        print("wrote", path, flush=True)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "train":
+        train_goldens(sys.argv[2:] or None)
+    else:
+        main()
