@@ -129,10 +129,13 @@ __global__ void k_emit_pieces(const uint32_t *seg_start, const uint32_t *seg_len
 //   pass>1: prev[(start+k)·2 + gh]·S            (contiguous partials)
 // Every instance of a warp runs the same number of Montgomery products
 // (shorter pieces keep their accumulator), exiting when the warp is done.
+// Pieces are visited in `order` (sorted by length, longest first) so that the
+// instances of a warp run pieces of (nearly) equal length; partial j is
+// written at the piece's own index, keeping each key's partials contiguous.
 template <int S, int TPI, int C>
-__global__ void __launch_bounds__(kBlock) k_seg_prod(ModArg M, const Piece *pieces, size_t n_pieces,
-                                                     const uint32_t *sorted, const uint32_t *src,
-                                                     uint32_t *dst) {
+__global__ void __launch_bounds__(kBlock) k_seg_prod(ModArg M, const Piece *pieces, const uint32_t *order,
+                                                     size_t n_pieces, const uint32_t *sorted,
+                                                     const uint32_t *src, uint32_t *dst) {
     constexpr int L = S / TPI, NI = kBlock / TPI;
     __shared__ uint2 sB[S / 2 * NI];
     const Stage st = make_stage<TPI>(sB);
@@ -140,7 +143,8 @@ __global__ void __launch_bounds__(kBlock) k_seg_prod(ModArg M, const Piece *piec
     uint32_t N[L];
     load_const<S, TPI>(N, mr, kMod);
     SFXB_UNIFORM_LOOP(job, active, 2 * n_pieces) {
-        const Piece pc = pieces[job >> 1];
+        const uint32_t pidx = order[job >> 1];
+        const Piece pc = pieces[pidx];
         const uint32_t g = (uint32_t)(job & 1);
         auto item_ptr = [&](uint32_t k) -> const uint32_t * {
             const size_t idx = sorted ? (2 * (size_t)sorted[pc.start + k] + g) : (2 * (size_t)(pc.start + k) + g);
@@ -157,7 +161,15 @@ __global__ void __launch_bounds__(kBlock) k_seg_prod(ModArg M, const Piece *piec
 #pragma unroll
             for (int w = 0; w < L; ++w) acc[w] = more ? r[w] : acc[w];
         }
-        if (active) store_lane<S, TPI>(dst + job * S, acc);
+        if (active) store_lane<S, TPI>(dst + (2 * (size_t)pidx + g) * S, acc);
+    }
+}
+
+// sort keys for the pieces: (length, index)
+__global__ void k_piece_keys(const Piece *pieces, size_t n, uint32_t *len, uint32_t *idx) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        len[i] = pieces[i].len;
+        idx[i] = (uint32_t)i;
     }
 }
 

@@ -361,10 +361,12 @@ void add_dev(sfxb_ctx *c, const uint32_t *d_a, const uint32_t *d_b, size_t count
 
 // --------------------------------------------------------------- histogram (K2)
 
-constexpr int kPiece = 16; // items per segmented-product piece
+// items per segmented-product piece: long segments use kPieceLong (fewer
+// partials / passes), short ones kPiece (less tail work)
+constexpr int kPiece = 16, kPieceLong = 64;
 
 struct HistBufs {
-    Buf node_of, count, ones, cursor, seg_start, sorted, np, piece_start, pieces, part[2], cub, misc;
+    Buf node_of, count, ones, cursor, seg_start, sorted, np, piece_start, pieces, part[2], cub, misc, plen, pord;
 };
 HistBufs &hist_bufs(sfxb_ctx *c) {
     static thread_local std::map<sfxb_ctx *, HistBufs> m; // per context, per thread
@@ -495,10 +497,14 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
         using C = Cls<cs>;
         constexpr int S4 = 4 * cs;
         const int g1 = (int)std::min<size_t>((nkeys + 255) / 256, (size_t)c->sms * 8);
+        size_t items = (size_t)R * J; // items of the current pass
         uint32_t m = maxc;
         for (int pass = 0; m > 0; ++pass) {
+            // piece length for this pass: long pieces when segments are long
+            const size_t avg = items / std::max<size_t>(1, std::min<size_t>(nkeys, items));
+            const uint32_t Cp = (avg >= 2 * (size_t)kPieceLong && m > (uint32_t)kPieceLong) ? kPieceLong : kPiece;
             uint32_t *np = npb[pass & 1], *ps = psb[pass & 1];
-            dev::k_npieces<<<g1, 256, 0, st>>>(cur_len, nkeys, kPiece, np);
+            dev::k_npieces<<<g1, 256, 0, st>>>(cur_len, nkeys, Cp, np);
             check_launch(*c);
             CK(cub::DeviceScan::ExclusiveSum(cubtmp, tmp_bytes, np, ps, (int)nkeys, st));
             uint32_t tail[2];
@@ -507,22 +513,46 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
             CK(cudaStreamSynchronize(st));
             const size_t P = (size_t)tail[0] + tail[1];
             dev::Piece *pieces = bget<dev::Piece>(B.pieces, P);
-            dev::k_emit_pieces<<<g1, 256, 0, st>>>(cur_start, cur_len, ps, nkeys, kPiece, pieces);
+            dev::k_emit_pieces<<<g1, 256, 0, st>>>(cur_start, cur_len, ps, nkeys, Cp, pieces);
             check_launch(*c);
+            // order pieces by length, longest first (warp-uniform trip counts)
+            uint32_t *plen = bget<uint32_t>(B.plen, 2 * P), *pidx = bget<uint32_t>(B.pord, 2 * P);
+            {
+                const int gp = (int)std::min<size_t>((P + 255) / 256, (size_t)c->sms * 8);
+                dev::k_piece_keys<<<gp, 256, 0, st>>>(pieces, P, plen, pidx);
+                check_launch(*c);
+                size_t sort_bytes = 0;
+                CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, plen, plen + P, pidx, pidx + P,
+                                                             (int)P, 0, 8, st));
+                cubtmp = grow(B.cub, std::max({tmp_bytes, tmp2, sort_bytes}) + 256);
+                CK(cub::DeviceRadixSort::SortPairsDescending(cubtmp, sort_bytes, plen, plen + P, pidx, pidx + P,
+                                                             (int)P, 0, 8, st));
+            }
+            const uint32_t *order = pidx + P;
             uint32_t *dst = bget<uint32_t>(B.part[pass & 1], P * 2 * S4);
-            auto k = dev::k_seg_prod<S4, C::TH, kPiece>;
             constexpr int NI = dev::kBlock / C::TH;
-            const int grid = occupancy_grid(*c, k, 2 * P, NI);
-            ProfScope prof_(*c, 0);
-            k<<<grid, dev::kBlock, 0, st>>>(arg(c->mod_n2), pieces, P, pass == 0 ? sorted : nullptr, src, dst);
+            if (Cp == (uint32_t)kPieceLong) {
+                auto k = dev::k_seg_prod<S4, C::TH, kPieceLong>;
+                const int grid = occupancy_grid(*c, k, 2 * P, NI);
+                ProfScope prof_(*c, 0);
+                k<<<grid, dev::kBlock, 0, st>>>(arg(c->mod_n2), pieces, order, P, pass == 0 ? sorted : nullptr, src,
+                                                dst);
+            } else {
+                auto k = dev::k_seg_prod<S4, C::TH, kPiece>;
+                const int grid = occupancy_grid(*c, k, 2 * P, NI);
+                ProfScope prof_(*c, 0);
+                k<<<grid, dev::kBlock, 0, st>>>(arg(c->mod_n2), pieces, order, P, pass == 0 ? sorted : nullptr, src,
+                                                dst);
+            }
             check_launch(*c);
             final_idx = ps;
             final_part = dst;
             cur_start = ps;
             cur_len = np;
             src = dst;
-            if (m <= (uint32_t)kPiece) break;
-            m = (m + kPiece - 1) / kPiece;
+            items = P;
+            if (m <= Cp) break;
+            m = (m + Cp - 1) / Cp;
         }
         auto kf = dev::k_hist_finalize<S4, C::TH>;
         constexpr int NI = dev::kBlock / C::TH;

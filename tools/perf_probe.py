@@ -82,10 +82,16 @@ def main():
     nslots = N * J * K * 2
     outh = torch.zeros((nslots, cw), dtype=torch.int32, device=dev)
     del gh
+    ops.accumulate(h, bins, J, offs, N, rows, R, K, outh)  # warm-up (allocations)
     torch.cuda.synchronize()
+    ctx.profile(True)
     t0 = time.perf_counter()
     adds = ops.accumulate(h, bins, J, offs, N, rows, R, K, outh)
     dt = time.perf_counter() - t0
+    nk, kms = ctx.kernel_time(0)
+    ctx.profile(False)
+    print(f"  seg_prod launches={nk} kernel_ms={kms:.1f} ({adds*(2*128*128+128)/(kms/1e3)/peak*100:.1f}% of peak "
+          f"inside the kernel)", flush=True)
     prods = adds * (2 * 128 * 128 + 128)
     print(f"histogram R={R} J={J} N={N}: {dt*1e3:.1f} ms  adds={adds}  {adds/dt:.3e} adds/s  "
           f"{prods/dt:.3e} products/s ({prods/dt/peak*100:.1f}% of peak)", flush=True)
