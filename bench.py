@@ -468,7 +468,11 @@ def run_ours(a):
         "gpu_launches": int(launches),
         "roofline": {
             "bound": "imad", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tproducts/s",
-            "frac": achieved / peak if peak else None, "traffic": None,
+            "frac": achieved / peak if peak else None,
+            # dram__bytes_read.sum + dram__bytes_write.sum of one K2 launch from the round's
+            # ncu --set full capture (profiles/r01_summary.md): a depth-0 pass-1 launch at
+            # 200k rows gathering 2.8M ciphertexts (1.43 GB algorithmic) read 2.07 GB + wrote 0.05 GB
+            "traffic": 2.12e9, "traffic_algorithmic": 1.43e9,
             "kernel": "k_seg_prod (K2 segmented Montgomery product mod n^2)",
             "work": f"{PRODUCTS_PER_ADD} 32x32->64 products per reference ciphertext addition",
             "kernel_launches": k2_launches, "kernel_ms": k2_ms, "kernel_share_of_step": k2_ms / ms,
