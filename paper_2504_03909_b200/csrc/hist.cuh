@@ -132,17 +132,29 @@ __global__ void k_emit_pieces(const uint32_t *seg_start, const uint32_t *seg_len
 // Pieces are visited in `order` (sorted by length, longest first) so that the
 // instances of a warp run pieces of (nearly) equal length; partial j is
 // written at the piece's own index, keeping each key's partials contiguous.
+// Work distribution: each warp claims its next NIW = 32/TPI jobs from a
+// global counter (warp-uniform trip counts; no block-level rounds, so the
+// tail is at most one piece).
 template <int S, int TPI, int C>
 __global__ void __launch_bounds__(kBlock) k_seg_prod(ModArg M, const Piece *pieces, const uint32_t *order,
                                                      size_t n_pieces, const uint32_t *sorted,
-                                                     const uint32_t *src, uint32_t *dst) {
-    constexpr int L = S / TPI, NI = kBlock / TPI;
+                                                     const uint32_t *src, uint32_t *dst,
+                                                     unsigned long long *next_job) {
+    constexpr int L = S / TPI, NI = kBlock / TPI, NIW = 32 / TPI;
     __shared__ uint2 sB[S / 2 * NI];
     const Stage st = make_stage<TPI>(sB);
     const ModRef mr = M.ref();
     uint32_t N[L];
     load_const<S, TPI>(N, mr, kMod);
-    SFXB_UNIFORM_LOOP(job, active, 2 * n_pieces) {
+    const size_t total = 2 * n_pieces;
+    for (;;) {
+        unsigned long long base = 0;
+        if ((threadIdx.x & 31) == 0) base = atomicAdd(next_job, (unsigned long long)NIW);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= total) break;
+        const size_t mine = base + (threadIdx.x & 31) / TPI;
+        const bool active = mine < total;
+        const size_t job = active ? mine : total - 1;
         const uint32_t pidx = order[job >> 1];
         const Piece pc = pieces[pidx];
         const uint32_t g = (uint32_t)(job & 1);

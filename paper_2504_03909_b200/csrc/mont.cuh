@@ -143,16 +143,24 @@ __device__ __forceinline__ uint32_t inst_ballot(bool pred) {
 // ---------------------------------------------------------------- shared-memory operand b
 //
 // Operand b of an instance lives in shared memory as S/2 limb pairs, pair i
-// of instance k at sB[i * NI + k] (uint2), NI = instances per block; the
-// TPI lanes of an instance read the same pair (broadcast) and the instances
-// of a warp read consecutive 8-byte words (conflict-free LDS.64).
+// of instance k at sB[i·NI + (k ^ (i/(L/2) mod NI))] (uint2), NI = instances
+// per block (a power of two).  The TPI lanes of an instance read the same pair
+// (broadcast) and the instances of a warp read distinct 8-byte words
+// (conflict-free LDS.64); the XOR swizzle by the owning lane t = i/(L/2)
+// spreads the writes of the TPI lanes of one instance over distinct banks.
+
+template <int L, int NI>
+__device__ __forceinline__ int b_slot(int pair, int inst) {
+    return pair * NI + (inst ^ ((pair / (L / 2)) & (NI - 1)));
+}
 
 template <int S, int TPI>
 __device__ __forceinline__ void store_b(uint2 *sB, int NI, int inst, const uint32_t (&v)[S / TPI]) {
-    constexpr int L = S / TPI;
+    constexpr int L = S / TPI, NIc = 128 / TPI;
     const int t = inst_lane<TPI>();
 #pragma unroll
-    for (int j = 0; j < L / 2; ++j) sB[(t * (L / 2) + j) * NI + inst] = make_uint2(v[2 * j], v[2 * j + 1]);
+    for (int j = 0; j < L / 2; ++j) sB[b_slot<L, NIc>(t * (L / 2) + j, inst)] = make_uint2(v[2 * j], v[2 * j + 1]);
+    (void)NI;
 }
 
 // ---------------------------------------------------------------- CIOS core
@@ -283,9 +291,10 @@ __device__ __forceinline__ void mont_mul(uint32_t (&r)[S / TPI], const uint32_t 
     uint32_t X[L], Y[L], Z = 0;
 #pragma unroll
     for (int k = 0; k < L; ++k) X[k] = Y[k] = 0;
+    constexpr int NIc = 128 / TPI;
 #pragma unroll U
     for (int i = 0; i < S / 2; ++i) {
-        const uint2 b = sB[i * NI + inst];
+        const uint2 b = sB[b_slot<L, NIc>(i, inst)];
         cios_step<L, TPI>(X, Y, Z, A, N, b.x, np, false);
         cios_step<L, TPI>(Y, X, Z, A, N, b.y, np, false);
     }

@@ -419,7 +419,7 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
     cudaStream_t st = c->stream;
     uint32_t *count = bget<uint32_t>(B.count, nkeys), *ones = bget<uint32_t>(B.ones, 2 * nkeys);
     uint32_t *cursor = bget<uint32_t>(B.cursor, nkeys), *seg_start = bget<uint32_t>(B.seg_start, nkeys);
-    uint32_t *misc = bget<uint32_t>(B.misc, 16);
+    uint32_t *misc = bget<uint32_t>(B.misc, 16); // [0] status, [4] max count, [8..9] adds, [12..13] job counter
     CK(cudaMemsetAsync(count, 0, nkeys * 4, st));
     CK(cudaMemsetAsync(ones, 0, 2 * nkeys * 4, st));
     CK(cudaMemsetAsync(cursor, 0, nkeys * 4, st));
@@ -531,18 +531,20 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
             const uint32_t *order = pidx + P;
             uint32_t *dst = bget<uint32_t>(B.part[pass & 1], P * 2 * S4);
             constexpr int NI = dev::kBlock / C::TH;
+            unsigned long long *next_job = reinterpret_cast<unsigned long long *>(misc + 12);
+            CK(cudaMemsetAsync(next_job, 0, 8, st));
             if (Cp == (uint32_t)kPieceLong) {
                 auto k = dev::k_seg_prod<S4, C::TH, kPieceLong>;
                 const int grid = occupancy_grid(*c, k, 2 * P, NI);
                 ProfScope prof_(*c, 0);
                 k<<<grid, dev::kBlock, 0, st>>>(arg(c->mod_n2), pieces, order, P, pass == 0 ? sorted : nullptr, src,
-                                                dst);
+                                                dst, next_job);
             } else {
                 auto k = dev::k_seg_prod<S4, C::TH, kPiece>;
                 const int grid = occupancy_grid(*c, k, 2 * P, NI);
                 ProfScope prof_(*c, 0);
                 k<<<grid, dev::kBlock, 0, st>>>(arg(c->mod_n2), pieces, order, P, pass == 0 ? sorted : nullptr, src,
-                                                dst);
+                                                dst, next_job);
             }
             check_launch(*c);
             final_idx = ps;
