@@ -476,7 +476,8 @@ def run_ours(a):
             "kernel": "k_seg_prod (K2 segmented Montgomery product mod n^2)",
             "work": f"{PRODUCTS_PER_ADD} 32x32->64 products per reference ciphertext addition",
             "kernel_launches": k2_launches, "kernel_ms": k2_ms, "kernel_share_of_step": k2_ms / ms,
-            "peak_source": f"sfxb_imad_peak (IMAD.WIDE.U32.X chains, all SMs) at {peak_clk:.0f} MHz",
+            "peak_source": "sfxb_imad_peak: IMAD.WIDE.U32(.X) carry chains on all SMs, measured in this process "
+                           "before the timed region (SM clock: see clocks)",
         },
         "roofline_encrypt": {"achieved": enc_products * E / (k1[1] / 1e3) / 1e12 if k1[1] else None,
                              "peak": peak / 1e12, "unit": "Tproducts/s",

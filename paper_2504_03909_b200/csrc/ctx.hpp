@@ -69,7 +69,7 @@ struct CtxState {
     } prof[4];
 
     // scratch (grown on demand, freed with the context)
-    Buf scratch_table, tmp[4], host_pinned[2];
+    Buf scratch_table, tmp[4], host_pinned[2], io[6]; // io: host-API staging (grow-only)
     std::vector<void *> owned; // device allocations of constants
 };
 

@@ -57,7 +57,13 @@ extern "C" int sfxb_imad_peak(int device, double *products_per_s, double *sm_clo
     if (cudaSetDevice(device) != cudaSuccess) return SFXB_ERR_CUDA;
     cudaDeviceProp p;
     if (cudaGetDeviceProperties(&p, device) != cudaSuccess) return SFXB_ERR_CUDA;
-    const int blocks = p.multiProcessorCount * 8, tpb = 256, iters = 4000;
+    // exactly one wave, so block 0 spans the whole kernel and clock64 / elapsed
+    // is the SM clock under this load
+    const int tpb = 256, iters = 4000;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_imad_peak, tpb, 0) != cudaSuccess || per_sm < 1)
+        return SFXB_ERR_CUDA;
+    const int blocks = p.multiProcessorCount * per_sm;
     uint32_t *seed = nullptr, *out = nullptr;
     long long *cyc = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;

@@ -199,33 +199,63 @@ __device__ __forceinline__ void from_mont(uint32_t (&r)[S / TPI], const uint32_t
 // Fixed-window exponentiation in the Montgomery domain:
 //   x <- x^e, e given as `nd` window digits of `w` bits, most significant first.
 // `table` = this instance's 2^w·S-word scratch in global memory (L2-resident).
+// The table build and the main loop share ONE Montgomery multiply call site
+// (the operand is either acc itself — a squaring — or a table entry / x), so
+// the hot loop is a single inlined copy of the unrolled CIOS body.
 template <int S, int TPI>
 __device__ __forceinline__ void mont_pow(uint32_t (&x)[S / TPI], const uint8_t *digits, int nd, int w,
                                          uint32_t *table, const ModRef &M, const Stage &st,
                                          const uint32_t (&N)[S / TPI]) {
     constexpr int L = S / TPI;
     const int T = 1 << w;
-    uint32_t cur[L], one[L];
+    uint32_t one[L];
     load_const<S, TPI>(one, M, kOne);
     store_lane<S, TPI>(table, one);
     store_lane<S, TPI>(table + S, x);
-#pragma unroll
-    for (int k = 0; k < L; ++k) cur[k] = x[k];
-    stage_b<S, TPI>(st, x); // b = x for the whole table build
-    for (int j = 2; j < T; ++j) {
-        mont_mul<S, TPI>(cur, cur, st.sB, st.NI, st.inst, N, M.np);
-        store_lane<S, TPI>(table + j * S, cur);
-    }
-    __syncwarp();
+    // op sequence: table build (T−2 multiplies by x), then for each digit
+    // after the first: w squarings and one multiply by table[d] (skipped for d == 0)
     uint32_t acc[L];
-    load_lane<S, TPI>(acc, table + (int)digits[0] * S);
-    for (int i = 1; i < nd; ++i) {
-        for (int k = 0; k < w; ++k) mmul<S, TPI>(acc, acc, acc, st, N, M.np);
-        const int d = digits[i];
-        if (d != 0) {
-            uint32_t tv[L];
-            load_lane<S, TPI>(tv, table + d * S);
-            mmul<S, TPI>(acc, acc, tv, st, N, M.np);
+#pragma unroll
+    for (int k = 0; k < L; ++k) acc[k] = x[k];
+    int j = 2;          // next table entry to build (build phase while j < T)
+    int i = 1, sq = 0;  // digit index and squarings done for it (main phase)
+    bool started = false;
+    for (;;) {
+        bool square;
+        const uint32_t *bsrc = nullptr;
+        if (j < T) {
+            square = false;
+            bsrc = table + S; // x
+        } else {
+            if (!started) {
+                load_lane<S, TPI>(acc, table + (int)digits[0] * S);
+                started = true;
+            }
+            if (i >= nd) break;
+            if (sq < w) {
+                square = true;
+            } else {
+                const int d = digits[i];
+                ++i;
+                sq = 0;
+                if (d == 0) continue;
+                square = false;
+                bsrc = table + d * S;
+            }
+        }
+        uint32_t b[L];
+        if (square) {
+#pragma unroll
+            for (int k = 0; k < L; ++k) b[k] = acc[k];
+        } else {
+            load_lane<S, TPI>(b, bsrc);
+        }
+        mmul<S, TPI>(acc, acc, b, st, N, M.np);
+        if (j < T) {
+            store_lane<S, TPI>(table + j * S, acc);
+            ++j;
+        } else if (square) {
+            ++sq;
         }
     }
 #pragma unroll

@@ -603,6 +603,13 @@ void d2h_padded(sfxb_ctx *c, uint32_t *h, const uint32_t *d, size_t count, size_
     for (size_t i = 0; i < count; ++i) std::memcpy(h + i * words, &tmp[i * stride], words * 4);
 }
 
+// view of a grow-only per-context staging buffer
+template <typename T>
+struct IoBuf {
+    T *p;
+    IoBuf(Buf &b, size_t n) : p((T *)grow(b, n * sizeof(T) + 64)) {}
+};
+
 template <typename T>
 struct DevBuf {
     T *p = nullptr;
@@ -822,9 +829,9 @@ int sfxb_encrypt(sfxb_ctx *c, const int64_t *q_fixed, const uint32_t *r, size_t 
             if (host::cmp(host::from_words(ri, c->nw), c->n) >= 0)
                 throw ApiError(SFXB_ERR_RANGE, "encrypt: blinding factor out of range");
         }
-        DevBuf<int64_t> dq(count);
-        DevBuf<uint32_t> dr(count * Sn), dout(count * S4);
-        DevBuf<uint8_t> dflags(count);
+        IoBuf<int64_t> dq(c->io[0], count);
+        IoBuf<uint32_t> dr(c->io[1], count * Sn), dout(c->io[2], count * S4);
+        IoBuf<uint8_t> dflags(c->io[3], count);
         CK(cudaMemsetAsync(dflags.p, 0, count, c->stream));
         CK(cudaMemcpyAsync(dq.p, q_fixed, count * 8, cudaMemcpyHostToDevice, c->stream));
         h2d_padded(c, dr.p, r, count, c->nw, Sn);
@@ -854,7 +861,7 @@ int sfxb_add(sfxb_ctx *c, const uint32_t *a, const uint32_t *b, size_t count, ui
             if (host::cmp(host::from_words(a + i * cw, cw), c->n2) >= 0 ||
                 host::cmp(host::from_words(b + i * cw, cw), c->n2) >= 0)
                 throw ApiError(SFXB_ERR_RANGE, "add_ciphertexts: ciphertext out of range");
-        DevBuf<uint32_t> da(count * S4), db(count * S4), dout(count * S4);
+        IoBuf<uint32_t> da(c->io[0], count * S4), db(c->io[1], count * S4), dout(c->io[2], count * S4);
         h2d_padded(c, da.p, a, count, cw, S4);
         h2d_padded(c, db.p, b, count, cw, S4);
         add_dev(c, da.p, db.p, count, dout.p);
@@ -877,8 +884,8 @@ int sfxb_decrypt(sfxb_ctx *c, const uint32_t *cts, size_t count, uint32_t scale,
         if (!c->has_priv) throw ApiError(SFXB_ERR_AUTH, "decrypt requested without private key material");
         if (count == 0) return;
         const size_t Sn = 2 * (size_t)c->s, S4 = 4 * (size_t)c->s;
-        DevBuf<uint32_t> dc(count * S4), dplain(out_plain ? count * Sn : 1);
-        DevBuf<double> dv(count);
+        IoBuf<uint32_t> dc(c->io[0], count * S4), dplain(c->io[1], out_plain ? count * Sn : 1);
+        IoBuf<double> dv(c->io[2], count);
         h2d_padded(c, dc.p, cts, count, 2 * c->nw, S4);
         decrypt_dev(c, dc.p, count, scale, dv.p, out_plain ? dplain.p : nullptr, decryptions);
         CK(cudaMemcpyAsync(out_values, dv.p, count * 8, cudaMemcpyDeviceToHost, c->stream));
@@ -948,8 +955,8 @@ int sfxb_accumulate(sfxb_ctx *c, const uint32_t *gh_cts, uint32_t n_samples, con
             g.reset(gp);
         }
         const size_t S4 = 4 * (size_t)c->s, nslots = 2ull * N * J * K;
-        DevBuf<uint16_t> db((size_t)J * n_samples);
-        DevBuf<uint32_t> doff((size_t)N + 1), drows(R ? R : 1), dout(nslots * S4);
+        IoBuf<uint16_t> db(c->io[0], (size_t)J * n_samples);
+        IoBuf<uint32_t> doff(c->io[1], (size_t)N + 1), drows(c->io[2], R ? R : 1), dout(c->io[3], nslots * S4);
         if ((size_t)J * n_samples)
             CK(cudaMemcpyAsync(db.p, bins, (size_t)J * n_samples * 2, cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemcpyAsync(doff.p, node_offsets, ((size_t)N + 1) * 4, cudaMemcpyHostToDevice, c->stream));
@@ -969,8 +976,8 @@ int sfxb_accumulate_gh(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *bins, uint
         if (N && node_offsets[0] != 0) throw ApiError(SFXB_ERR_ARG, "accumulate: node offsets must start at 0");
         const uint32_t R = N ? node_offsets[N] : 0;
         const size_t S4 = 4 * (size_t)c->s, nslots = 2ull * N * J * K, n_samples = g->n_samples;
-        DevBuf<uint16_t> db((size_t)J * n_samples);
-        DevBuf<uint32_t> doff((size_t)N + 1), drows(R ? R : 1), dout(nslots * S4);
+        IoBuf<uint16_t> db(c->io[0], (size_t)J * n_samples);
+        IoBuf<uint32_t> doff(c->io[1], (size_t)N + 1), drows(c->io[2], R ? R : 1), dout(c->io[3], nslots * S4);
         if ((size_t)J * n_samples)
             CK(cudaMemcpyAsync(db.p, bins, (size_t)J * n_samples * 2, cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemcpyAsync(doff.p, node_offsets, ((size_t)N + 1) * 4, cudaMemcpyHostToDevice, c->stream));
