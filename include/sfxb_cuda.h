@@ -131,6 +131,27 @@ int sfxb_accumulate_dev(sfxb_ctx *ctx, const sfxb_gh *gh, const uint16_t *d_bins
                         const uint32_t *d_rows, uint32_t n_rows, uint32_t n_bins,
                         uint32_t *d_out_slots, int mont_out, uint64_t *additions);
 
+/* Tree mode — sibling subtraction: parent[i] is the index of
+ * frontier node i's parent in the previous tree-mode call on this context
+ * (−1: none; the caller guarantees rows(parent) = rows(child a) ∪ rows(child b)
+ * for parents with exactly two children listed).  For such siblings only the
+ * child with fewer rows is multiplied out; the other is derived as
+ * hist(parent)·hist(small)⁻¹ mod n² (one batch inversion per call).  Results,
+ * `additions` and the output layout are identical to sfxb_accumulate — the
+ * residues are unique.  The context caches the last tree-mode call's
+ * histograms; sfxb_tree_reset, freeing the gh handle or a call with another
+ * gh / feature count / bin count forgets them. */
+int sfxb_accumulate_tree_dev(sfxb_ctx *ctx, const sfxb_gh *gh, const uint16_t *d_bins,
+                             uint32_t n_features, const uint32_t *d_node_offsets,
+                             const uint32_t *h_node_offsets, uint32_t n_nodes, const uint32_t *d_rows,
+                             uint32_t n_rows, uint32_t n_bins, const int32_t *h_parent,
+                             uint32_t *d_out_slots, int mont_out, uint64_t *additions);
+int sfxb_accumulate_tree_gh(sfxb_ctx *ctx, const sfxb_gh *gh, const uint16_t *bins, uint32_t n_features,
+                            const uint32_t *node_offsets, uint32_t n_nodes, const uint32_t *rows,
+                            uint32_t n_bins, const int32_t *parent, uint32_t *out_slots,
+                            uint64_t *additions);
+int sfxb_tree_reset(sfxb_ctx *ctx);
+
 /* K4: element-wise product of `parts` partial histograms (Montgomery form,
  * each n_slots ciphertexts, contiguous) into d_out (plain form, n_slots).
  * Used after the all-gather of per-GPU row-shard partials (homomorphic
@@ -160,6 +181,9 @@ int sfxb_ctx_sync(sfxb_ctx *ctx);
  * exponentiation).  Enabling resets the accumulators. */
 int sfxb_ctx_profile(sfxb_ctx *ctx, int enable);
 int sfxb_ctx_kernel_time(sfxb_ctx *ctx, int family, uint64_t *launches, double *ms);
+/* as above plus the Montgomery multiplications those launches executed
+ * (family 3: the sibling-subtraction batch inversion / derivation kernels) */
+int sfxb_ctx_kernel_stats(sfxb_ctx *ctx, int family, uint64_t *launches, double *ms, uint64_t *modmuls);
 /* integer-multiply peak microbenchmark: IMAD.WIDE.U32(.X) 32×32→64 products/s */
 int sfxb_imad_peak(int device, double *products_per_s, double *sm_clock_mhz);
 

@@ -40,6 +40,7 @@ _u16p = np.ctypeslib.ndpointer(dtype=np.uint16, flags="C_CONTIGUOUS")
 _i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
 _f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
 _u8p = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
+_i32p = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
 
 _lib = None
 
@@ -77,12 +78,19 @@ def load() -> C.CDLL:
                                           vp, C.c_int, C.POINTER(C.c_uint64)]),
         "sfxb_accumulate_gh": (C.c_int, [vp, vp, _u16p, C.c_uint32, _u32p, C.c_uint32, _u32p, C.c_uint32,
                                          _u32p, C.POINTER(C.c_uint64)]),
+        "sfxb_accumulate_tree_dev": (C.c_int, [vp, vp, vp, C.c_uint32, vp, _u32p, C.c_uint32, vp, C.c_uint32,
+                                               C.c_uint32, _i32p, vp, C.c_int, C.POINTER(C.c_uint64)]),
+        "sfxb_accumulate_tree_gh": (C.c_int, [vp, vp, _u16p, C.c_uint32, _u32p, C.c_uint32, _u32p, C.c_uint32,
+                                              _i32p, _u32p, C.POINTER(C.c_uint64)]),
+        "sfxb_tree_reset": (C.c_int, [vp]),
         "sfxb_reduce_partials_dev": (C.c_int, [vp, vp, C.c_uint32, sz, vp]),
         "sfxb_decrypt": (C.c_int, [vp, _u32p, sz, C.c_uint32, _f64p, vp, C.POINTER(C.c_uint64)]),
         "sfxb_decrypt_dev": (C.c_int, [vp, vp, sz, C.c_uint32, vp, vp, C.POINTER(C.c_uint64)]),
         "sfxb_imad_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "sfxb_ctx_profile": (C.c_int, [vp, C.c_int]),
         "sfxb_ctx_kernel_time": (C.c_int, [vp, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]),
+        "sfxb_ctx_kernel_stats": (C.c_int, [vp, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_double),
+                                            C.POINTER(C.c_uint64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name, None)
@@ -160,6 +168,12 @@ class Context:
         n, ms = C.c_uint64(), C.c_double()
         self._check(self.lib.sfxb_ctx_kernel_time(self.h, family, C.byref(n), C.byref(ms)))
         return n.value, ms.value
+
+    def kernel_stats(self, family: int):
+        """(launches, total ms, Montgomery multiplications) of a kernel family since profile(True)."""
+        n, ms, mm = C.c_uint64(), C.c_double(), C.c_uint64()
+        self._check(self.lib.sfxb_ctx_kernel_stats(self.h, family, C.byref(n), C.byref(ms), C.byref(mm)))
+        return n.value, ms.value, mm.value
 
     @property
     def launches(self) -> int:
@@ -289,6 +303,36 @@ class DeviceOps:
         if sync:
             self._post()
         return adds.value
+
+    def accumulate_tree(self, gh: GhHandle, d_bins, n_features: int, d_offsets, h_offsets, n_nodes: int, d_rows,
+                        n_rows: int, n_bins: int, parent, d_out, mont_out: bool = False, sync: bool = True) -> int:
+        """Tree-mode accumulate (sibling subtraction), device buffers + host metadata."""
+        if sync:
+            self._pre()
+        adds = C.c_uint64(0)
+        self.ctx._check(self.ctx.lib.sfxb_accumulate_tree_dev(
+            self.ctx.h, gh.h, _ptr(d_bins), n_features, _ptr(d_offsets),
+            np.ascontiguousarray(h_offsets, dtype=np.uint32), n_nodes, _ptr(d_rows), n_rows, n_bins,
+            np.ascontiguousarray(parent, dtype=np.int32), _ptr(d_out), 1 if mont_out else 0, C.byref(adds)))
+        if sync:
+            self._post()
+        return adds.value
+
+    def accumulate_tree_host(self, gh: GhHandle, bins, node_offsets, rows, n_bins: int, parent, out=None):
+        bins = np.ascontiguousarray(bins, dtype=np.uint16)
+        J = bins.shape[0]
+        n_nodes = len(node_offsets) - 1
+        if out is None:
+            out = np.zeros((n_nodes * J * n_bins * 2, self.ctx.ct_words), np.uint32)
+        adds = C.c_uint64(0)
+        self.ctx._check(self.ctx.lib.sfxb_accumulate_tree_gh(
+            self.ctx.h, gh.h, bins.reshape(-1), J, np.ascontiguousarray(node_offsets, dtype=np.uint32), n_nodes,
+            np.ascontiguousarray(rows, dtype=np.uint32), n_bins, np.ascontiguousarray(parent, dtype=np.int32),
+            out.reshape(-1), C.byref(adds)))
+        return out, adds.value
+
+    def tree_reset(self):
+        self.ctx._check(self.ctx.lib.sfxb_tree_reset(self.ctx.h))
 
     def reduce_partials(self, d_parts, parts: int, n_slots: int, d_out, sync: bool = True):
         if sync:

@@ -200,6 +200,81 @@ inline Big inv_mod_prime(const Big &x, const Big &p, size_t S) {
     return mh.pow(mod(x, p), sub(p, from_u64(2)));
 }
 
+// x^-1 mod M for odd M and gcd(x, M) = 1 (binary extended Euclid, fixed-size
+// in-place limb arithmetic).  Returns false when x is not invertible.
+inline bool inv_mod_odd(const Big &x_, const Big &M_, Big &out) {
+    const size_t W = M_.size() + 1;
+    Big M = low(M_, W), u = low(mod(x_, M_), W), v = M, x1(W, 0), x2(W, 0);
+    x1[0] = 1;
+    auto is_one = [&](const Big &a) {
+        if (a[0] != 1) return false;
+        for (size_t i = 1; i < W; ++i)
+            if (a[i]) return false;
+        return true;
+    };
+    auto is_zero_w = [&](const Big &a) {
+        for (size_t i = 0; i < W; ++i)
+            if (a[i]) return false;
+        return true;
+    };
+    auto shr1 = [&](Big &a) {
+        for (size_t i = 0; i + 1 < W; ++i) a[i] = (a[i] >> 1) | (a[i + 1] << 31);
+        a[W - 1] >>= 1;
+    };
+    auto add_in = [&](Big &a, const Big &b) { // a += b (no overflow: values < 2M < 2^(32W))
+        uint64_t c = 0;
+        for (size_t i = 0; i < W; ++i) {
+            c += (uint64_t)a[i] + b[i];
+            a[i] = (uint32_t)c;
+            c >>= 32;
+        }
+    };
+    auto sub_in = [&](Big &a, const Big &b) { // a -= b, requires a >= b
+        int64_t br = 0;
+        for (size_t i = 0; i < W; ++i) {
+            int64_t d = (int64_t)a[i] - b[i] - br;
+            br = d < 0;
+            a[i] = (uint32_t)(d + (br ? (int64_t(1) << 32) : 0));
+        }
+    };
+    auto geq = [&](const Big &a, const Big &b) {
+        for (size_t i = W; i-- > 0;)
+            if (a[i] != b[i]) return a[i] > b[i];
+        return true;
+    };
+    auto half_mod = [&](Big &a) { // a/2 mod M
+        if (a[0] & 1) add_in(a, M);
+        shr1(a);
+    };
+    auto sub_mod = [&](Big &a, const Big &b) { // a = a − b mod M (a, b < M)
+        if (!geq(a, b)) add_in(a, M);
+        sub_in(a, b);
+    };
+    if (is_zero_w(u)) return false;
+    while (!is_one(u) && !is_one(v)) {
+        if (is_zero_w(u) || is_zero_w(v)) return false;
+        while ((u[0] & 1) == 0) {
+            shr1(u);
+            half_mod(x1);
+        }
+        while ((v[0] & 1) == 0) {
+            shr1(v);
+            half_mod(x2);
+        }
+        if (geq(u, v)) {
+            sub_in(u, v);
+            sub_mod(x1, x2);
+        } else {
+            sub_in(v, u);
+            sub_mod(x2, x1);
+        }
+    }
+    out = is_one(u) ? x1 : x2;
+    trim(out);
+    out = mod(out, M_);
+    return true;
+}
+
 // Fixed-window digits of e (most significant first), window w bits.
 inline std::vector<uint8_t> window_digits(const Big &e, int w) {
     size_t nb = std::max<size_t>(bit_length(e), 1);

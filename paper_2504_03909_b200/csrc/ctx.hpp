@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -65,8 +66,18 @@ struct CtxState {
     struct Prof {
         std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
         uint64_t launches = 0;
+        uint64_t modmuls = 0; // Montgomery multiplications the launches executed
         double ms_done = 0;
     } prof[4];
+
+    // sibling-subtraction parent cache: the last tree-mode call's histograms
+    // (Montgomery form, node-major), double-buffered
+    Buf tree_buf[2];
+    int tree_cur = 0;
+    bool tree_valid = false;
+    const void *tree_gh = nullptr;
+    uint32_t tree_J = 0, tree_K = 0, tree_N = 0;
+    std::unique_ptr<host::MontHost> mh_n2;
 
     // scratch (grown on demand, freed with the context)
     Buf scratch_table, tmp[4], host_pinned[2], io[6]; // io: host-API staging (grow-only)

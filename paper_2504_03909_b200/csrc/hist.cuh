@@ -53,6 +53,7 @@ struct HistArgs {
     const uint32_t *seg_start;
     uint32_t *sorted;        // n_rows·J
     uint32_t *status;        // bit0 bin out of range, bit1 row out of range
+    const uint8_t *derived;  // per frontier node: 1 = derived by sibling subtraction (may be null)
 };
 
 __global__ void k_hist_count(HistArgs a) {
@@ -84,6 +85,7 @@ __global__ void k_hist_scatter(HistArgs a) {
     for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
         const uint32_t f = (uint32_t)(t / a.n_rows), i = (uint32_t)(t % a.n_rows);
         const uint32_t row = a.rows[i];
+        if (a.derived && a.derived[a.node_of[i]]) continue;
         const uint32_t b = a.bins[(size_t)f * a.n_samples + row];
         const size_t key = ((size_t)a.node_of[i] * a.J + f) * a.K + b;
         const uint32_t pos = a.seg_start[key] + atomicAdd(a.cursor + key, 1u);
@@ -209,6 +211,114 @@ __global__ void __launch_bounds__(kBlock) k_hist_finalize(ModArg M, const uint32
             for (int w = 0; w < L; ++w) v[w] = one_m[w];
         if (!mont_out) from_mont<S, TPI>(v, v, st, N, M.np); // Montgomery one -> 1
         if (active) store_lane<S, TPI>(out + slot * S, v);
+    }
+}
+
+// ---------------------------------------------------------------- sibling subtraction
+//
+// Level d ≥ 1 of a tree: for siblings (a, b) whose parent P was histogrammed
+// at level d−1, only the child with fewer rows is built directly and the other
+// is derived as hist(P)·hist(small)⁻¹ mod n² (residues are unique, so this is
+// bit-identical to the direct product).  The inverses of all small-child slots
+// come from one Montgomery batch inversion: a pairwise product tree (up),
+// one inversion of the root on the host, and the tree walked back down.
+
+// out[i] = in[2i]·in[2i+1] (Montgomery form), or in[2i] when 2i+1 == n_in
+template <int S, int TPI>
+__global__ void __launch_bounds__(kBlock) k_pair_up(ModArg M, const uint32_t *in, size_t n_in, uint32_t *out) {
+    constexpr int L = S / TPI, NI = kBlock / TPI;
+    __shared__ uint2 sB[S / 2 * NI];
+    const Stage st = make_stage<TPI>(sB);
+    const ModRef mr = M.ref();
+    uint32_t N[L], one_m[L];
+    load_const<S, TPI>(N, mr, kMod);
+    load_const<S, TPI>(one_m, mr, kOne);
+    const size_t n_out = (n_in + 1) / 2;
+    SFXB_UNIFORM_LOOP(i, active, n_out) {
+        uint32_t a[L], b[L];
+        load_lane<S, TPI>(a, in + 2 * i * S);
+        if (2 * i + 1 < n_in) load_lane<S, TPI>(b, in + (2 * i + 1) * S);
+        else
+#pragma unroll
+            for (int k = 0; k < L; ++k) b[k] = one_m[k];
+        mmul<S, TPI>(a, a, b, st, N, M.np);
+        if (active) store_lane<S, TPI>(out + i * S, a);
+    }
+}
+
+// inv_out[i] = inv_parent[i/2]·in[i^1] (or inv_parent[i/2] without a sibling)
+template <int S, int TPI>
+__global__ void __launch_bounds__(kBlock) k_pair_down(ModArg M, const uint32_t *inv_parent, const uint32_t *in,
+                                                      size_t n_in, uint32_t *inv_out) {
+    constexpr int L = S / TPI, NI = kBlock / TPI;
+    __shared__ uint2 sB[S / 2 * NI];
+    const Stage st = make_stage<TPI>(sB);
+    const ModRef mr = M.ref();
+    uint32_t N[L], one_m[L];
+    load_const<S, TPI>(N, mr, kMod);
+    load_const<S, TPI>(one_m, mr, kOne);
+    SFXB_UNIFORM_LOOP(i, active, n_in) {
+        uint32_t a[L], b[L];
+        load_lane<S, TPI>(a, inv_parent + (i / 2) * S);
+        if ((i ^ 1) < n_in) load_lane<S, TPI>(b, in + (i ^ 1) * S);
+        else
+#pragma unroll
+            for (int k = 0; k < L; ++k) b[k] = one_m[k];
+        mmul<S, TPI>(a, a, b, st, N, M.np);
+        if (active) store_lane<S, TPI>(inv_out + i * S, a);
+    }
+}
+
+struct Derived {
+    uint32_t derived, small, parent; // node indices: this level, this level, previous level
+};
+
+// gather the slots of the small siblings: v[d·spn + k] = hist[small_d·spn + k]
+__global__ void k_gather_small(const uint32_t *hist, const Derived *dv, size_t n_derived, size_t spn, int S,
+                               uint32_t *v) {
+    const size_t words = n_derived * spn * (size_t)S;
+    for (size_t w = (size_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (size_t)gridDim.x * blockDim.x) {
+        const size_t slot = w / S, k = w % S;
+        const size_t d = slot / spn, j = slot % spn;
+        v[w] = hist[((size_t)dv[d].small * spn + j) * S + k];
+    }
+}
+
+// hist[derived_d·spn + k] = parent_hist[parent_d·spn + k] · inv_small[d·spn + k]
+template <int S, int TPI>
+__global__ void __launch_bounds__(kBlock) k_derive(ModArg M, const uint32_t *parent_hist, const uint32_t *inv_small,
+                                                   const Derived *dv, size_t n_derived, size_t spn, uint32_t *hist) {
+    constexpr int L = S / TPI, NI = kBlock / TPI;
+    __shared__ uint2 sB[S / 2 * NI];
+    const Stage st = make_stage<TPI>(sB);
+    const ModRef mr = M.ref();
+    uint32_t N[L];
+    load_const<S, TPI>(N, mr, kMod);
+    SFXB_UNIFORM_LOOP(j, active, n_derived * spn) {
+        const Derived d = dv[j / spn];
+        const size_t k = j % spn;
+        uint32_t a[L], b[L];
+        load_lane<S, TPI>(a, parent_hist + ((size_t)d.parent * spn + k) * S);
+        load_lane<S, TPI>(b, inv_small + j * S);
+        mmul<S, TPI>(a, a, b, st, N, M.np);
+        if (active) store_lane<S, TPI>(hist + ((size_t)d.derived * spn + k) * S, a);
+    }
+}
+
+// out = from_mont(in) element-wise
+template <int S, int TPI>
+__global__ void __launch_bounds__(kBlock) k_from_mont_copy(ModArg M, const uint32_t *in, size_t count, uint32_t *out) {
+    constexpr int L = S / TPI, NI = kBlock / TPI;
+    __shared__ uint2 sB[S / 2 * NI];
+    const Stage st = make_stage<TPI>(sB);
+    const ModRef mr = M.ref();
+    uint32_t N[L];
+    load_const<S, TPI>(N, mr, kMod);
+    SFXB_UNIFORM_LOOP(e, active, count) {
+        uint32_t v[L];
+        load_lane<S, TPI>(v, in + e * S);
+        from_mont<S, TPI>(v, v, st, N, M.np);
+        if (active) store_lane<S, TPI>(out + e * S, v);
     }
 }
 

@@ -178,8 +178,9 @@ struct ProfScope {
     CtxState &c;
     int fam;
     cudaEvent_t a = nullptr, b = nullptr;
-    ProfScope(CtxState &c_, int fam_) : c(c_), fam(fam_) {
+    ProfScope(CtxState &c_, int fam_, uint64_t modmuls = 0) : c(c_), fam(fam_) {
         if (!c.profile) return;
+        c.prof[fam].modmuls += modmuls;
         CK(cudaEventCreate(&a));
         CK(cudaEventCreate(&b));
         CK(cudaEventRecord(a, c.stream));
@@ -366,7 +367,8 @@ void add_dev(sfxb_ctx *c, const uint32_t *d_a, const uint32_t *d_b, size_t count
 constexpr int kPiece = 16, kPieceLong = 64;
 
 struct HistBufs {
-    Buf node_of, count, ones, cursor, seg_start, sorted, np, piece_start, pieces, part[2], cub, misc, plen, pord;
+    Buf node_of, count, ones, cursor, seg_start, sorted, np, piece_start, pieces, part[2], cub, misc, plen, pord,
+        derived, pairs, tree_up, tree_dn;
 };
 HistBufs &hist_bufs(sfxb_ctx *c) {
     static thread_local std::map<sfxb_ctx *, HistBufs> m; // per context, per thread
@@ -406,13 +408,48 @@ T *bget(Buf &b, size_t n) {
     return (T *)grow(b, n * sizeof(T) + 64);
 }
 
+// Tree mode (h_parent != nullptr): h_parent[i] is the index of frontier node
+// i's parent in the PREVIOUS tree-mode call on this context (−1: none).  The
+// context keeps that call's histograms (Montgomery form) as parents; siblings
+// (exactly two children of one cached parent) are split into a directly built
+// small child and a derived large child.
 void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint32_t J, const uint32_t *d_offsets,
                     uint32_t N, const uint32_t *d_rows, uint32_t R, uint32_t K, uint32_t *d_out, int mont_out,
-                    uint64_t *additions) {
+                    uint64_t *additions, const int32_t *h_parent = nullptr, const uint32_t *h_offsets = nullptr) {
     if (!g || g->ctx != c) throw ApiError(SFXB_ERR_ARG, "accumulate: gradient handle belongs to another context");
     if (K == 0 || K > 65536) throw ApiError(SFXB_ERR_ARG, "accumulate: n_bins out of range");
     const size_t nkeys = (size_t)N * J * K;
-    if (nkeys == 0) return;
+    const bool tree = h_parent != nullptr;
+    if (nkeys == 0) {
+        if (tree) c->tree_valid = false;
+        return;
+    }
+    const size_t spn = (size_t)J * K * 2; // slots per node
+    // ---- sibling pairs whose parent histogram is cached
+    std::vector<dev::Derived> pairs;
+    std::vector<uint8_t> derived_flag;
+    size_t derived_rows = 0;
+    if (tree && c->tree_valid && c->tree_gh == g && c->tree_J == J && c->tree_K == K) {
+        std::vector<uint32_t> offs(N + 1);
+        if (h_offsets) std::copy(h_offsets, h_offsets + N + 1, offs.begin());
+        else {
+            CK(cudaMemcpyAsync(offs.data(), d_offsets, (N + 1) * 4, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+        }
+        std::vector<std::vector<uint32_t>> kids(c->tree_N);
+        for (uint32_t i = 0; i < N; ++i)
+            if (h_parent[i] >= 0 && (uint32_t)h_parent[i] < c->tree_N) kids[h_parent[i]].push_back(i);
+        derived_flag.assign(N, 0);
+        for (uint32_t pnode = 0; pnode < c->tree_N; ++pnode) {
+            if (kids[pnode].size() != 2) continue;
+            const uint32_t a = kids[pnode][0], b = kids[pnode][1];
+            const uint32_t na = offs[a + 1] - offs[a], nb = offs[b + 1] - offs[b];
+            const uint32_t small = na <= nb ? a : b, large = na <= nb ? b : a;
+            pairs.push_back(dev::Derived{large, small, pnode});
+            derived_flag[large] = 1;
+            derived_rows += std::max(na, nb);
+        }
+    }
     if (nkeys >= 0xffffffffull || (size_t)R * J >= 0xffffffffull)
         throw ApiError(SFXB_ERR_ARG, "accumulate: frontier too large for one call");
     HistBufs &B = hist_bufs(c);
@@ -437,6 +474,15 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
     a.cursor = cursor;
     a.seg_start = seg_start;
     a.status = misc;
+    uint8_t *d_derived = nullptr;
+    dev::Derived *d_pairs = nullptr;
+    if (!pairs.empty()) {
+        d_derived = bget<uint8_t>(B.derived, N);
+        d_pairs = bget<dev::Derived>(B.pairs, pairs.size());
+        CK(cudaMemcpyAsync(d_derived, derived_flag.data(), N, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d_pairs, pairs.data(), pairs.size() * sizeof(dev::Derived), cudaMemcpyHostToDevice, st));
+        a.derived = d_derived;
+    }
     if (R > 0) {
         uint32_t *node_of = bget<uint32_t>(B.node_of, R);
         a.node_of = node_of;
@@ -452,6 +498,16 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
         if (status & 2u) throw ApiError(SFXB_ERR_ARG, "row index out of range in accumulate");
         if (status & 1u) throw ApiError(SFXB_ERR_ARG, "bin index out of range in accumulate");
     }
+    // reference counter over ALL nodes (derived ones included)
+    unsigned long long *adds_d = reinterpret_cast<unsigned long long *>(misc + 8);
+    {
+        int grid = (int)std::min<size_t>((nkeys + 255) / 256, (size_t)c->sms * 8);
+        dev::k_hist_adds<<<grid, 256, 0, st>>>(count, ones, nkeys, adds_d);
+        check_launch(*c);
+    }
+    // derived nodes are not built directly
+    for (const dev::Derived &d : pairs)
+        CK(cudaMemsetAsync(count + (size_t)d.derived * J * K, 0, (size_t)J * K * 4, st));
     // scan counts -> segment starts; max count -> number of passes
     size_t tmp_bytes = 0, tmp2 = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, count, seg_start, (int)nkeys, st));
@@ -459,12 +515,6 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
     void *cubtmp = grow(B.cub, std::max(tmp_bytes, tmp2) + 256);
     CK(cub::DeviceScan::ExclusiveSum(cubtmp, tmp_bytes, count, seg_start, (int)nkeys, st));
     CK(cub::DeviceReduce::Max(cubtmp, tmp2, count, misc + 4, (int)nkeys, st));
-    unsigned long long *adds_d = reinterpret_cast<unsigned long long *>(misc + 8);
-    {
-        int grid = (int)std::min<size_t>((nkeys + 255) / 256, (size_t)c->sms * 8);
-        dev::k_hist_adds<<<grid, 256, 0, st>>>(count, ones, nkeys, adds_d);
-        check_launch(*c);
-    }
     if (R > 0) {
         const size_t items = (size_t)R * J;
         uint32_t *sorted = bget<uint32_t>(B.sorted, items);
@@ -497,7 +547,8 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
         using C = Cls<cs>;
         constexpr int S4 = 4 * cs;
         const int g1 = (int)std::min<size_t>((nkeys + 255) / 256, (size_t)c->sms * 8);
-        size_t items = (size_t)R * J; // items of the current pass
+        // items of the current pass (pass 1: frontier rows of directly built nodes)
+        size_t items = ((size_t)R - derived_rows) * J;
         uint32_t m = maxc;
         for (int pass = 0; m > 0; ++pass) {
             // piece length for this pass: long pieces when segments are long
@@ -536,13 +587,13 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
             if (Cp == (uint32_t)kPieceLong) {
                 auto k = dev::k_seg_prod<S4, C::TH, kPieceLong>;
                 const int grid = occupancy_grid(*c, k, 2 * P, NI);
-                ProfScope prof_(*c, 0);
+                ProfScope prof_(*c, 0, 2 * (items - P)); // each piece: len − 1 products, G and H
                 k<<<grid, dev::kBlock, 0, st>>>(arg(c->mod_n2), pieces, order, P, pass == 0 ? sorted : nullptr, src,
                                                 dst, next_job);
             } else {
                 auto k = dev::k_seg_prod<S4, C::TH, kPiece>;
                 const int grid = occupancy_grid(*c, k, 2 * P, NI);
-                ProfScope prof_(*c, 0);
+                ProfScope prof_(*c, 0, 2 * (items - P));
                 k<<<grid, dev::kBlock, 0, st>>>(arg(c->mod_n2), pieces, order, P, pass == 0 ? sorted : nullptr, src,
                                                 dst, next_job);
             }
@@ -559,8 +610,90 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
         auto kf = dev::k_hist_finalize<S4, C::TH>;
         constexpr int NI = dev::kBlock / C::TH;
         const int grid = occupancy_grid(*c, kf, 2 * nkeys, NI);
-        kf<<<grid, dev::kBlock, 0, st>>>(arg(c->mod_n2), count, final_idx, nkeys, final_part, d_out, mont_out);
+        if (!tree) {
+            kf<<<grid, dev::kBlock, 0, st>>>(arg(c->mod_n2), count, final_idx, nkeys, final_part, d_out, mont_out);
+            check_launch(*c);
+            return;
+        }
+        // tree mode: all nodes in Montgomery form in the context's current buffer
+        uint32_t *hist = (uint32_t *)grow(c->tree_buf[c->tree_cur ^ 1], (size_t)N * spn * S4 * 4 + 64);
+        kf<<<grid, dev::kBlock, 0, st>>>(arg(c->mod_n2), count, final_idx, nkeys, final_part, hist, 1);
         check_launch(*c);
+        bool derived_ok = true;
+        if (!pairs.empty()) {
+            const size_t m = pairs.size() * spn; // values to invert
+            // level sizes of the product tree
+            std::vector<size_t> lvl_n{m}, lvl_off{0};
+            while (lvl_n.back() > 1) {
+                lvl_off.push_back(lvl_off.back() + lvl_n.back());
+                lvl_n.push_back((lvl_n.back() + 1) / 2);
+            }
+            const size_t total = lvl_off.back() + lvl_n.back();
+            uint32_t *tr = bget<uint32_t>(B.tree_up, total * S4);
+            uint32_t *inv = bget<uint32_t>(B.tree_dn, total * S4);
+            {
+                const size_t words = m * S4;
+                const int gg = (int)std::min<size_t>((words + 255) / 256, (size_t)c->sms * 16);
+                dev::k_gather_small<<<gg, 256, 0, st>>>(hist, d_pairs, pairs.size(), spn, S4, tr);
+                check_launch(*c);
+            }
+            auto kup = dev::k_pair_up<S4, C::TH>;
+            for (size_t l = 0; l + 1 < lvl_n.size(); ++l) {
+                const int gu = occupancy_grid(*c, kup, lvl_n[l + 1], NI);
+                ProfScope prof_(*c, 3, lvl_n[l] / 2);
+                kup<<<gu, dev::kBlock, 0, st>>>(arg(c->mod_n2), tr + lvl_off[l] * S4, lvl_n[l],
+                                               tr + lvl_off[l + 1] * S4);
+                check_launch(*c);
+            }
+            // invert the root on the host (plain value, binary extended Euclid)
+            std::vector<uint32_t> root(S4);
+            CK(cudaMemcpyAsync(root.data(), tr + lvl_off.back() * S4, S4 * 4, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            host::Big plain = c->mh_n2->from_mont(host::from_words(root.data(), S4)), rinv;
+            if (!host::inv_mod_odd(plain, c->n2, rinv)) {
+                derived_ok = false; // some slot is not a unit: build those nodes directly below
+            } else {
+                host::Big rinv_m = host::pad(c->mh_n2->to_mont(rinv), S4);
+                CK(cudaMemcpyAsync(inv + lvl_off.back() * S4, rinv_m.data(), S4 * 4, cudaMemcpyHostToDevice, st));
+                auto kdn = dev::k_pair_down<S4, C::TH>;
+                for (size_t l = lvl_n.size() - 1; l-- > 0;) {
+                    const int gd = occupancy_grid(*c, kdn, lvl_n[l], NI);
+                    ProfScope prof_(*c, 3, lvl_n[l]);
+                    kdn<<<gd, dev::kBlock, 0, st>>>(arg(c->mod_n2), inv + lvl_off[l + 1] * S4, tr + lvl_off[l] * S4,
+                                                    lvl_n[l], inv + lvl_off[l] * S4);
+                    check_launch(*c);
+                }
+                CK(cudaStreamSynchronize(st)); // rinv_m is a host temporary
+                auto kd = dev::k_derive<S4, C::TH>;
+                const int gdv = occupancy_grid(*c, kd, m, NI);
+                ProfScope prof_(*c, 3, m);
+                kd<<<gdv, dev::kBlock, 0, st>>>(arg(c->mod_n2), (const uint32_t *)c->tree_buf[c->tree_cur].p, inv,
+                                                d_pairs, pairs.size(), spn, hist);
+                check_launch(*c);
+            }
+        }
+        if (!derived_ok) {
+            // exact fallback: rebuild this level without sibling subtraction
+            c->tree_valid = false;
+            std::vector<int32_t> none(N, -1);
+            accumulate_dev(c, g, d_bins, J, d_offsets, N, d_rows, R, K, d_out, mont_out, nullptr, none.data(),
+                           h_offsets);
+            return;
+        }
+        if (mont_out) {
+            CK(cudaMemcpyAsync(d_out, hist, (size_t)N * spn * S4 * 4, cudaMemcpyDeviceToDevice, st));
+        } else {
+            auto kc = dev::k_from_mont_copy<S4, C::TH>;
+            const int gc = occupancy_grid(*c, kc, (size_t)N * spn, NI);
+            kc<<<gc, dev::kBlock, 0, st>>>(arg(c->mod_n2), hist, (size_t)N * spn, d_out);
+            check_launch(*c);
+        }
+        c->tree_cur ^= 1;
+        c->tree_valid = true;
+        c->tree_gh = g;
+        c->tree_J = J;
+        c->tree_K = K;
+        c->tree_N = N;
     });
 }
 
@@ -679,6 +812,7 @@ int sfxb_ctx_create(sfxb_ctx **out, int device, const uint32_t *n, uint32_t n_wo
         c->d_n4 = dev_big(*c, N, 4 * s);
         c->d_n2w = dev_big(*c, c->n2, 4 * s);
         host::MontHost mn2(c->n2, 4 * s);
+        c->mh_n2 = std::make_unique<host::MontHost>(c->n2, 4 * s);
         c->d_nR_n2 = dev_big(*c, mn2.to_mont(N), 4 * s);
         c->d_dig_n = dev_digits(*c, N, kWindowN, c->nd_n);
         if (p && q && pq_words) {
@@ -740,6 +874,8 @@ void sfxb_ctx_destroy(sfxb_ctx *c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (void *d : c->owned) cudaFree(d);
     if (c->scratch_table.p) cudaFree(c->scratch_table.p);
+    for (auto &b : c->tree_buf)
+        if (b.p) cudaFree(b.p);
     for (auto &b : c->tmp)
         if (b.p) cudaFree(b.p);
     for (auto &b : c->host_pinned)
@@ -767,6 +903,12 @@ int sfxb_ctx_profile(sfxb_ctx *c, int enable) {
         }
         c->profile = enable != 0;
     });
+}
+
+int sfxb_ctx_kernel_stats(sfxb_ctx *c, int family, uint64_t *launches, double *ms, uint64_t *modmuls) {
+    int rc = sfxb_ctx_kernel_time(c, family, launches, ms);
+    if (rc == SFXB_OK && modmuls) *modmuls = c->prof[family].modmuls;
+    return rc;
 }
 
 int sfxb_ctx_kernel_time(sfxb_ctx *c, int family, uint64_t *launches, double *ms) {
@@ -921,6 +1063,7 @@ int sfxb_gh_from_dev(sfxb_ctx *c, const uint32_t *d_gh, uint32_t n_samples, sfxb
 
 void sfxb_gh_free(sfxb_gh *g) {
     if (!g) return;
+    if (g->ctx->tree_gh == g) g->ctx->tree_valid = false;
     cudaSetDevice(g->ctx->device);
     cudaStreamSynchronize(g->ctx->stream);
     cudaFree(g->d);
@@ -985,6 +1128,45 @@ int sfxb_accumulate_gh(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *bins, uint
         accumulate_dev(c, g, db.p, J, doff.p, N, drows.p, R, K, dout.p, 0, additions);
         d2h_padded(c, out_slots, dout.p, nslots, 2 * c->nw, S4);
     });
+}
+
+int sfxb_accumulate_tree_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint32_t n_features,
+                             const uint32_t *d_node_offsets, const uint32_t *h_node_offsets, uint32_t n_nodes,
+                             const uint32_t *d_rows, uint32_t n_rows, uint32_t n_bins, const int32_t *h_parent,
+                             uint32_t *d_out, int mont_out, uint64_t *additions) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (!h_parent) throw ApiError(SFXB_ERR_ARG, "accumulate_tree: parent indices required");
+        accumulate_dev(c, g, d_bins, n_features, d_node_offsets, n_nodes, d_rows, n_rows, n_bins, d_out, mont_out,
+                       additions, h_parent, h_node_offsets);
+    });
+}
+
+int sfxb_accumulate_tree_gh(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *bins, uint32_t J,
+                            const uint32_t *node_offsets, uint32_t N, const uint32_t *rows, uint32_t K,
+                            const int32_t *parent, uint32_t *out_slots, uint64_t *additions) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (!g || g->ctx != c) throw ApiError(SFXB_ERR_ARG, "accumulate: gradient handle belongs to another context");
+        if (!parent) throw ApiError(SFXB_ERR_ARG, "accumulate_tree: parent indices required");
+        for (uint32_t i = 0; i < N; ++i)
+            if (node_offsets[i + 1] < node_offsets[i]) throw ApiError(SFXB_ERR_ARG, "accumulate: node offsets decrease");
+        if (N && node_offsets[0] != 0) throw ApiError(SFXB_ERR_ARG, "accumulate: node offsets must start at 0");
+        const uint32_t R = N ? node_offsets[N] : 0;
+        const size_t S4 = 4 * (size_t)c->s, nslots = 2ull * N * J * K, n_samples = g->n_samples;
+        IoBuf<uint16_t> db(c->io[0], (size_t)J * n_samples);
+        IoBuf<uint32_t> doff(c->io[1], (size_t)N + 1), drows(c->io[2], R ? R : 1), dout(c->io[3], nslots * S4);
+        if ((size_t)J * n_samples)
+            CK(cudaMemcpyAsync(db.p, bins, (size_t)J * n_samples * 2, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(doff.p, node_offsets, ((size_t)N + 1) * 4, cudaMemcpyHostToDevice, c->stream));
+        if (R) CK(cudaMemcpyAsync(drows.p, rows, (size_t)R * 4, cudaMemcpyHostToDevice, c->stream));
+        accumulate_dev(c, g, db.p, J, doff.p, N, drows.p, R, K, dout.p, 0, additions, parent, node_offsets);
+        d2h_padded(c, out_slots, dout.p, nslots, 2 * c->nw, S4);
+    });
+}
+
+int sfxb_tree_reset(sfxb_ctx *c) {
+    return guard(c, [&] { c->tree_valid = false; });
 }
 
 int sfxb_reduce_partials_dev(sfxb_ctx *c, const uint32_t *d_parts, uint32_t parts, size_t n_slots, uint32_t *d_out) {

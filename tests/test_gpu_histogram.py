@@ -123,3 +123,63 @@ def test_partial_reduce_equals_full_histogram():
     ops.reduce_partials(parts, 2, n_slots, out)
     got = out.cpu().numpy().view(np.uint32)
     assert np.array_equal(got, full)
+
+
+def _random_tree(rng, n_samples, depth, leaf_prob=0.15):
+    """Frontiers of a random tree: children partition their parent; some
+    nodes become leaves (leave the frontier); child order random; the root's
+    first split sends every row to one side (an empty child)."""
+    levels = [([list(range(n_samples))], [-1])]
+    for d in range(1, depth):
+        nodes, parents = [], []
+        for pi, rows in enumerate(levels[-1][0]):
+            if d > 1 and rng.random() < leaf_prob:
+                continue
+            cut = 1.0 if d == 1 else rng.random()
+            left = [r for r in rows if rng.random() < cut]
+            ls = set(left)
+            right = [r for r in rows if r not in ls]
+            for child in ([left, right] if rng.random() < 0.5 else [right, left]):
+                nodes.append(child)
+                parents.append(pi)
+        levels.append((nodes, parents))
+    return levels
+
+
+@pytest.mark.parametrize("kname,shape", [("k512_c0ffee", (400, 3, 8, 4)), ("k2048_7", (300, 2, 16, 3))])
+def test_tree_mode_sibling_subtraction_is_bit_exact(kname, shape):
+    """Sibling subtraction (hist(parent)·hist(small)^-1) == direct histograms,
+    level by level, incl. leaves, empty children and trivial-zero inputs."""
+    import torch
+
+    n_samples, J, K, depth = shape
+    n, p, q = key(kname)
+    ctx = _lib.Context(n)
+    ops = _lib.DeviceOps(ctx)
+    rng = random.Random(kname)
+    cts = [rng.randrange(2, n * n) for _ in range(2 * n_samples)]
+    cts[3] = 1
+    cw = ints_to_words(cts, ctx.ct_words)
+    bins = np.array([[rng.randrange(K) for _ in range(n_samples)] for _ in range(J)], np.uint16)
+    gh = ops.gh_upload(cw)
+    levels = _random_tree(rng, n_samples, depth)
+    for lvl, (nodes, parents) in enumerate(levels):
+        offs, rows = frontier(nodes)
+        want, want_adds = ctx.accumulate(cw, bins, offs, rows, K)
+        got, adds = ops.accumulate_tree_host(gh, bins, offs, rows, K, np.array(parents, np.int32))
+        bad = sorted({i // (J * K * 2) for i in np.nonzero((got != want).any(axis=1))[0]})
+        assert not bad, (lvl, bad, parents)
+        assert adds == want_adds
+    # device-buffer variant on a fresh cache
+    ops.tree_reset()
+    dev = torch.device("cuda:0")
+    d_bins = torch.from_numpy(bins.astype(np.int16).copy()).to(dev)
+    for nodes, parents in levels:
+        offs, rows = frontier(nodes)
+        want, _ = ctx.accumulate(cw, bins, offs, rows, K)
+        out = torch.zeros((len(nodes) * J * K * 2, ctx.ct_words), dtype=torch.int32, device=dev)
+        d_off = torch.from_numpy(offs.astype(np.int32)).to(dev)
+        d_rows = torch.from_numpy(rows.astype(np.int32) if len(rows) else np.zeros(1, np.int32)).to(dev)
+        ops.accumulate_tree(gh, d_bins, J, d_off, offs, len(nodes), d_rows, len(rows), K,
+                            np.array(parents, np.int32), out)
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), want)
