@@ -151,6 +151,8 @@ int sfxb_accumulate_tree_gh(sfxb_ctx *ctx, const sfxb_gh *gh, const uint16_t *bi
                             uint32_t n_bins, const int32_t *parent, uint32_t *out_slots,
                             uint64_t *additions);
 int sfxb_tree_reset(sfxb_ctx *ctx);
+/* number of frontier nodes obtained by sibling subtraction on this context */
+uint64_t sfxb_ctx_tree_derived(const sfxb_ctx *ctx);
 
 /* K4: element-wise product of `parts` partial histograms (Montgomery form,
  * each n_slots ciphertexts, contiguous) into d_out (plain form, n_slots).

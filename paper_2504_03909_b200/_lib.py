@@ -83,6 +83,7 @@ def load() -> C.CDLL:
         "sfxb_accumulate_tree_gh": (C.c_int, [vp, vp, _u16p, C.c_uint32, _u32p, C.c_uint32, _u32p, C.c_uint32,
                                               _i32p, _u32p, C.POINTER(C.c_uint64)]),
         "sfxb_tree_reset": (C.c_int, [vp]),
+        "sfxb_ctx_tree_derived": (C.c_uint64, [vp]),
         "sfxb_reduce_partials_dev": (C.c_int, [vp, vp, C.c_uint32, sz, vp]),
         "sfxb_decrypt": (C.c_int, [vp, _u32p, sz, C.c_uint32, _f64p, vp, C.POINTER(C.c_uint64)]),
         "sfxb_decrypt_dev": (C.c_int, [vp, vp, sz, C.c_uint32, vp, vp, C.POINTER(C.c_uint64)]),

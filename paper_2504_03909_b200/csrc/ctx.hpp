@@ -77,6 +77,7 @@ struct CtxState {
     bool tree_valid = false;
     const void *tree_gh = nullptr;
     uint32_t tree_J = 0, tree_K = 0, tree_N = 0;
+    uint64_t tree_derived_nodes = 0; // nodes obtained by sibling subtraction so far
     std::unique_ptr<host::MontHost> mh_n2;
 
     // scratch (grown on demand, freed with the context)

@@ -688,6 +688,7 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
             kc<<<gc, dev::kBlock, 0, st>>>(arg(c->mod_n2), hist, (size_t)N * spn, d_out);
             check_launch(*c);
         }
+        c->tree_derived_nodes += pairs.size();
         c->tree_cur ^= 1;
         c->tree_valid = true;
         c->tree_gh = g;
@@ -1164,6 +1165,8 @@ int sfxb_accumulate_tree_gh(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *bins,
         d2h_padded(c, out_slots, dout.p, nslots, 2 * c->nw, S4);
     });
 }
+
+uint64_t sfxb_ctx_tree_derived(const sfxb_ctx *c) { return c->tree_derived_nodes; }
 
 int sfxb_tree_reset(sfxb_ctx *c) {
     return guard(c, [&] { c->tree_valid = false; });

@@ -22,6 +22,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -121,6 +122,12 @@ public:
         open_ctx(&kp);
     }
     ~CudaPaillierPlugin() override {
+        if (std::getenv("SFXB_PLUGIN_VERBOSE") && ctx_)
+            std::fprintf(stderr, "[sfxb-cuda-plugin] key=%016llx enc=%llu adds=%llu dec=%llu derived_nodes=%llu launches=%llu\n",
+                         (unsigned long long)pub_.key_id, (unsigned long long)counters_.encryptions,
+                         (unsigned long long)counters_.ciphertext_additions,
+                         (unsigned long long)counters_.decryptions,
+                         (unsigned long long)sfxb_ctx_tree_derived(ctx_), (unsigned long long)sfxb_ctx_launches(ctx_));
         if (gh_) sfxb_gh_free(gh_);
         if (ctx_) sfxb_ctx_destroy(ctx_);
         gmp_randclear(rng_);
@@ -210,11 +217,38 @@ public:
         for (size_t i = 0; i < N; ++i) offs[i + 1] = offs[i] + (uint32_t)nodes[i].rows.size();
         rows.reserve(offs[N]);
         for (const NodeRows &nd : nodes) rows.insert(rows.end(), nd.rows.begin(), nd.rows.end());
+        // Sibling subtraction: the reference's next frontier lists the two
+        // children of each split node consecutively, in parent order
+        // (federation.cpp:591-592).  A parent is accepted only when the merged
+        // rows of the pair equal its rows exactly and the features, bins and
+        // gradients are those of the previous call.
+        const uint64_t bins_key = bins_fingerprint(flat, feature_ids, n_bins);
+        std::vector<int32_t> parent(N, -1);
+        if (prev_valid_ && prev_bins_key_ == bins_key && prev_gh_ == gh_) {
+            size_t p = 0;
+            for (size_t i = 0; i + 1 < N && p < prev_rows_.size(); ) {
+                const auto &a = nodes[i].rows, &b = nodes[i + 1].rows;
+                size_t q = p;
+                while (q < prev_rows_.size() && prev_rows_[q].size() != a.size() + b.size()) ++q;
+                if (q < prev_rows_.size() && merged_equals(a, b, prev_rows_[q])) {
+                    parent[i] = parent[i + 1] = (int32_t)q;
+                    p = q + 1;
+                    i += 2;
+                } else {
+                    ++i;
+                }
+            }
+        }
         std::vector<uint32_t> slots(N * J * K * 2 * ct_words_);
         uint64_t adds = 0;
         if (N && J && K)
-            check(sfxb_accumulate_gh(ctx_, gh_, flat.data(), (uint32_t)J, offs.data(), (uint32_t)N, rows.data(),
-                                     (uint32_t)K, slots.data(), &adds));
+            check(sfxb_accumulate_tree_gh(ctx_, gh_, flat.data(), (uint32_t)J, offs.data(), (uint32_t)N, rows.data(),
+                                          (uint32_t)K, parent.data(), slots.data(), &adds));
+        prev_valid_ = N && J && K;
+        prev_bins_key_ = bins_key;
+        prev_gh_ = gh_;
+        prev_rows_.resize(N);
+        for (size_t i = 0; i < N; ++i) prev_rows_[i] = nodes[i].rows;
         counters_.ciphertext_additions += adds;
         const size_t per_node = 2 * J * K;
         out.nodes.resize(N);
@@ -348,6 +382,28 @@ private:
         }
     }
 
+    static bool merged_equals(const std::vector<std::uint32_t> &a, const std::vector<std::uint32_t> &b,
+                              const std::vector<std::uint32_t> &p) {
+        if (a.size() + b.size() != p.size()) return false;
+        size_t i = 0, j = 0;
+        for (std::uint32_t v : p) {
+            if (i < a.size() && a[i] == v) ++i;
+            else if (j < b.size() && b[j] == v) ++j;
+            else return false;
+        }
+        return i == a.size() && j == b.size();
+    }
+
+    static uint64_t bins_fingerprint(const std::vector<uint16_t> &flat, const std::vector<int> &fids, int n_bins) {
+        uint64_t h = 14695981039346656037ULL ^ (uint64_t)n_bins;
+        for (int f : fids) h = (h ^ (uint32_t)f) * 1099511628211ULL;
+        const uint64_t *w = reinterpret_cast<const uint64_t *>(flat.data());
+        const size_t n64 = flat.size() / 4;
+        for (size_t i = 0; i < n64; ++i) h = (h ^ w[i]) * 1099511628211ULL;
+        for (size_t i = n64 * 4; i < flat.size(); ++i) h = (h ^ flat[i]) * 1099511628211ULL;
+        return h;
+    }
+
     // Device-resident gh keyed on the ciphertext contents: one parallel
     // read-only pass hashes the mpz limbs (and applies the checks); only on a
     // miss are the limbs marshalled and uploaded (sfxb_gh_upload).
@@ -438,6 +494,11 @@ private:
     sfxb_ctx *ctx_ = nullptr;
     size_t n_words_ = 0, ct_words_ = 0;
     sfxb_gh *gh_ = nullptr;
+    // previous accumulate call (sibling-subtraction parents)
+    bool prev_valid_ = false;
+    uint64_t prev_bins_key_ = 0;
+    const sfxb_gh *prev_gh_ = nullptr;
+    std::vector<std::vector<std::uint32_t>> prev_rows_;
     uint64_t gh_hash_ = 0;
     size_t gh_count_ = 0;
     std::unique_ptr<EncryptionPlugin> ref_;

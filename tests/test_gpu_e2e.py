@@ -29,11 +29,12 @@ def _train_with_plugin(name):
     from make_golden import TRAIN_CONFIGS
 
     ini, bits, seed = TRAIN_CONFIGS[name]
-    env = dict(os.environ, LD_PRELOAD=PLUGIN)
+    env = dict(os.environ, LD_PRELOAD=PLUGIN, SFXB_PLUGIN_VERBOSE="1")
     out = subprocess.run([sys.executable, os.path.join(HERE, "train_driver.py"), os.path.join(HERE, "configs", ini),
                           str(bits), str(seed)], env=env, capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stderr[-2000:]
-    return json.loads(out.stdout)
+    stats = [ln for ln in out.stderr.splitlines() if ln.startswith("[sfxb-cuda-plugin]")]
+    return json.loads(out.stdout), stats
 
 
 @pytest.mark.parametrize("name", ["vertical_toy512", "vertical_threaded_3p", "vertical_c1_1024"])
@@ -43,7 +44,10 @@ def test_reference_training_loop_with_gpu_plugin(name):
     gpath = os.path.join(HERE, "golden", f"train_{name}.json")
     _need(gpath)
     want = json.load(open(gpath))
-    got = _train_with_plugin(name)
+    got, stats = _train_with_plugin(name)
+    # every party's plugin was the GPU adapter, and sibling subtraction derived nodes
+    assert len(stats) >= 2
+    assert sum(int(s.split("derived_nodes=")[1].split()[0]) for s in stats) > 0
     assert got["forest"] == want["forest"]
     assert got["partials"] == want["partials"]
     assert got["counters"] == want["counters"]
