@@ -35,6 +35,7 @@ exchanged with all_to_all and reduced by the K4 kernel (strong scaling).
 from __future__ import annotations
 
 import argparse
+import collections
 import json
 import os
 import statistics
@@ -252,7 +253,9 @@ def run_reference(a):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "u32", "data": "synthetic", "config": config(a, world),
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": dict(config(a, world), histogram="reference PaillierPlugin::accumulate_rows (direct folds)",
+                       parallelism=f"{last['cores']} host threads, one plugin instance each, feature-sliced"),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": last["kind"],
                          "sample": last["sample"]},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -390,44 +393,69 @@ def run_ours(a):
     # ---- e2e through the C ABI with host buffers
     h_bins = [torch.from_numpy(b[:, lo:hi].copy()).pin_memory().numpy() for b in bins_pp]
     h_front = [(o, torch.from_numpy(r.astype(np.int32)).pin_memory().numpy().view(np.uint32)) for o, r in fronts]
-    h_out = [torch.empty((n_slots[d], cw), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
-             for d in range(D)]
     h2d = d2h = 0
     e2e_times = []
     gh_np = gh_host.numpy().view(np.uint32)
+    def e2e_party(pi, counters):
+        # one party's calls for one tree (the adapter's pattern: gh up once,
+        # then per level bins + frontier up, slots down)
+        tg = time.perf_counter()
+        g = ops[pi].gh_upload(gh_np)
+        e2e_phase["gh_upload"] += time.perf_counter() - tg
+        h2d_p, d2h_p = gh_np.nbytes, 0
+        for d in range(D):
+            offs, rows = h_front[d]
+            if world > 1:
+                outp = outs[d][pi]
+                ops[pi].accumulate_tree(g, d_bins[pi], J, d_front[d][0], offs, len(offs) - 1, d_front[d][1],
+                                        len(rows), K, parents[d], outp, mont_out=True)
+                recv = pdist.exchange(outp, world)
+                fin = pdist.reduce_slice(recv, lambda parts, k, sl, out: ops[pi].reduce_partials(parts, k, sl, out))
+                full = pdist.gather_slices(fin, n_slots[d], world)
+                if rank == 0:
+                    h_out[pi][d][:] = full.cpu().numpy().view(np.uint32)
+                    d2h_p += h_out[pi][d].nbytes
+            elif a.no_tree:
+                ops[pi].accumulate_host(g, h_bins[pi], offs, rows, K, out=h_out[pi][d])
+                d2h_p += h_out[pi][d].nbytes
+            else:
+                ta = time.perf_counter()
+                ops[pi].accumulate_tree_host(g, h_bins[pi], offs, rows, K, parents[d], out=h_out[pi][d])
+                e2e_phase[f"level{d}"] += time.perf_counter() - ta
+                d2h_p += h_out[pi][d].nbytes
+            h2d_p += h_bins[pi].nbytes + offs.nbytes + rows.nbytes
+        g.free()
+        counters[pi] = (h2d_p, d2h_p)
+
+    e2e_phase = collections.defaultdict(float)
+    h_out = [[torch.empty((n_slots[d], cw), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+              for d in range(D)] for _ in range(a.parties)]
+    # parties one after the other (the reference's default threaded=false order;
+    # concurrent parties on one GPU only contend for the same SMs)
+    concurrent = False
     for it in range(1 + max(1, a.e2e_steps)):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        counters = [None] * a.parties
         t0 = time.perf_counter()
-        h2d = d2h = 0
-        for pi in range(a.parties):
-            g = ops[pi].gh_upload(gh_np)
-            h2d += gh_np.nbytes
-            for d in range(D):
-                offs, rows = h_front[d]
-                if world > 1:
-                    outp = outs[d][pi]
-                    ops[pi].accumulate(g, d_bins[pi], J, d_front[d][0], len(offs) - 1, d_front[d][1],
-                                       len(rows), K, outp, mont_out=True)
-                    recv = pdist.exchange(outp, world)
-                    fin = pdist.reduce_slice(recv, lambda parts, k, sl, out: ops[pi].reduce_partials(parts, k, sl, out))
-                    full = pdist.gather_slices(fin, n_slots[d], world)
-                    if rank == 0:
-                        h_out[d][:] = full.cpu().numpy().view(np.uint32)
-                    h2d += h_bins[pi].nbytes + offs.nbytes + rows.nbytes
-                    d2h += h_out[d].nbytes if rank == 0 else 0
-                elif a.no_tree:
-                    ops[pi].accumulate_host(g, h_bins[pi], offs, rows, K, out=h_out[d])
-                else:
-                    ops[pi].accumulate_tree_host(g, h_bins[pi], offs, rows, K, parents[d], out=h_out[d])
-                    h2d += h_bins[pi].nbytes + offs.nbytes + rows.nbytes
-                    d2h += h_out[d].nbytes
-            g.free()
+        if concurrent:
+            ths = [threading.Thread(target=e2e_party, args=(pi, counters)) for pi in range(a.parties)]
+            for th in ths:
+                th.start()
+            for th in ths:
+                th.join()
+        else:
+            for pi in range(a.parties):
+                e2e_party(pi, counters)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
+        h2d = sum(c[0] for c in counters)
+        d2h = sum(c[1] for c in counters)
         if it > 0:  # first iteration is a warm-up
             e2e_times.append(dt)
+        else:
+            e2e_phase.clear()
     e2e = torch.tensor([statistics.median(e2e_times)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
@@ -484,7 +512,12 @@ def run_ours(a):
             "encrypt_2M": 2 * a.rows / enc_per_s, "histogram": ms_step / 1e3,
             "decrypt_occupied": sum(n_slots) * a.parties / dec_per_s,
         },
-        "e2e": {"value": e2e.item(), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "e2e": {"value": e2e.item(), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "pattern": "C ABI with pinned host buffers: per party sfxb_gh_upload once per tree, then per level "
+                           "sfxb_accumulate_tree_gh (bins + frontier up, slots down), parties in sequence"
+                           if world == 1 else
+                           "per party gh up, device histograms, all_to_all + K4, slots gathered to rank 0"},
+        "e2e_phase_s": {k: v / max(1, len(e2e_times)) for k, v in e2e_phase.items()},
         "gpu_launches": int(launches),
         "roofline": {
             "bound": "imad", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tproducts/s",

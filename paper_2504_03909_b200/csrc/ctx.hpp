@@ -83,6 +83,9 @@ struct CtxState {
     // scratch (grown on demand, freed with the context)
     Buf scratch_table, tmp[4], host_pinned[2], io[6]; // io: host-API staging (grow-only)
     std::vector<void *> owned; // device allocations of constants
+    // one spare gh allocation (limbs + flags), recycled by the next upload
+    void *spare_gh = nullptr, *spare_flags = nullptr;
+    size_t spare_gh_bytes = 0, spare_flags_bytes = 0;
 };
 
 constexpr int kWindow = 5; // fixed exponent window for the 1024-bit CRT exponents

@@ -26,6 +26,7 @@ struct sfxb_gh {
     uint32_t *d = nullptr;     // 2·n_samples × 4s limbs, Montgomery form
     uint8_t *flags = nullptr;  // per row: bit0 Enc(g) == 1, bit1 Enc(h) == 1
     uint32_t n_samples = 0;
+    size_t bytes = 0, fbytes = 0;
 };
 
 namespace {
@@ -398,8 +399,20 @@ sfxb_gh *gh_alloc(sfxb_ctx *c, uint32_t n_samples) {
     auto g = std::make_unique<sfxb_gh>();
     g->ctx = c;
     g->n_samples = n_samples;
-    CK(cudaMalloc(&g->d, (size_t)n_samples * 2 * 4 * c->s * 4 + 16));
-    CK(cudaMalloc(&g->flags, (size_t)n_samples + 16));
+    const size_t bytes = (size_t)n_samples * 2 * 4 * c->s * 4 + 16, fbytes = (size_t)n_samples + 16;
+    if (c->spare_gh && c->spare_gh_bytes >= bytes && c->spare_flags_bytes >= fbytes) {
+        // recycle the spare allocation (one gh per tree: avoids a 1 GB free + malloc)
+        g->d = (uint32_t *)c->spare_gh;
+        g->flags = (uint8_t *)c->spare_flags;
+        g->bytes = c->spare_gh_bytes;
+        g->fbytes = c->spare_flags_bytes;
+        c->spare_gh = c->spare_flags = nullptr;
+        return g.release();
+    }
+    CK(cudaMalloc(&g->d, bytes));
+    CK(cudaMalloc(&g->flags, fbytes));
+    g->bytes = bytes;
+    g->fbytes = fbytes;
     return g.release();
 }
 
@@ -877,6 +890,8 @@ void sfxb_ctx_destroy(sfxb_ctx *c) {
     if (c->scratch_table.p) cudaFree(c->scratch_table.p);
     for (auto &b : c->tree_buf)
         if (b.p) cudaFree(b.p);
+    if (c->spare_gh) cudaFree(c->spare_gh);
+    if (c->spare_flags) cudaFree(c->spare_flags);
     for (auto &b : c->tmp)
         if (b.p) cudaFree(b.p);
     for (auto &b : c->host_pinned)
@@ -1064,11 +1079,19 @@ int sfxb_gh_from_dev(sfxb_ctx *c, const uint32_t *d_gh, uint32_t n_samples, sfxb
 
 void sfxb_gh_free(sfxb_gh *g) {
     if (!g) return;
-    if (g->ctx->tree_gh == g) g->ctx->tree_valid = false;
-    cudaSetDevice(g->ctx->device);
-    cudaStreamSynchronize(g->ctx->stream);
-    cudaFree(g->d);
-    cudaFree(g->flags);
+    sfxb_ctx *c = g->ctx;
+    if (c->tree_gh == g) c->tree_valid = false;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    if (!c->spare_gh) { // keep as the context's spare
+        c->spare_gh = g->d;
+        c->spare_flags = g->flags;
+        c->spare_gh_bytes = g->bytes;
+        c->spare_flags_bytes = g->fbytes;
+    } else {
+        cudaFree(g->d);
+        cudaFree(g->flags);
+    }
     delete g;
 }
 
