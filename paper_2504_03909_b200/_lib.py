@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libsfxb_cuda.so")
+LIB_PATH = os.environ.get("SFXB_LIB") or os.path.join(PKG, "lib", "libsfxb_cuda.so")
 
 SFXB_OK = 0
 SFXB_ERR_ARG = -1

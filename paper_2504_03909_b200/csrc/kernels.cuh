@@ -211,7 +211,6 @@ __global__ void __launch_bounds__(kBlock) k_enc_combine(EncArgs a, int crt) {
     constexpr int S2 = 2 * s, S4 = 4 * s, L2 = S2 / TPI, L4 = S4 / TPI, NI = kBlock / TPI;
     __shared__ uint2 sB[S4 / 2 * NI];
     const Stage st = make_stage<TPI>(sB);
-    const size_t gi = (size_t)blockIdx.x * NI + st.inst;
     const ModRef M4 = a.mod_n2.ref();
     uint32_t N4[L4];
     load_const<S4, TPI>(N4, M4, kMod);
@@ -386,7 +385,6 @@ __global__ void __launch_bounds__(kBlock) k_dec_combine(DecArgs a, uint32_t n_it
     constexpr int Sn = 2 * s, L1 = s / TPI, Ln = Sn / TPI, NI = kBlock / TPI;
     __shared__ uint2 sB[Sn / 2 * NI];
     const Stage st = make_stage<TPI>(sB);
-    const size_t gi = (size_t)blockIdx.x * NI + st.inst;
     const ModRef M1 = a.mod_pq[0].ref(), Mn = a.mod_n.ref();
     uint32_t N1[L1], Nn[Ln];
     load_const<s, TPI>(N1, M1, kMod);

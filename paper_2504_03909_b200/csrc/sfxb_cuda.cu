@@ -106,15 +106,6 @@ void *grow(Buf &b, size_t bytes) {
     }
     return b.p;
 }
-void *grow_pinned(Buf &b, size_t bytes) {
-    if (b.bytes < bytes) {
-        if (b.p) CK(cudaFreeHost(b.p));
-        b.p = nullptr;
-        CK(cudaMallocHost(&b.p, bytes));
-        b.bytes = bytes;
-    }
-    return b.p;
-}
 
 dev::ModArg arg(const DevMod &m) { return dev::ModArg{m.w, m.np}; }
 
@@ -136,9 +127,21 @@ template <>
 struct Cls<16> {
     static constexpr int T1 = 1, T2 = 2, TC = 4, TD = 2, TE = 2, TH = 4, TN = 4;
 };
+#ifndef SFXB_T1_32
+#define SFXB_T1_32 1
+#endif
+#ifndef SFXB_T2_32
+#define SFXB_T2_32 4
+#endif
+#ifndef SFXB_TD_32
+#define SFXB_TD_32 2
+#endif
+#ifndef SFXB_TH_32
+#define SFXB_TH_32 4
+#endif
 template <>
-struct Cls<32> {
-    static constexpr int T1 = 2, T2 = 4, TC = 8, TD = 4, TE = 4, TH = 8, TN = 8;
+struct Cls<32> { // 2048-bit keys (tuned on B200, profiles/)
+    static constexpr int T1 = SFXB_T1_32, T2 = SFXB_T2_32, TC = 8, TD = SFXB_TD_32, TE = 4, TH = SFXB_TH_32, TN = 8;
 };
 template <>
 struct Cls<48> {
