@@ -21,6 +21,15 @@ struct ModArg {
     __device__ __forceinline__ ModRef ref() const { return ModRef{w, np}; }
 };
 
+// Plain word i of the instance's staging area: the low/high half of pair
+// i/2 in the swizzled b_slot layout (so staging never aliases another
+// instance's slots, see mont.cuh).
+template <int TPI>
+__device__ __forceinline__ uint32_t *staged_ptr(const Stage &st, int i) {
+    constexpr int NIc = kBlock / TPI;
+    return reinterpret_cast<uint32_t *>(st.sB + b_slot<NIc>(i >> 1, st.inst)) + (i & 1);
+}
+
 // Redistribute a value between two lane layouts of the same TPI through the
 // instance's staging buffer: `src` has Ssrc limbs (Ssrc/TPI per lane), the
 // result has Sdst limbs (zero-extended or truncated).
@@ -28,35 +37,30 @@ template <int Ssrc, int Sdst, int TPI>
 __device__ __forceinline__ void relayout(uint32_t (&dst)[Sdst / TPI], const uint32_t (&src)[Ssrc / TPI],
                                          const Stage &st) {
     constexpr int Ls = Ssrc / TPI, Ld = Sdst / TPI;
-    uint32_t *w = reinterpret_cast<uint32_t *>(st.sB);
     const int t = inst_lane<TPI>();
     __syncwarp();
-    // plain word layout per instance: word i at w[(i/2)·2·NI + 2·inst + (i&1)]
 #pragma unroll
     for (int k = 0; k < Ls; ++k) {
         const int i = t * Ls + k;
-        if (i < Sdst) w[(i >> 1) * 2 * st.NI + 2 * st.inst + (i & 1)] = src[k];
+        if (i < Sdst) *staged_ptr<TPI>(st, i) = src[k];
     }
     if constexpr (Sdst > Ssrc) {
 #pragma unroll
         for (int k = 0; k < Ld; ++k) {
             const int i = t * Ld + k;
-            if (i >= Ssrc) w[(i >> 1) * 2 * st.NI + 2 * st.inst + (i & 1)] = 0u;
+            if (i >= Ssrc) *staged_ptr<TPI>(st, i) = 0u;
         }
     }
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < Ld; ++k) {
-        const int i = t * Ld + k;
-        dst[k] = w[(i >> 1) * 2 * st.NI + 2 * st.inst + (i & 1)];
-    }
+    for (int k = 0; k < Ld; ++k) dst[k] = *staged_ptr<TPI>(st, t * Ld + k);
     __syncwarp();
 }
 
-// word i of the value last written by relayout/stage (all lanes may read)
+// word i of the value last written by relayout (all lanes may read)
+template <int TPI>
 __device__ __forceinline__ uint32_t staged_word(const Stage &st, int i) {
-    const uint32_t *w = reinterpret_cast<const uint32_t *>(st.sB);
-    return w[(i >> 1) * 2 * st.NI + 2 * st.inst + (i & 1)];
+    return *staged_ptr<TPI>(st, i);
 }
 
 // Grid-stride loop in which every instance of a block runs the same number
@@ -350,7 +354,7 @@ __global__ void __launch_bounds__(kBlock) k_dec_step(DecArgs a, uint32_t n_items
         uint32_t borrow = 1u;
 #pragma unroll
         for (int i = 0; i < s; ++i) {
-            const uint32_t ui = staged_word(st, i);
+            const uint32_t ui = staged_word<TPI>(st, i);
             const uint32_t xi = ui - borrow;
             borrow = ui < borrow ? 1u : 0u;
             uint32_t c = 0;
@@ -412,7 +416,7 @@ __global__ void __launch_bounds__(kBlock) k_dec_combine(DecArgs a, uint32_t n_it
         int cmpv = 0;
         for (int k = Sn - 1; k >= 0 && cmpv == 0; --k) {
             const uint32_t hn_k = (a.nw[k] >> 1) | (k + 1 < Sn ? (a.nw[k + 1] << 31) : 0u);
-            const uint32_t mk = staged_word(st, k);
+            const uint32_t mk = staged_word<TPI>(st, k);
             cmpv = mk > hn_k ? 1 : (mk < hn_k ? -1 : 0);
         }
         const bool neg = cmpv > 0;
@@ -421,7 +425,7 @@ __global__ void __launch_bounds__(kBlock) k_dec_combine(DecArgs a, uint32_t n_it
         uint32_t w_top = 0, w_1 = 0, w_2 = 0, prev1 = 0, prev2 = 0, bw = 0;
         int topk = -1;
         for (int k = 0; k < Sn; ++k) {
-            const uint32_t mk = staged_word(st, k);
+            const uint32_t mk = staged_word<TPI>(st, k);
             uint32_t vk = mk;
             if (neg) {
                 const uint64_t diff = (uint64_t)a.nw[k] - mk - bw;

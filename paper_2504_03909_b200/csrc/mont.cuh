@@ -142,16 +142,19 @@ __device__ __forceinline__ uint32_t inst_ballot(bool pred) {
 
 // ---------------------------------------------------------------- shared-memory operand b
 //
-// Operand b of an instance lives in shared memory as S/2 limb pairs, pair i
-// of instance k at sB[i·NI + (k ^ (i/(L/2) mod NI))] (uint2), NI = instances
-// per block (a power of two).  The TPI lanes of an instance read the same pair
+// Operand b of an instance lives in shared memory as limb pairs: pair p of
+// instance k at sB[p·NI + (k ^ ((p >> 3) mod NI))] (uint2), NI = instances per
+// block (a power of two).  The TPI lanes of an instance read the same pair
 // (broadcast) and the instances of a warp read distinct 8-byte words
-// (conflict-free LDS.64); the XOR swizzle by the owning lane t = i/(L/2)
-// spreads the writes of the TPI lanes of one instance over distinct banks.
+// (conflict-free LDS.64).  The XOR swizzle spreads the writes of the lanes of
+// one instance (lane t owns pairs [t·L/2, (t+1)·L/2)) over distinct banks.
+// It depends on the pair index ONLY, so for every operand size and for the
+// plain word staging (relayout) an instance always owns the same slots —
+// instances of different warps never alias.
 
-template <int L, int NI>
+template <int NI>
 __device__ __forceinline__ int b_slot(int pair, int inst) {
-    return pair * NI + (inst ^ ((pair / (L / 2)) & (NI - 1)));
+    return pair * NI + (inst ^ ((pair >> 3) & (NI - 1)));
 }
 
 template <int S, int TPI>
@@ -159,7 +162,7 @@ __device__ __forceinline__ void store_b(uint2 *sB, int NI, int inst, const uint3
     constexpr int L = S / TPI, NIc = 128 / TPI;
     const int t = inst_lane<TPI>();
 #pragma unroll
-    for (int j = 0; j < L / 2; ++j) sB[b_slot<L, NIc>(t * (L / 2) + j, inst)] = make_uint2(v[2 * j], v[2 * j + 1]);
+    for (int j = 0; j < L / 2; ++j) sB[b_slot<NIc>(t * (L / 2) + j, inst)] = make_uint2(v[2 * j], v[2 * j + 1]);
     (void)NI;
 }
 
@@ -294,7 +297,7 @@ __device__ __forceinline__ void mont_mul(uint32_t (&r)[S / TPI], const uint32_t 
     constexpr int NIc = 128 / TPI;
 #pragma unroll U
     for (int i = 0; i < S / 2; ++i) {
-        const uint2 b = sB[b_slot<L, NIc>(i, inst)];
+        const uint2 b = sB[b_slot<NIc>(i, inst)];
         cios_step<L, TPI>(X, Y, Z, A, N, b.x, np, false);
         cios_step<L, TPI>(Y, X, Z, A, N, b.y, np, false);
     }

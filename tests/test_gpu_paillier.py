@@ -156,3 +156,38 @@ def test_decode_truncates_like_mpz_get_d(oracle):
     for m, v in zip(ms, vals):
         w = ok.decode_fixed(m)
         assert v == w or (np.isinf(v) and np.isinf(w) and (v > 0) == (w > 0)), (m, v, w)
+
+
+@pytest.mark.parametrize("kname", ["k1024_7", "k2048_7", "k3072_7"])
+def test_large_batches_equal_small_batches(oracle, kname):
+    """Multi-iteration grid-stride batches (every warp of every kernel busy,
+    instances of different warps at different phases) give the same
+    ciphertexts and plaintexts as one-wave batches, and match the oracle."""
+    import torch
+
+    n, p, q = key(kname)
+    ok = OracleKey(oracle, n, p, q)
+    ctx = _lib.Context(n, p, q)
+    ops = _lib.DeviceOps(ctx)
+    dev = torch.device("cuda:0")
+    count = {"k1024_7": 120_000, "k2048_7": 60_000, "k3072_7": 16_000}[kname]
+    chunk = 1000
+    g = torch.Generator(device=dev).manual_seed(9)
+    qf = torch.randint(-(1 << 40), 1 << 40, (count,), dtype=torch.int64, device=dev, generator=g)
+    r = torch.randint(-(2**31), 2**31 - 1, (count, ctx.nw), dtype=torch.int32, device=dev, generator=g)
+    r[:, -1] &= 0x3FFFFFFF
+    big = torch.empty((count, ctx.ct_words), dtype=torch.int32, device=dev)
+    ops.encrypt(qf, r, count, big)
+    small = torch.empty_like(big)
+    for s in range(0, count, chunk):
+        ops.encrypt(qf[s:s + chunk], r[s:s + chunk], min(chunk, count - s), small[s:s + chunk])
+    assert torch.equal(big, small)
+    c = big.cpu().numpy().view(np.uint32)
+    rr = r.cpu().numpy().view(np.uint32)
+    qq = qf.cpu().numpy()
+    for i in [0, 1, count // 3, count - 1]:
+        assert from_words(c[i]) == ok.encrypt_with_r(int(qq[i]) % n, from_words(rr[i]))
+    vals = torch.empty(count, dtype=torch.float64, device=dev)
+    decs = ops.decrypt(big, count, vals)
+    assert decs == count
+    np.testing.assert_array_equal(vals.cpu().numpy(), np.ldexp(qq.astype(np.float64), -40))
