@@ -275,6 +275,12 @@ inline bool inv_mod_odd(const Big &x_, const Big &M_, Big &out) {
     return true;
 }
 
+// x^-1 mod M through libgmp's mpz_invert when libgmp.so.10 can be loaded at
+// runtime (≈50 µs at 4096 bits; the reference links GMP anyway), else the
+// binary extended Euclid above (≈3.5 ms).  dlopen keeps GMP an optional
+// runtime dependency of libsfxb_cuda.so.
+bool inv_mod_fast(const Big &x, const Big &M, Big &out);
+
 // Fixed-window digits of e (most significant first), window w bits.
 inline std::vector<uint8_t> window_digits(const Big &e, int w) {
     size_t nb = std::max<size_t>(bit_length(e), 1);

@@ -9,6 +9,8 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+
 #include "../../include/sfxb_cuda.h"
 #include "bignum_host.hpp"
 #include "ctx.hpp"
@@ -19,6 +21,62 @@
 
 using namespace sfxb;
 using sfxb::host::Big;
+
+namespace sfxb {
+namespace host {
+namespace {
+// the GMP ABI subset used for inversion (x86-64 GMP 6: 64-bit limbs)
+struct GmpMpz {
+    int alloc, size;
+    void *d;
+};
+struct GmpApi {
+    void (*init)(GmpMpz *) = nullptr;
+    void (*clear)(GmpMpz *) = nullptr;
+    void (*import_)(GmpMpz *, size_t, int, size_t, int, size_t, const void *) = nullptr;
+    void *(*export_)(void *, size_t *, int, size_t, int, size_t, const GmpMpz *) = nullptr;
+    int (*invert)(GmpMpz *, const GmpMpz *, const GmpMpz *) = nullptr;
+    bool ok = false;
+    GmpApi() {
+        void *h = dlopen("libgmp.so.10", RTLD_NOW | RTLD_LOCAL);
+        if (!h) return;
+        init = (decltype(init))dlsym(h, "__gmpz_init");
+        clear = (decltype(clear))dlsym(h, "__gmpz_clear");
+        import_ = (decltype(import_))dlsym(h, "__gmpz_import");
+        export_ = (decltype(export_))dlsym(h, "__gmpz_export");
+        invert = (decltype(invert))dlsym(h, "__gmpz_invert");
+        ok = init && clear && import_ && export_ && invert;
+    }
+};
+const GmpApi &gmp() {
+    static GmpApi api;
+    return api;
+}
+} // namespace
+
+bool inv_mod_fast(const Big &x, const Big &M, Big &out) {
+    const GmpApi &g = gmp();
+    if (!g.ok) return inv_mod_odd(x, M, out);
+    GmpMpz a, m, r;
+    g.init(&a);
+    g.init(&m);
+    g.init(&r);
+    g.import_(&a, x.size(), -1, 4, 0, 0, x.data());
+    g.import_(&m, M.size(), -1, 4, 0, 0, M.data());
+    const int ok = g.invert(&r, &a, &m);
+    if (ok) {
+        out.assign(M.size() + 1, 0);
+        size_t cnt = 0;
+        g.export_(out.data(), &cnt, -1, 4, 0, 0, &r);
+        trim(out);
+    }
+    g.clear(&a);
+    g.clear(&m);
+    g.clear(&r);
+    return ok != 0;
+}
+} // namespace host
+} // namespace sfxb
 
 struct sfxb_ctx : CtxState {};
 struct sfxb_gh {
@@ -666,7 +724,7 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
             CK(cudaMemcpyAsync(root.data(), tr + lvl_off.back() * S4, S4 * 4, cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             host::Big plain = c->mh_n2->from_mont(host::from_words(root.data(), S4)), rinv;
-            if (!host::inv_mod_odd(plain, c->n2, rinv)) {
+            if (!host::inv_mod_fast(plain, c->n2, rinv)) {
                 derived_ok = false; // some slot is not a unit: build those nodes directly below
             } else {
                 host::Big rinv_m = host::pad(c->mh_n2->to_mont(rinv), S4);
