@@ -174,6 +174,22 @@ int sfxb_decrypt(sfxb_ctx *ctx, const uint32_t *cts, size_t count, uint32_t scal
                  double *out_values, uint32_t *out_plain, uint64_t *decryptions);
 int sfxb_decrypt_dev(sfxb_ctx *ctx, const uint32_t *d_cts, size_t count, uint32_t scale_bits,
                      double *d_out_values, uint32_t *d_out_plain, uint64_t *decryptions);
+/* Tree-level decrypt with verified sibling reuse (B200-side extension of
+ * decrypt_histogram, secure_processor.cpp:679-719; same outputs and counter).
+ * cts: n_nodes × slots_per_node ciphertexts of one histogram stream `tag`
+ * (node-major).  parent[i] (optional, −1 = none) indexes the nodes of the
+ * previous call with the same tag.  For two children a, b of one parent P the
+ * context checks, per slot, ct_a·ct_b ≡ ct_P (mod n²) on the GPU; where it
+ * holds, Dec(ct_b) = Dec(ct_P) − Dec(ct_a) mod n (Paillier is a group
+ * homomorphism Z*_{n²} → Z_n) replaces the CRT exponentiations.  Slots whose
+ * check fails are decrypted normally, so a wrong or hostile `parent` costs
+ * time, never correctness.  `decryptions` counts every non-trivial slot, as
+ * the reference does.  Each call becomes the cached parent level of `tag`. */
+int sfxb_decrypt_tree(sfxb_ctx *ctx, uint64_t tag, const uint32_t *cts, uint32_t n_nodes,
+                      uint32_t slots_per_node, const int32_t *parent, uint32_t scale_bits,
+                      double *out_values, uint64_t *decryptions);
+/* slots sfxb_decrypt_tree obtained by verified sibling reuse on this context */
+uint64_t sfxb_ctx_dec_derived(const sfxb_ctx *ctx);
 
 /* ---- stream / timing helpers (bench + tests) ---------------------------------- */
 void *sfxb_ctx_stream(sfxb_ctx *ctx); /* cudaStream_t of the context */
@@ -183,8 +199,10 @@ int sfxb_ctx_sync(sfxb_ctx *ctx);
  * exponentiation).  Enabling resets the accumulators. */
 int sfxb_ctx_profile(sfxb_ctx *ctx, int enable);
 int sfxb_ctx_kernel_time(sfxb_ctx *ctx, int family, uint64_t *launches, double *ms);
-/* as above plus the Montgomery multiplications those launches executed
- * (family 3: the sibling-subtraction batch inversion / derivation kernels) */
+/* as above plus the Montgomery multiplications those launches executed:
+ * families 0, 3 (3: sibling-subtraction batch inversion / derivation) count
+ * multiplications mod n²; families 1, 2 count multiplications mod p² (the
+ * CRT exponentiations; encrypt step 1 mod p counts 1/4). */
 int sfxb_ctx_kernel_stats(sfxb_ctx *ctx, int family, uint64_t *launches, double *ms, uint64_t *modmuls);
 /* integer-multiply peak microbenchmark: IMAD.WIDE.U32(.X) 32×32→64 products/s */
 int sfxb_imad_peak(int device, double *products_per_s, double *sm_clock_mhz);

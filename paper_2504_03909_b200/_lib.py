@@ -63,6 +63,7 @@ def load() -> C.CDLL:
         "sfxb_ctx_has_private": (C.c_int, [vp]),
         "sfxb_ctx_key_id": (C.c_uint64, [vp]),
         "sfxb_ctx_launches": (C.c_uint64, [vp]),
+        "sfxb_ctx_dec_derived": (C.c_uint64, [vp]),
         "sfxb_ctx_stream": (vp, [vp]),
         "sfxb_ctx_sync": (C.c_int, [vp]),
         "sfxb_encrypt": (C.c_int, [vp, _i64p, _u32p, sz, _u32p, vp]),
@@ -87,6 +88,8 @@ def load() -> C.CDLL:
         "sfxb_reduce_partials_dev": (C.c_int, [vp, vp, C.c_uint32, sz, vp]),
         "sfxb_decrypt": (C.c_int, [vp, _u32p, sz, C.c_uint32, _f64p, vp, C.POINTER(C.c_uint64)]),
         "sfxb_decrypt_dev": (C.c_int, [vp, vp, sz, C.c_uint32, vp, vp, C.POINTER(C.c_uint64)]),
+        "sfxb_decrypt_tree": (C.c_int, [vp, C.c_uint64, _u32p, C.c_uint32, C.c_uint32, vp, C.c_uint32, _f64p,
+                                        C.POINTER(C.c_uint64)]),
         "sfxb_imad_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "sfxb_ctx_profile": (C.c_int, [vp, C.c_int]),
         "sfxb_ctx_kernel_time": (C.c_int, [vp, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_double)]),
@@ -180,6 +183,11 @@ class Context:
     def launches(self) -> int:
         return self.lib.sfxb_ctx_launches(self.h)
 
+    @property
+    def dec_derived(self) -> int:
+        """Slots decrypt_tree derived by verified sibling reuse."""
+        return self.lib.sfxb_ctx_dec_derived(self.h)
+
     def encode_check(self, x: float, scale: int = 40) -> int:
         q = C.c_int64()
         self._check(self.lib.sfxb_encode_check(self.h, float(x), scale, C.byref(q)))
@@ -224,6 +232,23 @@ class Context:
         self._check(self.lib.sfxb_decrypt(self.h, cts.reshape(-1), count, scale, vals,
                                           plain.ctypes.data if want_plain else None, C.byref(decs)))
         return (vals, decs.value, plain) if want_plain else (vals, decs.value)
+
+    def decrypt_tree(self, tag: int, cts, n_nodes: int, parent=None, scale: int = 40):
+        """sfxb_decrypt_tree: one tree level of histogram stream `tag`
+        (n_nodes × slots_per_node ciphertexts), with verified sibling reuse
+        against the previous level of the same tag."""
+        cts = np.ascontiguousarray(cts, dtype=np.uint32)
+        count = cts.shape[0]
+        spn = count // n_nodes if n_nodes else 0
+        if n_nodes * spn != count:
+            raise ValueError("ciphertext count is not a multiple of n_nodes")
+        vals = np.zeros(count, np.float64)
+        par = None if parent is None else np.ascontiguousarray(parent, dtype=np.int32)
+        decs = C.c_uint64(0)
+        self._check(self.lib.sfxb_decrypt_tree(self.h, tag, cts.reshape(-1), n_nodes, spn,
+                                               None if par is None else par.ctypes.data, scale, vals,
+                                               C.byref(decs)))
+        return vals, decs.value
 
 
 class GhHandle:

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -79,6 +80,17 @@ struct CtxState {
     uint32_t tree_J = 0, tree_K = 0, tree_N = 0;
     uint64_t tree_derived_nodes = 0; // nodes obtained by sibling subtraction so far
     std::unique_ptr<host::MontHost> mh_n2;
+
+    // decrypt-side sibling reuse: previous level per histogram stream (tag)
+    struct DecCache {
+        Buf cts[2], plain[2]; // [cur] = previous level, [cur ^ 1] = this call
+        int cur = 0;
+        uint32_t n_nodes = 0, spn = 0;
+        bool valid = false;
+    };
+    std::map<uint64_t, DecCache> dec_cache;
+    uint64_t dec_derived = 0;         // slots decrypted by verified sibling reuse
+    uint64_t mm_dec = 0, mm_enc = 0; // per-item multiplications mod p² (CRT decrypt / encrypt)
 
     // scratch (grown on demand, freed with the context)
     Buf scratch_table, tmp[4], host_pinned[2], io[6]; // io: host-API staging (grow-only)

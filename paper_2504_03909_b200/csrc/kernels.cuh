@@ -267,6 +267,57 @@ __global__ void __launch_bounds__(kBlock) k_enc_combine(EncArgs a, int crt) {
 
 // ------------------------------------------------------------------ K3 decrypt (CRT)
 
+// decode_fixed (he.cpp:138-143) before the final ldexp: v = m − n if 2m > n,
+// converted like mpz_get_d (truncation toward zero).  word(k) = limb k of m.
+template <typename W>
+__device__ __forceinline__ double decode_words(int Sn, W word, const uint32_t *nw) {
+    // 2m > n  <=>  m > n >> 1 (n odd)
+    int cmpv = 0;
+    for (int k = Sn - 1; k >= 0 && cmpv == 0; --k) {
+        const uint32_t hn_k = (nw[k] >> 1) | (k + 1 < Sn ? (nw[k + 1] << 31) : 0u);
+        const uint32_t mk = word(k);
+        cmpv = mk > hn_k ? 1 : (mk < hn_k ? -1 : 0);
+    }
+    const bool neg = cmpv > 0;
+    // |v| = neg ? n − m : m, scanned from limb 0 keeping the highest
+    // nonzero limb and the two limbs below it.
+    uint32_t w_top = 0, w_1 = 0, w_2 = 0, prev1 = 0, prev2 = 0, bw = 0;
+    int topk = -1;
+    for (int k = 0; k < Sn; ++k) {
+        const uint32_t mk = word(k);
+        uint32_t vk = mk;
+        if (neg) {
+            const uint64_t diff = (uint64_t)nw[k] - mk - bw;
+            vk = (uint32_t)diff;
+            bw = (uint32_t)(diff >> 63);
+        }
+        if (vk != 0) {
+            topk = k;
+            w_top = vk;
+            w_1 = prev1;
+            w_2 = prev2;
+        }
+        prev2 = prev1;
+        prev1 = vk;
+    }
+    double val = 0.0;
+    if (topk >= 0) {
+        const int lz = __clz(w_top);
+        const int bits = topk * 32 + (32 - lz);
+        if (bits <= 64) {
+            const unsigned long long w64 =
+                topk == 0 ? (unsigned long long)w_top : ((unsigned long long)w_top << 32) | w_1;
+            val = __ull2double_rz(w64); // truncation == mpz_get_d
+        } else {
+            unsigned long long w64 = ((unsigned long long)w_top << 32) | w_1;
+            if (lz) w64 = (w64 << lz) | (w_2 >> (32 - lz));
+            val = ldexp(__ull2double_rz(w64), bits - 64);
+        }
+        if (neg) val = -val;
+    }
+    return val;
+}
+
 struct DecArgs {
     const uint32_t *cts;     // count × 4s
     size_t count;
@@ -289,6 +340,8 @@ struct DecArgs {
     uint32_t *status;        // bit1 = out of range, bit2 = not coprime
     uint32_t scale;
     uint32_t *scratch;
+    const uint8_t *skip;     // optional: 1 = plaintext derived elsewhere (sibling reuse)
+    uint32_t *n_skipped;     // non-trivial slots skipped (still counted as decryptions)
 };
 
 // Flag trivial slots (== 1 -> 0.0, uncounted), range-check the rest and
@@ -318,6 +371,10 @@ __global__ void k_dec_scan(DecArgs a) {
             }
         }
         if (zero || ge) atomicOr(a.status, 2u);
+        if (a.skip && a.skip[e]) {
+            atomicAdd(a.n_skipped, 1u);
+            continue;
+        }
         const uint32_t slot = atomicAdd(a.n_idx, 1u);
         a.idx[slot] = (uint32_t)e;
     }
@@ -412,51 +469,79 @@ __global__ void __launch_bounds__(kBlock) k_dec_combine(DecArgs a, uint32_t n_it
         // decode_fixed (he.cpp:138-143): v = m − n if 2m > n; mpz_get_d truncates.
         uint32_t tmp[Ln];
         relayout<Sn, Sn, TPI>(tmp, m, st);
-        // 2m > n  <=>  m > n >> 1 (n odd)
-        int cmpv = 0;
-        for (int k = Sn - 1; k >= 0 && cmpv == 0; --k) {
-            const uint32_t hn_k = (a.nw[k] >> 1) | (k + 1 < Sn ? (a.nw[k + 1] << 31) : 0u);
-            const uint32_t mk = staged_word<TPI>(st, k);
-            cmpv = mk > hn_k ? 1 : (mk < hn_k ? -1 : 0);
-        }
-        const bool neg = cmpv > 0;
-        // |v| = neg ? n − m : m, scanned from limb 0 keeping the highest
-        // nonzero limb and the two limbs below it.
-        uint32_t w_top = 0, w_1 = 0, w_2 = 0, prev1 = 0, prev2 = 0, bw = 0;
-        int topk = -1;
-        for (int k = 0; k < Sn; ++k) {
-            const uint32_t mk = staged_word<TPI>(st, k);
-            uint32_t vk = mk;
-            if (neg) {
-                const uint64_t diff = (uint64_t)a.nw[k] - mk - bw;
-                vk = (uint32_t)diff;
-                bw = (uint32_t)(diff >> 63);
-            }
-            if (vk != 0) {
-                topk = k;
-                w_top = vk;
-                w_1 = prev1;
-                w_2 = prev2;
-            }
-            prev2 = prev1;
-            prev1 = vk;
-        }
-        double val = 0.0;
-        if (topk >= 0) {
-            const int lz = __clz(w_top);
-            const int bits = topk * 32 + (32 - lz);
-            if (bits <= 64) {
-                const unsigned long long w64 =
-                    topk == 0 ? (unsigned long long)w_top : ((unsigned long long)w_top << 32) | w_1;
-                val = __ull2double_rz(w64); // truncation == mpz_get_d
-            } else {
-                unsigned long long w64 = ((unsigned long long)w_top << 32) | w_1;
-                if (lz) w64 = (w64 << lz) | (w_2 >> (32 - lz));
-                val = ldexp(__ull2double_rz(w64), bits - 64);
-            }
-            if (neg) val = -val;
-        }
+        const double val = decode_words(Sn, [&](int k) { return staged_word<TPI>(st, k); }, a.nw);
         if (active && inst_lane<TPI>() == 0) a.values[e] = ldexp(val, -(int)a.scale);
+    }
+}
+
+// ------------------------------------------------------------------ K3 sibling reuse
+
+// flag[j] = 1 when ct_a·ct_b ≡ ct_parent (mod n²) for derived slot j; then
+// m_b = m_parent − m_a (mod n) by the homomorphism and b need not be decrypted.
+struct SibArgs {
+    const uint32_t *cts;      // this call, node-major, n_nodes × spn × 4s
+    const uint32_t *prev_cts; // previous call (same tag)
+    const uint32_t *pairs;    // per derived node: (b, a, parent)
+    size_t n_pairs, spn;
+    uint8_t *skip;            // per slot of this call
+};
+
+template <int S, int TPI>
+__global__ void __launch_bounds__(kBlock) k_sib_verify(ModArg M, SibArgs a) {
+    constexpr int L = S / TPI, NI = kBlock / TPI;
+    __shared__ uint2 sB[S / 2 * NI];
+    const Stage st = make_stage<TPI>(sB);
+    const ModRef mr = M.ref();
+    uint32_t N[L], R2[L];
+    load_const<S, TPI>(N, mr, kMod);
+    load_const<S, TPI>(R2, mr, kR2);
+    SFXB_UNIFORM_LOOP(j, active, a.n_pairs * a.spn) {
+        const uint32_t *pr = a.pairs + 3 * (j / a.spn);
+        const size_t k = j % a.spn;
+        uint32_t x[L], y[L], z[L];
+        load_lane<S, TPI>(x, a.cts + ((size_t)pr[1] * a.spn + k) * S);
+        load_lane<S, TPI>(y, a.cts + ((size_t)pr[0] * a.spn + k) * S);
+        load_lane<S, TPI>(z, a.prev_cts + ((size_t)pr[2] * a.spn + k) * S);
+        // x·y mod n² = MontMul(MontMul(x, y), R²); x, y < n² (range-checked by the scan)
+        mmul<S, TPI>(x, x, y, st, N, M.np);
+        mmul<S, TPI>(x, R2, x, st, N, M.np);
+        bool eq = true;
+#pragma unroll
+        for (int w = 0; w < L; ++w) eq &= x[w] == z[w];
+        const bool all = inst_ballot<TPI>(!eq) == 0;
+        if (active && inst_lane<TPI>() == 0) a.skip[(size_t)pr[0] * a.spn + k] = all ? 1 : 0;
+    }
+}
+
+// m_b = (m_parent − m_a) mod n for the skipped slots, then decode_fixed.
+template <int Sn>
+__global__ void k_sib_derive(const uint32_t *pairs, size_t n_pairs, size_t spn, const uint8_t *skip,
+                             const uint32_t *plain, const uint32_t *prev_plain, const uint32_t *nw,
+                             uint32_t scale, uint32_t *plain_out, double *values) {
+    for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_pairs * spn;
+         j += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t *pr = pairs + 3 * (j / spn);
+        const size_t k = j % spn, eb = (size_t)pr[0] * spn + k;
+        if (!skip[eb]) continue;
+        const uint32_t *ma = plain + ((size_t)pr[1] * spn + k) * Sn;
+        const uint32_t *mp = prev_plain + ((size_t)pr[2] * spn + k) * Sn;
+        uint32_t m[Sn];
+        uint32_t br = 0;
+        for (int w = 0; w < Sn; ++w) {
+            const uint64_t d = (uint64_t)mp[w] - ma[w] - br;
+            m[w] = (uint32_t)d;
+            br = (uint32_t)(d >> 63);
+        }
+        if (br) { // add n back
+            uint32_t c = 0;
+            for (int w = 0; w < Sn; ++w) {
+                const uint64_t t = (uint64_t)m[w] + nw[w] + c;
+                m[w] = (uint32_t)t;
+                c = (uint32_t)(t >> 32);
+            }
+        }
+        for (int w = 0; w < Sn; ++w) plain_out[eb * Sn + w] = m[w];
+        values[eb] = ldexp(decode_words(Sn, [&](int w) { return m[w]; }, nw), -(int)scale);
     }
 }
 

@@ -155,6 +155,14 @@ uint8_t *dev_digits(CtxState &c, const Big &e, int w, int &nd) {
     nd = (int)d.size();
     return dev_upload(c, d.data(), d.size());
 }
+// Montgomery multiplications of mont_pow for exponent e at window w (modexp.cuh:206):
+// table build, w squarings per digit after the first, one multiply per non-zero digit
+uint64_t pow_mmuls(const Big &e, int w) {
+    std::vector<uint8_t> d = host::window_digits(e, w);
+    uint64_t m = (1u << w) - 2 + (uint64_t)(d.size() - 1) * w;
+    for (size_t i = 1; i < d.size(); ++i) m += d[i] != 0;
+    return m;
+}
 void *grow(Buf &b, size_t bytes) {
     if (b.bytes < bytes) {
         if (b.p) CK(cudaFree(b.p));
@@ -301,7 +309,7 @@ void encrypt_dev(sfxb_ctx *c, const int64_t *d_q, const uint32_t *d_r, size_t co
                 constexpr int NI = dev::kBlock / C::T1;
                 int grid = occupancy_grid(*c, k, 2 * count, NI, 2);
                 a.scratch = (uint32_t *)grow(c->scratch_table, 2 * (size_t)grid * NI * ((size_t)cs << kWindow) * 4);
-                ProfScope prof_(*c, 1);
+                ProfScope prof_(*c, 1, c->mm_enc * count);
                 k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(a);
                 check_launch(*c);
             }
@@ -339,7 +347,7 @@ void encrypt_dev(sfxb_ctx *c, const int64_t *d_q, const uint32_t *d_r, size_t co
 // --------------------------------------------------------------- decrypt
 
 void decrypt_dev(sfxb_ctx *c, const uint32_t *d_cts, size_t count, uint32_t scale, double *d_values,
-                 uint32_t *d_plain, uint64_t *decryptions) {
+                 uint32_t *d_plain, uint64_t *decryptions, const uint8_t *d_skip = nullptr) {
     if (!c->has_priv) throw ApiError(SFXB_ERR_AUTH, "decrypt requested without private key material");
     if (count == 0) return;
     if (count > 0xffffffffull) throw ApiError(SFXB_ERR_ARG, "decrypt: too many slots in one call");
@@ -351,7 +359,9 @@ void decrypt_dev(sfxb_ctx *c, const uint32_t *d_cts, size_t count, uint32_t scal
     uint32_t *misc = (uint32_t *)grow(c->tmp[3], 64);
     a.n_idx = misc + 1;
     a.status = misc;
-    CK(cudaMemsetAsync(misc, 0, 8, c->stream));
+    a.n_skipped = misc + 2;
+    a.skip = d_skip;
+    CK(cudaMemsetAsync(misc, 0, 12, c->stream));
     for (int i = 0; i < 2; ++i) {
         a.mod_pq[i] = arg(c->mod_pq[i]);
         a.mod_pq2[i] = arg(c->mod_pq2[i]);
@@ -377,19 +387,21 @@ void decrypt_dev(sfxb_ctx *c, const uint32_t *d_cts, size_t count, uint32_t scal
             dev::k_dec_scan<4 * cs><<<grid, 256, 0, c->stream>>>(a);
             check_launch(*c);
         }
-        uint32_t hst[2];
-        CK(cudaMemcpyAsync(hst, misc, 8, cudaMemcpyDeviceToHost, c->stream));
+        uint32_t hst[3];
+        CK(cudaMemcpyAsync(hst, misc, 12, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         if (hst[0] & 2u) throw ApiError(SFXB_ERR_RANGE, "decrypt: ciphertext out of range");
         const uint32_t n_items = hst[1];
-        if (decryptions) *decryptions += n_items;
+        // the reference's counter: every non-trivial slot (decrypted or derived)
+        if (decryptions) *decryptions += (uint64_t)n_items + hst[2];
+        c->dec_derived += hst[2];
         if (n_items == 0) return;
         {
             auto k = dev::k_dec_step<cs, C::TD, kWindow>;
             constexpr int NI = dev::kBlock / C::TD;
             int grid = occupancy_grid(*c, k, 2 * (size_t)n_items, NI, 2);
             a.scratch = (uint32_t *)grow(c->scratch_table, 2 * (size_t)grid * NI * ((size_t)(2 * cs) << kWindow) * 4);
-            ProfScope prof_(*c, 2);
+            ProfScope prof_(*c, 2, c->mm_dec * n_items);
             k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(a, n_items);
             check_launch(*c);
         }
@@ -913,6 +925,9 @@ int sfxb_ctx_create(sfxb_ctx **out, int device, const uint32_t *n, uint32_t n_wo
                 c->d_dig_e1[i] = dev_digits(*c, host::mod(ot, pm1), kWindow, c->nd_e1[i]);
                 c->d_dig_pq[i] = dev_digits(*c, pr, kWindow, c->nd_pq[i]);
                 c->d_dig_m1[i] = dev_digits(*c, pm1, kWindow, c->nd_m1[i]);
+                // profiling units: multiplications mod p² (step 1 runs mod p: 1/4 of the products)
+                c->mm_dec += pow_mmuls(pm1, kWindow);
+                c->mm_enc += pow_mmuls(host::mod(ot, pm1), kWindow) / 4 + pow_mmuls(pr, kWindow);
                 c->d_pinv[i] = dev_big(*c, host::inv_pow2(pr, s), s);
                 // h = (−other mod prime)^-1 mod prime, in Montgomery form
                 Big negot = host::sub(pr, host::mod(ot, pr));
@@ -955,6 +970,13 @@ void sfxb_ctx_destroy(sfxb_ctx *c) {
     if (c->spare_flags) cudaFree(c->spare_flags);
     for (auto &b : c->tmp)
         if (b.p) cudaFree(b.p);
+    for (auto &b : c->io)
+        if (b.p) cudaFree(b.p);
+    for (auto &kv : c->dec_cache)
+        for (int i = 0; i < 2; ++i) {
+            if (kv.second.cts[i].p) cudaFree(kv.second.cts[i].p);
+            if (kv.second.plain[i].p) cudaFree(kv.second.plain[i].p);
+        }
     for (auto &b : c->host_pinned)
         if (b.p) cudaFreeHost(b.p);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -967,6 +989,7 @@ uint32_t sfxb_ctx_ct_words(const sfxb_ctx *c) { return 2 * c->nw; }
 int sfxb_ctx_has_private(const sfxb_ctx *c) { return c->has_priv ? 1 : 0; }
 uint64_t sfxb_ctx_key_id(const sfxb_ctx *c) { return c->key_id; }
 uint64_t sfxb_ctx_launches(const sfxb_ctx *c) { return c->launches; }
+uint64_t sfxb_ctx_dec_derived(const sfxb_ctx *c) { return c->dec_derived; }
 void *sfxb_ctx_stream(sfxb_ctx *c) { return (void *)c->stream; }
 int sfxb_ctx_profile(sfxb_ctx *c, int enable) {
     return guard(c, [&] {
@@ -1093,6 +1116,72 @@ int sfxb_decrypt_dev(sfxb_ctx *c, const uint32_t *d_cts, size_t count, uint32_t 
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
         decrypt_dev(c, d_cts, count, scale, d_values, d_plain, decryptions);
+    });
+}
+
+int sfxb_decrypt_tree(sfxb_ctx *c, uint64_t tag, const uint32_t *cts, uint32_t n_nodes, uint32_t spn,
+                      const int32_t *parent, uint32_t scale, double *out_values, uint64_t *decryptions) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (!c->has_priv) throw ApiError(SFXB_ERR_AUTH, "decrypt requested without private key material");
+        const size_t count = (size_t)n_nodes * spn;
+        const size_t Sn = 2 * (size_t)c->s, S4 = 4 * (size_t)c->s;
+        CtxState::DecCache &prev = c->dec_cache[tag];
+        // sibling pairs (two children of one cached parent): b = second child
+        std::vector<uint32_t> pairs;
+        if (parent && prev.valid && prev.spn == spn) {
+            std::vector<std::vector<uint32_t>> kids(prev.n_nodes);
+            for (uint32_t i = 0; i < n_nodes; ++i)
+                if (parent[i] >= 0 && (uint32_t)parent[i] < prev.n_nodes) kids[parent[i]].push_back(i);
+            for (uint32_t pnode = 0; pnode < prev.n_nodes; ++pnode)
+                if (kids[pnode].size() == 2) {
+                    pairs.push_back(kids[pnode][1]);
+                    pairs.push_back(kids[pnode][0]);
+                    pairs.push_back(pnode);
+                }
+        }
+        const int nx = prev.cur ^ 1;
+        uint32_t *dc = (uint32_t *)grow(prev.cts[nx], count * S4 * 4 + 64);
+        uint32_t *dplain = (uint32_t *)grow(prev.plain[nx], count * Sn * 4 + 64);
+        IoBuf<double> dv(c->io[2], count ? count : 1);
+        if (count) h2d_padded(c, dc, cts, count, 2 * c->nw, S4);
+        uint8_t *skip = nullptr;
+        const size_t np = pairs.size() / 3;
+        uint32_t *dpairs = nullptr;
+        if (np) {
+            skip = (uint8_t *)grow(c->io[4], count + 64);
+            dpairs = (uint32_t *)grow(c->io[5], pairs.size() * 4 + 64);
+            CK(cudaMemsetAsync(skip, 0, count, c->stream));
+            CK(cudaMemcpyAsync(dpairs, pairs.data(), pairs.size() * 4, cudaMemcpyHostToDevice, c->stream));
+            dev::SibArgs sa{dc, (const uint32_t *)prev.cts[prev.cur].p, dpairs, np, spn, skip};
+            dispatch_class(c->s, [&](auto sc) {
+                constexpr int cs = decltype(sc)::value;
+                using C = Cls<cs>;
+                auto k = dev::k_sib_verify<4 * cs, C::TH>;
+                constexpr int NI = dev::kBlock / C::TH;
+                const int grid = occupancy_grid(*c, k, np * spn, NI);
+                k<<<grid, dev::kBlock, 0, c->stream>>>(arg(c->mod_n2), sa);
+                check_launch(*c);
+            });
+        }
+        if (count) decrypt_dev(c, dc, count, scale, dv.p, dplain, decryptions, skip);
+        if (np) {
+            dispatch_class(c->s, [&](auto sc) {
+                constexpr int cs = decltype(sc)::value;
+                const int grid = (int)std::min<size_t>((np * spn + 127) / 128, (size_t)c->sms * 8);
+                dev::k_sib_derive<2 * cs><<<grid, 128, 0, c->stream>>>(
+                    dpairs, np, spn, skip, dplain, (const uint32_t *)prev.plain[prev.cur].p, c->d_n, scale, dplain,
+                    dv.p);
+                check_launch(*c);
+            });
+        }
+        if (count) CK(cudaMemcpyAsync(out_values, dv.p, count * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        // this level becomes the parent level of the tag
+        prev.cur = nx;
+        prev.n_nodes = n_nodes;
+        prev.spn = spn;
+        prev.valid = true;
     });
 }
 

@@ -20,7 +20,9 @@
 #include <dlfcn.h>
 #include <gmp.h>
 
+#include <algorithm>
 #include <atomic>
+#include <map>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -109,6 +111,16 @@ using FactoryPub = std::unique_ptr<EncryptionPlugin> (*)(const PaillierPublicKey
 
 // ------------------------------------------------------------ the plugin
 
+// previous decrypted level of one histogram stream (one sender's tree)
+struct DecStream {
+    uint64_t tag = 0; // sfxb_decrypt_tree cache tag
+    std::vector<uint32_t> cts;
+    uint32_t n_nodes = 0;
+    size_t spn = 0;
+    uint64_t last_use = 0;
+};
+constexpr size_t kStreams = 8;
+
 class CudaPaillierPlugin final : public EncryptionPlugin {
 public:
     CudaPaillierPlugin(const PaillierPublicKey &pk, const PaillierPluginConfig &cfg)
@@ -123,11 +135,13 @@ public:
     }
     ~CudaPaillierPlugin() override {
         if (std::getenv("SFXB_PLUGIN_VERBOSE") && ctx_)
-            std::fprintf(stderr, "[sfxb-cuda-plugin] key=%016llx enc=%llu adds=%llu dec=%llu derived_nodes=%llu launches=%llu\n",
+            std::fprintf(stderr, "[sfxb-cuda-plugin] key=%016llx enc=%llu adds=%llu dec=%llu derived_nodes=%llu "
+                         "derived_slots=%llu launches=%llu\n",
                          (unsigned long long)pub_.key_id, (unsigned long long)counters_.encryptions,
                          (unsigned long long)counters_.ciphertext_additions,
                          (unsigned long long)counters_.decryptions,
-                         (unsigned long long)sfxb_ctx_tree_derived(ctx_), (unsigned long long)sfxb_ctx_launches(ctx_));
+                         (unsigned long long)sfxb_ctx_tree_derived(ctx_), (unsigned long long)sfxb_ctx_dec_derived(ctx_),
+                         (unsigned long long)sfxb_ctx_launches(ctx_));
         if (gh_) sfxb_gh_free(gh_);
         if (ctx_) sfxb_ctx_destroy(ctx_);
         gmp_randclear(rng_);
@@ -303,7 +317,7 @@ public:
         }
         std::vector<double> vals(total);
         uint64_t decs = 0;
-        if (total) check(sfxb_decrypt(ctx_, cts.data(), total, scale_bits_, vals.data(), nullptr, &decs));
+        if (total) decrypt_level(payload, cts, vals, &decs);
         counters_.decryptions += decs;
         base = 0;
         for (const NodeHistogram &node : payload.nodes) {
@@ -479,6 +493,89 @@ private:
         counters_ += r.counters() - before;
         return res;
     }
+    // One tree level of one sender's histograms: sibling nodes (ids k, k+1 with
+    // k odd, federation.cpp:331-345) whose parent is found in a previously
+    // decrypted level are decrypted by verified reuse (sfxb_decrypt_tree);
+    // everything else decrypts slot by slot as before.  Senders are not
+    // named in the payload, so up to kStreams previous levels are kept and a
+    // level continues the stream its first sibling pair matches.
+    bool find_parent(const DecStream &st, const NodeHistogram &a, const NodeHistogram &b, uint32_t from,
+                     uint32_t *out) {
+        mpz_class P, t;
+        for (uint32_t tries = 0; tries < st.n_nodes; ++tries) {
+            const uint32_t pc = (from + tries) % st.n_nodes;
+            const uint32_t *pw = &st.cts[(size_t)pc * st.spn * ct_words_];
+            size_t s = 0;
+            auto trivial = [&](size_t k) {
+                const uint32_t *w = pw + k * ct_words_;
+                return w[0] == 1 && std::all_of(w + 1, w + ct_words_, [](uint32_t x) { return x == 0; });
+            };
+            while (s < st.spn && trivial(s)) ++s;
+            if (s == st.spn) continue;
+            // one non-trivial slot selects the candidate; the GPU verifies every slot
+            mpz_import(P.get_mpz_t(), ct_words_, -1, 4, 0, 0, pw + s * ct_words_);
+            t = a.scalar_cts[s].value * b.scalar_cts[s].value;
+            mpz_mod(t.get_mpz_t(), t.get_mpz_t(), pub_.n2.get_mpz_t());
+            if (t == P) {
+                *out = pc;
+                return true;
+            }
+        }
+        return false;
+    }
+
+    void decrypt_level(const HistogramPayload &payload, std::vector<uint32_t> &cts, std::vector<double> &vals,
+                       uint64_t *decs) {
+        const auto &nodes = payload.nodes;
+        const size_t spn = 2 * nodes[0].feature_ids.size() * (size_t)std::max(nodes[0].n_bins, 0);
+        bool uniform = spn > 0;
+        for (const NodeHistogram &nd : nodes)
+            uniform &= nd.feature_ids == nodes[0].feature_ids && nd.n_bins == nodes[0].n_bins;
+        if (!uniform) {
+            check(sfxb_decrypt(ctx_, cts.data(), vals.size(), scale_bits_, vals.data(), nullptr, decs));
+            return;
+        }
+        std::vector<size_t> pairs; // index of the first node of each sibling pair
+        for (size_t i = 0; i + 1 < nodes.size(); ++i)
+            if ((nodes[i].node_id & 1u) && nodes[i + 1].node_id == nodes[i].node_id + 1) pairs.push_back(i++);
+        // the stream this level continues
+        DecStream *st = nullptr;
+        uint32_t first = 0;
+        if (!pairs.empty())
+            for (DecStream &c : dec_streams_)
+                if (c.spn == spn && c.n_nodes &&
+                    find_parent(c, nodes[pairs[0]], nodes[pairs[0] + 1], 0, &first)) {
+                    st = &c;
+                    break;
+                }
+        std::vector<int32_t> parent(nodes.size(), -1);
+        if (st) {
+            uint32_t cand = first;
+            for (size_t i : pairs) {
+                uint32_t pc;
+                if (find_parent(*st, nodes[i], nodes[i + 1], cand, &pc)) {
+                    parent[i] = parent[i + 1] = (int32_t)pc;
+                    cand = pc + 1;
+                }
+            }
+        } else {
+            if (dec_streams_.size() < kStreams) {
+                dec_streams_.emplace_back();
+                dec_streams_.back().tag = dec_streams_.size();
+                st = &dec_streams_.back();
+            } else {
+                st = &*std::min_element(dec_streams_.begin(), dec_streams_.end(),
+                                        [](const DecStream &x, const DecStream &y) { return x.last_use < y.last_use; });
+            }
+        }
+        check(sfxb_decrypt_tree(ctx_, st->tag, cts.data(), (uint32_t)nodes.size(), (uint32_t)spn, parent.data(),
+                                scale_bits_, vals.data(), decs));
+        st->cts.swap(cts);
+        st->n_nodes = (uint32_t)nodes.size();
+        st->spn = spn;
+        st->last_use = ++dec_clock_;
+    }
+
     std::vector<std::pair<std::uint32_t, Histogram>> delegate_decrypt(const HistogramPayload &p) {
         return delegated<std::vector<std::pair<std::uint32_t, Histogram>>>(
             [&](EncryptionPlugin &r) { return r.decrypt_histogram(p); });
@@ -502,6 +599,8 @@ private:
     uint64_t gh_hash_ = 0;
     size_t gh_count_ = 0;
     std::unique_ptr<EncryptionPlugin> ref_;
+    std::vector<DecStream> dec_streams_;
+    uint64_t dec_clock_ = 0;
 };
 
 } // namespace

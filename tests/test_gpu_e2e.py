@@ -48,6 +48,8 @@ def test_reference_training_loop_with_gpu_plugin(name):
     # every party's plugin was the GPU adapter, and sibling subtraction derived nodes
     assert len(stats) >= 2
     assert sum(int(s.split("derived_nodes=")[1].split()[0]) for s in stats) > 0
+    # and the active party decrypted sibling slots by verified reuse
+    assert sum(int(s.split("derived_slots=")[1].split()[0]) for s in stats) > 0
     assert got["forest"] == want["forest"]
     assert got["partials"] == want["partials"]
     assert got["counters"] == want["counters"]

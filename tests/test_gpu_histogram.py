@@ -183,3 +183,47 @@ def test_tree_mode_sibling_subtraction_is_bit_exact(kname, shape):
         ops.accumulate_tree(gh, d_bins, J, d_off, offs, len(nodes), d_rows, len(rows), K,
                             np.array(parents, np.int32), out)
         assert np.array_equal(out.cpu().numpy().view(np.uint32), want)
+
+
+@pytest.mark.parametrize("kname,shape", [("k512_c0ffee", (400, 3, 8, 4)), ("k2048_7", (300, 2, 16, 3))])
+def test_decrypt_tree_sibling_reuse_is_bit_exact(kname, shape):
+    """sfxb_decrypt_tree == plain decrypt (values bitwise, decryption counter)
+    level by level; sibling slots are derived (fewer CRT exponentiations), and
+    a wrong parent map or a foreign level still decrypts correctly (every
+    derivation is verified ct_a·ct_b ≡ ct_P mod n² first)."""
+    n_samples, J, K, depth = shape
+    n, p, q = key(kname)
+    ctx = _lib.Context(n, p, q)
+    rng = random.Random(kname + "dec")
+    cts = [rng.randrange(2, n * n) for _ in range(2 * n_samples)]
+    cts[3] = 1
+    cw = ints_to_words(cts, ctx.ct_words)
+    bins = np.array([[rng.randrange(K) for _ in range(n_samples)] for _ in range(J)], np.uint16)
+    levels = _random_tree(rng, n_samples, depth)
+    hists = []
+    for nodes, parents in levels:
+        offs, rows = frontier(nodes)
+        hists.append((ctx.accumulate(cw, bins, offs, rows, K)[0], len(nodes), np.array(parents, np.int32)))
+    work = {}
+    for mode in ("plain", "tree", "wrong_parents"):
+        ctx.profile(True)
+        for lvl, (h, nn, parents) in enumerate(hists):
+            want, want_decs = ctx.decrypt(h) if mode != "plain" else (None, None)
+            if mode == "plain":
+                ctx.decrypt(h)
+                continue
+            par = parents if mode == "tree" else np.array([(x + 1) % max(len(hists[lvl - 1][0]) // (J * K * 2), 1)
+                                                           if x >= 0 else -1 for x in parents], np.int32)
+            got, decs = ctx.decrypt_tree(11 if mode == "tree" else 12, h, nn, par)
+            assert np.array_equal(got.view(np.int64), want.view(np.int64)), (mode, lvl)
+            assert decs == want_decs
+        work[mode] = ctx.kernel_stats(2)[2]
+    # tree mode skipped sibling exponentiations (work includes the plain
+    # decrypts re-run for `want`); wrong parents fail verification below level 1
+    plain = work["plain"]
+    assert work["tree"] - plain < 0.9 * plain, work
+    assert work["wrong_parents"] > work["tree"], work
+    # an unrelated cached level (tag 11 holds the deepest level) is rejected slot by slot
+    h0, nn0, _ = hists[1]
+    got, _ = ctx.decrypt_tree(11, h0, nn0, np.zeros(nn0, np.int32))
+    assert np.array_equal(got.view(np.int64), ctx.decrypt(h0)[0].view(np.int64))
