@@ -1,0 +1,38 @@
+"""enc/s and dec/s (exponentiation kernels, CUDA events) at one batch size
+(development tool; SFXB_LIB selects a library variant)."""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+sys.path.insert(0, "tests")
+from keys import key  # noqa: E402
+from paper_2504_03909_b200 import _lib  # noqa: E402
+
+kname = sys.argv[1] if len(sys.argv) > 1 else "k2048_7"
+count = int(sys.argv[2]) if len(sys.argv) > 2 else 262144
+n, p, q = key(kname)
+dev = torch.device("cuda:0")
+ctx = _lib.Context(n, p, q)
+ops = _lib.DeviceOps(ctx)
+g = torch.Generator(device=dev).manual_seed(1)
+qf = torch.randint(-(1 << 40), 1 << 40, (count,), dtype=torch.int64, device=dev, generator=g)
+r = torch.randint(-(2**31), 2**31 - 1, (count, ctx.nw), dtype=torch.int32, device=dev, generator=g)
+r[:, -1] &= 0x3FFFFFFF
+cts = torch.empty((count, ctx.ct_words), dtype=torch.int32, device=dev)
+vals = torch.empty(count, dtype=torch.float64, device=dev)
+ops.encrypt(qf, r, count, cts)
+ops.decrypt(cts, count, vals)
+res = {}
+for name, fam, fn in (("enc", 1, lambda: ops.encrypt(qf, r, count, cts)),
+                      ("dec", 2, lambda: ops.decrypt(cts, count, vals))):
+    best = 0
+    for _ in range(3):
+        ctx.profile(True)
+        fn()
+        nl, ms, mm = ctx.kernel_stats(fam)
+        ctx.profile(False)
+        best = max(best, count / (ms / 1e3))
+    res[name] = best
+print(os.environ.get("SFXB_LIB", "default"), kname, count, {k: round(v) for k, v in res.items()}, flush=True)
