@@ -75,6 +75,9 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=40000, help="single-core cpu_baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tree", action="store_true", help="disable sibling subtraction (direct histograms)")
+    ap.add_argument("--check", action="store_true",
+                    help="N>1: rank 0 recomputes every level's histograms from all rows on one GPU and compares "
+                         "them with the row-sharded result (bit-exact)")
     return ap.parse_args()
 
 
@@ -267,6 +270,41 @@ def run_reference(a):
 # ------------------------------------------------------------------ our arm
 
 
+def check_sharded(a, ops, ctxs, h_out, fronts_full, bins_pp, world, dev, cw):
+    """Rank 0: rebuild every rank's gradient shard (same generators), histogram
+    all rows on this GPU level by level (direct products) and compare with the
+    row-sharded, exchanged and K4-reduced result of the e2e pass."""
+    import torch
+
+    from paper_2504_03909_b200 import dist as pdist
+
+    shards = []
+    for r in range(world):
+        lo, hi = pdist.row_shard(a.rows, world, r)
+        g = torch.Generator(device=dev).manual_seed(1000 + r)
+        x = torch.randint(-(2**31), 2**31 - 1, (2 * (hi - lo), cw), dtype=torch.int32, device=dev, generator=g)
+        x[:, -1] &= 0x3FFFFFFF
+        shards.append(x)
+    full = torch.cat(shards, 0)
+    slots = 0
+    for pi in range(a.parties):
+        gh = ops[pi].gh_from_dev(full, a.rows)
+        d_bins = torch.from_numpy(bins_pp[pi].astype(np.int16)).to(dev)
+        for d, (offs, rows) in enumerate(fronts_full):
+            N = len(offs) - 1
+            out = torch.empty((N * a.feats * a.bins * 2, cw), dtype=torch.int32, device=dev)
+            ops[pi].accumulate(gh, d_bins, a.feats, torch.from_numpy(offs.astype(np.int32)).to(dev), N,
+                               torch.from_numpy(rows.astype(np.int32)).to(dev), len(rows), a.bins, out)
+            want = out.cpu().numpy().view(np.uint32)
+            if not np.array_equal(want, h_out[pi][d]):
+                bad = int((want != h_out[pi][d]).any(axis=1).sum())
+                raise SystemExit(f"--check: party {pi} level {d}: {bad} slots differ from the one-GPU histogram")
+            slots += want.shape[0]
+        gh.free()
+    return {"ok": True, "slots_compared": slots,
+            "against": "direct one-GPU histogram of all rows, bit-exact"}
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
@@ -278,10 +316,19 @@ def run_ours(a):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test knobs: SFXB_DIST_BACKEND=gloo + SFXB_BENCH_SAME_GPU=1 run the N>1
+    # data path (sharding, exchange, K4 reduce) with several ranks on one GPU,
+    # exchanging through host memory — a logic check, not a performance run
+    if os.environ.get("SFXB_BENCH_SAME_GPU"):
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("SFXB_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     peak, peak_clk = _lib.imad_peak(local)
     n, p, q = key(a.key)
@@ -457,6 +504,9 @@ def run_ours(a):
         else:
             e2e_phase.clear()
     e2e = torch.tensor([statistics.median(e2e_times)], dtype=torch.float64, device=dev)
+    check = None
+    if a.check and world > 1 and rank == 0:
+        check = check_sharded(a, ops, ctxs, h_out, fronts_full, bins_pp, world, dev, cw)
     if world > 1:
         dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
 
@@ -569,6 +619,7 @@ def run_ours(a):
                              "frac": k3[2] * PRODUCTS_P2 / (k3[1] / 1e3) / peak if k3[1] else None,
                              "kernel": "k_dec_step (CRT c^(p-1) mod p^2, q^2)"},
         "decrypt_tree": dec_tree,
+        "check": check,
         "clocks": clk.summary(),
     }
     if world == 1 and not a.no_cpu:

@@ -44,6 +44,12 @@ def exchange(partial: torch.Tensor, world: int, group=None) -> torch.Tensor:
     recv = torch.empty_like(partial)
     if world == 1:
         recv.copy_(partial)
+    elif partial.is_cuda and dist.get_backend(group) == "gloo":
+        # host-staged path (gloo has no CUDA all_to_all): used by the
+        # several-ranks-on-one-GPU logic check only
+        host = torch.empty(partial.shape, dtype=partial.dtype)
+        dist.all_to_all_single(host, partial.cpu().contiguous(), group=group)
+        recv.copy_(host)
     else:
         dist.all_to_all_single(recv, partial.contiguous(), group=group)
     return recv.view(world, partial.shape[0] // world, partial.shape[1])
@@ -63,6 +69,10 @@ def gather_slices(local: torch.Tensor, n_slots: int, world: int, group=None) -> 
     (what the active party collects)."""
     if world == 1:
         return local[:n_slots]
+    if local.is_cuda and dist.get_backend(group) == "gloo":
+        parts = [torch.empty(local.shape, dtype=local.dtype) for _ in range(world)]
+        dist.all_gather(parts, local.cpu().contiguous(), group=group)
+        return torch.cat(parts, 0)[:n_slots].to(local.device)
     parts = [torch.empty_like(local) for _ in range(world)]
     dist.all_gather(parts, local.contiguous(), group=group)
     return torch.cat(parts, 0)[:n_slots]
