@@ -80,6 +80,12 @@ uint64_t sfxb_ctx_launches(const sfxb_ctx *ctx);
  * caller can re-draw per the reference's rejection rule, he.cpp:19-28). */
 int sfxb_encrypt(sfxb_ctx *ctx, const int64_t *q_fixed, const uint32_t *r, size_t count,
                  uint32_t *out_cts, uint8_t *r_flags);
+/* encrypt_with_r for arbitrary plaintexts m ∈ [0, n) given as count × n_words
+ * little-endian words (the packed-vector path: pack_encrypt, he.cpp:220-232,
+ * plaintexts from pack_plain).  Same r semantics, flags and errors as
+ * sfxb_encrypt, plus "encrypt: plaintext out of range [0, n)" (he.cpp:88). */
+int sfxb_encrypt_plain(sfxb_ctx *ctx, const uint32_t *m_words, const uint32_t *r_words, size_t count,
+                       uint32_t *out_cts, uint8_t *r_flags);
 int sfxb_encrypt_dev(sfxb_ctx *ctx, const int64_t *d_q_fixed, const uint32_t *d_r, size_t count,
                      uint32_t *d_out_cts, uint8_t *d_r_flags);
 

@@ -218,7 +218,10 @@ class Reference:
     def __init__(self):
         if not reference_available():
             raise RefError("oracle/_ref not built (run `make -C oracle ref` in the dev container)")
-        lib = C.CDLL(REF_CAPI_SO)
+        # global symbol scope, as for a program linked against the reference:
+        # an interposed plugin (LD_PRELOAD) calls back into the reference's
+        # public helpers (e.g. pack_plain, he.hpp)
+        lib = C.CDLL(REF_CAPI_SO, mode=C.RTLD_GLOBAL)
         self.lib = lib
         lib.ref_last_error.restype = C.c_char_p
         lib.ref_keygen.argtypes = [C.c_uint, C.c_uint64, _u32p, _u32p, _u32p, C.c_size_t]

@@ -68,6 +68,7 @@ def load() -> C.CDLL:
         "sfxb_ctx_sync": (C.c_int, [vp]),
         "sfxb_encrypt": (C.c_int, [vp, _i64p, _u32p, sz, _u32p, vp]),
         "sfxb_encrypt_dev": (C.c_int, [vp, vp, vp, sz, vp, vp]),
+        "sfxb_encrypt_plain": (C.c_int, [vp, _u32p, _u32p, sz, _u32p, vp]),
         "sfxb_encode_check": (C.c_int, [vp, C.c_double, C.c_uint32, C.POINTER(C.c_int64)]),
         "sfxb_add": (C.c_int, [vp, _u32p, _u32p, sz, _u32p]),
         "sfxb_accumulate": (C.c_int, [vp, _u32p, C.c_uint32, _u16p, C.c_uint32, _u32p, C.c_uint32, _u32p,
@@ -187,6 +188,16 @@ class Context:
     def dec_derived(self) -> int:
         """Slots decrypt_tree derived by verified sibling reuse."""
         return self.lib.sfxb_ctx_dec_derived(self.h)
+
+    def encrypt_plain(self, m_words, r_words):
+        """Encrypt plaintexts m ∈ [0, n) given as words (packed vectors)."""
+        m_words = np.ascontiguousarray(m_words, dtype=np.uint32)
+        r_words = np.ascontiguousarray(r_words, dtype=np.uint32)
+        count = m_words.shape[0]
+        out = np.zeros((count, self.ct_words), np.uint32)
+        self._check(self.lib.sfxb_encrypt_plain(self.h, m_words.reshape(-1), r_words.reshape(-1), count,
+                                                out.reshape(-1), None))
+        return out
 
     def encode_check(self, x: float, scale: int = 40) -> int:
         q = C.c_int64()

@@ -108,7 +108,8 @@ __global__ void __launch_bounds__(kBlock) k_mulmod(ModArg M, const uint32_t *a, 
 
 struct EncArgs {
     const uint32_t *r;      // count × 2s
-    const int64_t *qfix;    // count
+    const int64_t *qfix;    // count (fixed-point plaintexts), or null when mw is set
+    const uint32_t *mw;     // count × 2s plaintext words m < n (packed vectors), or null
     size_t count;
     ModArg mod_pq[2];       // S = s
     ModArg mod_pq2[2];      // S = 2s
@@ -239,20 +240,28 @@ __global__ void __launch_bounds__(kBlock) k_enc_combine(EncArgs a, int crt) {
         } else {
             load_lane<S4, TPI>(Y, a.y + e * S4);
         }
-        // m = q mod n: q >= 0 -> q ; q < 0 -> n − |q|
-        const int64_t qv = a.qfix[e];
-        const uint64_t mag = qv < 0 ? (uint64_t)(-(qv + 1)) + 1u : (uint64_t)qv;
-        uint32_t mq[L4];
-        set_small<L4, TPI>(mq, 0u);
-        if (inst_lane<TPI>() == 0) {
-            mq[0] = (uint32_t)mag;
-            mq[1] = (uint32_t)(mag >> 32);
-        }
-        uint32_t m[L4], n4[L4];
-        load_lane<S4, TPI>(n4, a.n4);
-        sub_full<S4, TPI>(m, n4, mq); // warp-uniform; selected below
+        uint32_t m[L4];
+        if (a.mw) {
+            // plaintext given as words (packed vectors, he.cpp:220-225)
+            uint32_t m2[L2];
+            load_lane<S2, TPI>(m2, a.mw + e * S2);
+            relayout<S2, S4, TPI>(m, m2, st);
+        } else {
+            // m = q mod n: q >= 0 -> q ; q < 0 -> n − |q|
+            const int64_t qv = a.qfix[e];
+            const uint64_t mag = qv < 0 ? (uint64_t)(-(qv + 1)) + 1u : (uint64_t)qv;
+            uint32_t mq[L4];
+            set_small<L4, TPI>(mq, 0u);
+            if (inst_lane<TPI>() == 0) {
+                mq[0] = (uint32_t)mag;
+                mq[1] = (uint32_t)(mag >> 32);
+            }
+            uint32_t n4[L4];
+            load_lane<S4, TPI>(n4, a.n4);
+            sub_full<S4, TPI>(m, n4, mq); // warp-uniform; selected below
 #pragma unroll
-        for (int k = 0; k < L4; ++k) m[k] = qv < 0 ? m[k] : mq[k];
+            for (int k = 0; k < L4; ++k) m[k] = qv < 0 ? m[k] : mq[k];
+        }
         load_lane<S4, TPI>(C4, a.nR_n2);
         mmul<S4, TPI>(t4, C4, m, st, N4, M4.np); // m·n (< n², exact)
         uint32_t one[L4];

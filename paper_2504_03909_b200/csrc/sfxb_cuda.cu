@@ -266,13 +266,14 @@ struct ProfScope {
 // --------------------------------------------------------------- encrypt
 
 void encrypt_dev(sfxb_ctx *c, const int64_t *d_q, const uint32_t *d_r, size_t count,
-                 uint32_t *d_out, uint8_t *d_flags) {
+                 uint32_t *d_out, uint8_t *d_flags, const uint32_t *d_m = nullptr) {
     if (count == 0) return;
     const int s = c->s;
     const size_t S2 = 2 * (size_t)s, S4 = 4 * (size_t)s;
     dev::EncArgs a{};
     a.r = d_r;
     a.qfix = d_q;
+    a.mw = d_m;
     a.count = count;
     a.mod_n2 = arg(c->mod_n2);
     a.dig_n = c->d_dig_n;
@@ -1056,42 +1057,57 @@ int sfxb_encrypt_dev(sfxb_ctx *c, const int64_t *d_q, const uint32_t *d_r, size_
     });
 }
 
+namespace {
+// sfxb_encrypt / sfxb_encrypt_plain: q_fixed xor m_words (count × n_words)
+void encrypt_host(sfxb_ctx *c, const int64_t *q_fixed, const uint32_t *m_words, const uint32_t *r, size_t count,
+                  uint32_t *out_cts, uint8_t *r_flags) {
+    CK(cudaSetDevice(c->device));
+    if (count == 0) return;
+    const size_t Sn = 2 * (size_t)c->s, S4 = 4 * (size_t)c->s;
+    // range checks of encrypt_with_r (he.cpp:88-89), in its order per element
+    for (size_t i = 0; i < count; ++i) {
+        if (m_words && host::cmp(host::from_words(m_words + i * c->nw, c->nw), c->n) >= 0)
+            throw ApiError(SFXB_ERR_RANGE, "encrypt: plaintext out of range [0, n)");
+        const uint32_t *ri = r + i * c->nw;
+        bool small = true;
+        for (uint32_t k = 1; k < c->nw; ++k) small &= ri[k] == 0;
+        if (small && ri[0] < 1) throw ApiError(SFXB_ERR_RANGE, "encrypt: blinding factor out of range");
+        if (host::cmp(host::from_words(ri, c->nw), c->n) >= 0)
+            throw ApiError(SFXB_ERR_RANGE, "encrypt: blinding factor out of range");
+    }
+    IoBuf<int64_t> dq(c->io[0], m_words ? 1 : count);
+    IoBuf<uint32_t> dr(c->io[1], count * Sn), dout(c->io[2], count * S4);
+    IoBuf<uint8_t> dflags(c->io[3], count);
+    IoBuf<uint32_t> dm(c->io[4], m_words ? count * Sn : 1);
+    CK(cudaMemsetAsync(dflags.p, 0, count, c->stream));
+    if (m_words) h2d_padded(c, dm.p, m_words, count, c->nw, Sn);
+    else CK(cudaMemcpyAsync(dq.p, q_fixed, count * 8, cudaMemcpyHostToDevice, c->stream));
+    h2d_padded(c, dr.p, r, count, c->nw, Sn);
+    int st = SFXB_OK;
+    try {
+        encrypt_dev(c, m_words ? nullptr : dq.p, dr.p, count, dout.p, dflags.p, m_words ? dm.p : nullptr);
+    } catch (const ApiError &e) {
+        if (e.code != SFXB_ERR_COPRIME) throw;
+        st = e.code;
+        c->err = e.what();
+    }
+    if (r_flags) {
+        CK(cudaMemcpyAsync(r_flags, dflags.p, count, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    if (st != SFXB_OK) throw ApiError(st, c->err);
+    d2h_padded(c, out_cts, dout.p, count, 2 * c->nw, S4);
+}
+} // namespace
+
 int sfxb_encrypt(sfxb_ctx *c, const int64_t *q_fixed, const uint32_t *r, size_t count, uint32_t *out_cts,
                  uint8_t *r_flags) {
-    return guard(c, [&] {
-        CK(cudaSetDevice(c->device));
-        if (count == 0) return;
-        const size_t Sn = 2 * (size_t)c->s, S4 = 4 * (size_t)c->s;
-        // range checks of encrypt_with_r (he.cpp:88-89) on the blinding factors
-        for (size_t i = 0; i < count; ++i) {
-            const uint32_t *ri = r + i * c->nw;
-            bool small = true;
-            for (uint32_t k = 1; k < c->nw; ++k) small &= ri[k] == 0;
-            if (small && ri[0] < 1) throw ApiError(SFXB_ERR_RANGE, "encrypt: blinding factor out of range");
-            if (host::cmp(host::from_words(ri, c->nw), c->n) >= 0)
-                throw ApiError(SFXB_ERR_RANGE, "encrypt: blinding factor out of range");
-        }
-        IoBuf<int64_t> dq(c->io[0], count);
-        IoBuf<uint32_t> dr(c->io[1], count * Sn), dout(c->io[2], count * S4);
-        IoBuf<uint8_t> dflags(c->io[3], count);
-        CK(cudaMemsetAsync(dflags.p, 0, count, c->stream));
-        CK(cudaMemcpyAsync(dq.p, q_fixed, count * 8, cudaMemcpyHostToDevice, c->stream));
-        h2d_padded(c, dr.p, r, count, c->nw, Sn);
-        int st = SFXB_OK;
-        try {
-            encrypt_dev(c, dq.p, dr.p, count, dout.p, dflags.p);
-        } catch (const ApiError &e) {
-            if (e.code != SFXB_ERR_COPRIME) throw;
-            st = e.code;
-            c->err = e.what();
-        }
-        if (r_flags) {
-            CK(cudaMemcpyAsync(r_flags, dflags.p, count, cudaMemcpyDeviceToHost, c->stream));
-            CK(cudaStreamSynchronize(c->stream));
-        }
-        if (st != SFXB_OK) throw ApiError(st, c->err);
-        d2h_padded(c, out_cts, dout.p, count, 2 * c->nw, S4);
-    });
+    return guard(c, [&] { encrypt_host(c, q_fixed, nullptr, r, count, out_cts, r_flags); });
+}
+
+int sfxb_encrypt_plain(sfxb_ctx *c, const uint32_t *m_words, const uint32_t *r, size_t count, uint32_t *out_cts,
+                       uint8_t *r_flags) {
+    return guard(c, [&] { encrypt_host(c, nullptr, m_words, r, count, out_cts, r_flags); });
 }
 
 int sfxb_add(sfxb_ctx *c, const uint32_t *a, const uint32_t *b, size_t count, uint32_t *out) {

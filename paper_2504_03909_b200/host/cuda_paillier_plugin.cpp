@@ -14,10 +14,11 @@
 //     advance exactly as the reference would, including on failure;
 //   * accumulate_rows / decrypt_histogram keep the reference's validation
 //     order, messages, slot layout, trivial-zero handling and counter laws;
-//   * the packed (horizontal) vector path is outside the GPU scope and is
-//     delegated to the reference implementation (dlsym RTLD_NEXT), with its
-//     counter deltas folded into ours.
-#include <dlfcn.h>
+//   * the packed (horizontal) vector path (encrypt_histogram, add_histograms,
+//     packed decrypt) uses the reference's packing layer (pack_plain /
+//     unpack_plain, he.hpp) on the host and the GPU for every encryption,
+//     ciphertext product and decryption, with the reference's r order, checks,
+//     error order and vector-granularity counters.
 #include <gmp.h>
 
 #include <algorithm>
@@ -106,8 +107,6 @@ void from_words(mpz_class &z, const uint32_t *w, size_t words) {
 }
 
 // the reference implementation, for the out-of-scope packed path
-using Factory = std::unique_ptr<EncryptionPlugin> (*)(const PaillierKeypair &, const PaillierPluginConfig &);
-using FactoryPub = std::unique_ptr<EncryptionPlugin> (*)(const PaillierPublicKey &, const PaillierPluginConfig &);
 
 // ------------------------------------------------------------ the plugin
 
@@ -121,15 +120,24 @@ struct DecStream {
 };
 constexpr size_t kStreams = 8;
 
+// PaillierPlugin's packed layout (secure_processor.cpp:553-558)
+PackedLayout packed_layout(const PaillierPublicKey &pk, const PaillierPluginConfig &cfg) {
+    PackedLayout l = cfg.packed;
+    l.modulus_bits = pk.modulus_bits;
+    l.scale_bits = cfg.scale_bits;
+    return l;
+}
+
 class CudaPaillierPlugin final : public EncryptionPlugin {
 public:
     CudaPaillierPlugin(const PaillierPublicKey &pk, const PaillierPluginConfig &cfg)
-        : pub_(pk), has_priv_(false), cfg_(cfg), scale_bits_(cfg.scale_bits) {
+        : pub_(pk), has_priv_(false), scale_bits_(cfg.scale_bits), layout_(packed_layout(pk, cfg)) {
         init_rng(cfg.rng_seed);
         open_ctx(nullptr);
     }
     CudaPaillierPlugin(const PaillierKeypair &kp, const PaillierPluginConfig &cfg)
-        : pub_(kp.pub), priv_(kp.priv), has_priv_(true), kp_(kp), cfg_(cfg), scale_bits_(cfg.scale_bits) {
+        : pub_(kp.pub), priv_(kp.priv), has_priv_(true), scale_bits_(cfg.scale_bits),
+          layout_(packed_layout(kp.pub, cfg)) {
         init_rng(cfg.rng_seed);
         open_ctx(&kp);
     }
@@ -287,7 +295,7 @@ public:
     std::vector<std::pair<std::uint32_t, Histogram>> decrypt_histogram(const HistogramPayload &payload) override {
         if (!has_priv_) throw AuthorizationError("decrypt requested without private key material");
         if (payload.layout != HistLayout::enc_scalar) {
-            if (payload.layout == HistLayout::enc_packed) return delegate_decrypt(payload);
+            if (payload.layout == HistLayout::enc_packed) return decrypt_packed(payload);
             throw Error("paillier decrypt expects encrypted layouts");
         }
         std::vector<std::pair<std::uint32_t, Histogram>> out;
@@ -336,12 +344,131 @@ public:
         return out;
     }
 
-    // ---- packed (horizontal) path: the reference implementation
-    HistogramPayload encrypt_histogram(const std::vector<std::pair<std::uint32_t, Histogram>> &h) override {
-        return delegated<HistogramPayload>([&](EncryptionPlugin &p) { return p.encrypt_histogram(h); });
+    // ---- packed (horizontal) path: encrypt_histogram (secure_processor.cpp:622-645)
+    // = pack_plain (the reference's packing layer, he.cpp:166-193) + one GPU
+    // batch of encrypt_with_r over every packed plaintext, r drawn in the
+    // reference's order (node: G vector, then H vector).
+    HistogramPayload encrypt_histogram(const std::vector<std::pair<std::uint32_t, Histogram>> &node_hists) override {
+        layout_.validate();
+        HistogramPayload out;
+        out.layout = HistLayout::enc_packed;
+        std::vector<mpz_class> plains;
+        std::vector<size_t> first(1, 0);
+        std::vector<std::uint32_t> lengths;
+        size_t done_nodes = 0;
+        try {
+            for (const auto &[node_id, hist] : node_hists) {
+                std::vector<double> gs, hs;
+                gs.reserve(hist.feats.size() * hist.n_bins);
+                hs.reserve(hist.feats.size() * hist.n_bins);
+                for (const auto &slots : hist.feats)
+                    for (const GHPair &b : slots) {
+                        gs.push_back(b.g);
+                        hs.push_back(b.h);
+                    }
+                for (const std::vector<double> *v : {&gs, &hs}) {
+                    std::vector<mpz_class> p = pack_plain(layout_, *v);
+                    for (mpz_class &m : p) plains.push_back(std::move(m));
+                    first.push_back(plains.size());
+                    lengths.push_back(static_cast<std::uint32_t>(v->size()));
+                }
+                ++done_nodes;
+            }
+        } catch (...) {
+            // the reference encrypted (drew r for) every vector packed before the failure
+            std::vector<uint32_t> r(plains.size() * n_words_);
+            draw_blinding(r.data(), plains.size());
+            counters_.encryptions += 2 * done_nodes;
+            throw;
+        }
+        const size_t count = plains.size();
+        std::vector<uint32_t> m(count * n_words_), r(count * n_words_), cts(count * ct_words_);
+        for (size_t i = 0; i < count; ++i) to_words(plains[i], &m[i * n_words_], n_words_);
+        draw_blinding(r.data(), count);
+        if (count) {
+            int rc = sfxb_encrypt_plain(ctx_, m.data(), r.data(), count, cts.data(), nullptr);
+            if (rc == SFXB_ERR_COPRIME) {
+                gmp_randclear(rng_);
+                gmp_randinit_set(rng_, rng_snapshot_);
+                draw_blinding(r.data(), count, /*exact_gcd=*/true);
+                rc = sfxb_encrypt_plain(ctx_, m.data(), r.data(), count, cts.data(), nullptr);
+            }
+            check(rc);
+        }
+        size_t v = 0;
+        for (const auto &[node_id, hist] : node_hists) {
+            NodeHistogram nh;
+            nh.node_id = node_id;
+            nh.feature_ids = hist.feature_ids;
+            nh.n_bins = hist.n_bins;
+            for (PackedVector *pv : {&nh.packed_g, &nh.packed_h}) {
+                pv->logical_length = lengths[v];
+                pv->addend_count = 1;
+                pv->slot_bits = layout_.slot_bits;
+                pv->guard_bits = layout_.guard_bits;
+                pv->scale_bits = layout_.scale_bits;
+                pv->cts.resize(first[v + 1] - first[v]);
+                for (size_t k = 0; k < pv->cts.size(); ++k) {
+                    from_words(pv->cts[k].value, &cts[(first[v] + k) * ct_words_], ct_words_);
+                    pv->cts[k].key_id = pub_.key_id;
+                }
+                ++v;
+            }
+            counters_.encryptions += 2; // vector granularity
+            out.nodes.push_back(std::move(nh));
+        }
+        return out;
     }
+
+    // ---- add_histograms (secure_processor.cpp:647-676): validation, fold
+    // rules and counters in the reference's order; the ciphertext products of
+    // each part run as one GPU batch (sfxb_add).
     HistogramPayload add_histograms(const std::vector<HistogramPayload> &parts) override {
-        return delegated<HistogramPayload>([&](EncryptionPlugin &p) { return p.add_histograms(parts); });
+        if (parts.empty()) throw Error("add_histograms: no inputs");
+        HistogramPayload acc = parts[0];
+        for (std::size_t p = 1; p < parts.size(); ++p) {
+            const HistogramPayload &cur = parts[p];
+            if (cur.layout != acc.layout || cur.nodes.size() != acc.nodes.size())
+                throw Error("add_histograms: shape mismatch");
+            std::vector<std::pair<Ciphertext *, const Ciphertext *>> work; // lhs ⊗= rhs
+            uint64_t adds = 0;
+            try {
+                for (std::size_t i = 0; i < acc.nodes.size(); ++i) {
+                    NodeHistogram &a = acc.nodes[i];
+                    const NodeHistogram &b = cur.nodes[i];
+                    if (a.node_id != b.node_id || a.feature_ids != b.feature_ids || a.n_bins != b.n_bins)
+                        throw Error("add_histograms: shape mismatch");
+                    if (acc.layout == HistLayout::enc_packed) {
+                        plan_add_packed(a.packed_g, b.packed_g, work);
+                        plan_add_packed(a.packed_h, b.packed_h, work);
+                        adds += 2; // vector granularity
+                    } else if (acc.layout == HistLayout::enc_scalar) {
+                        if (a.scalar_cts.size() != b.scalar_cts.size()) throw Error("add_histograms: shape mismatch");
+                        for (std::size_t s = 0; s < a.scalar_cts.size(); ++s) {
+                            Ciphertext &lhs = a.scalar_cts[s];
+                            const Ciphertext &rhs = b.scalar_cts[s];
+                            if (is_trivial_zero(rhs)) continue; // fold_into (:724-732)
+                            if (is_trivial_zero(lhs)) {
+                                lhs = rhs;
+                                continue;
+                            }
+                            if (lhs.key_id != rhs.key_id || lhs.key_id != pub_.key_id)
+                                throw Error("add_ciphertexts: key mismatch");
+                            work.emplace_back(&lhs, &rhs);
+                            ++adds;
+                        }
+                    } else {
+                        throw Error("paillier add_histograms expects encrypted layouts");
+                    }
+                }
+            } catch (...) {
+                counters_.ciphertext_additions += adds;
+                throw;
+            }
+            multiply_into(work);
+            counters_.ciphertext_additions += adds;
+        }
+        return acc;
     }
 
 private:
@@ -469,30 +596,6 @@ private:
         throw Error(msg);
     }
 
-    EncryptionPlugin &reference() {
-        if (!ref_) {
-            const char *kp_sym = "_ZN4sfxb20make_paillier_pluginERKNS_15PaillierKeypairERKNS_20PaillierPluginConfigE";
-            const char *pk_sym = "_ZN4sfxb20make_paillier_pluginERKNS_17PaillierPublicKeyERKNS_20PaillierPluginConfigE";
-            if (has_priv_) {
-                auto f = reinterpret_cast<Factory>(dlsym(RTLD_NEXT, kp_sym));
-                if (!f) throw Error("CUDA Paillier plugin: reference factory not found for the packed path");
-                ref_ = f(kp_, cfg_);
-            } else {
-                auto f = reinterpret_cast<FactoryPub>(dlsym(RTLD_NEXT, pk_sym));
-                if (!f) throw Error("CUDA Paillier plugin: reference factory not found for the packed path");
-                ref_ = f(pub_, cfg_);
-            }
-        }
-        return *ref_;
-    }
-    template <typename R, typename F>
-    R delegated(F &&f) {
-        EncryptionPlugin &r = reference();
-        const OpCounters before = r.counters();
-        R res = f(r);
-        counters_ += r.counters() - before;
-        return res;
-    }
     // One tree level of one sender's histograms: sibling nodes (ids k, k+1 with
     // k odd, federation.cpp:331-345) whose parent is found in a previously
     // decrypted level are decrypted by verified reuse (sfxb_decrypt_tree);
@@ -576,17 +679,142 @@ private:
         st->last_use = ++dec_clock_;
     }
 
-    std::vector<std::pair<std::uint32_t, Histogram>> delegate_decrypt(const HistogramPayload &p) {
-        return delegated<std::vector<std::pair<std::uint32_t, Histogram>>>(
-            [&](EncryptionPlugin &r) { return r.decrypt_histogram(p); });
+    // add_packed (he.cpp:234-253): shape and guard-capacity checks, key checks
+    // of add_ciphertexts per element; a becomes the sum's descriptor
+    void plan_add_packed(PackedVector &a, const PackedVector &b,
+                         std::vector<std::pair<Ciphertext *, const Ciphertext *>> &work) {
+        if (a.logical_length != b.logical_length || a.slot_bits != b.slot_bits || a.guard_bits != b.guard_bits ||
+            a.scale_bits != b.scale_bits || a.cts.size() != b.cts.size())
+            throw Error("add_packed: shape mismatch");
+        const std::uint64_t count = std::uint64_t(a.addend_count) + b.addend_count;
+        if (count > (std::uint64_t(1) << a.guard_bits)) throw Error("add_packed: addend capacity exceeded (guard bits)");
+        for (std::size_t i = 0; i < a.cts.size(); ++i)
+            if (a.cts[i].key_id != b.cts[i].key_id || a.cts[i].key_id != pub_.key_id)
+                throw Error("add_ciphertexts: key mismatch");
+        a.addend_count = static_cast<std::uint32_t>(count);
+        for (std::size_t i = 0; i < a.cts.size(); ++i) work.emplace_back(&a.cts[i], &b.cts[i]);
+    }
+
+    // lhs = lhs·rhs mod n² for every pair: one GPU batch; values outside
+    // [0, n²) (never produced by an encryption) take GMP's a·b % n² exactly
+    void multiply_into(const std::vector<std::pair<Ciphertext *, const Ciphertext *>> &work) {
+        std::vector<size_t> dev;
+        for (size_t i = 0; i < work.size(); ++i) {
+            const mpz_class &x = work[i].first->value, &y = work[i].second->value;
+            if (x >= 0 && x < pub_.n2 && y >= 0 && y < pub_.n2 && fits(x, ct_words_) && fits(y, ct_words_))
+                dev.push_back(i);
+            else
+                work[i].first->value = x * y % pub_.n2;
+        }
+        if (dev.empty()) return;
+        std::vector<uint32_t> A(dev.size() * ct_words_), B(dev.size() * ct_words_), C(dev.size() * ct_words_);
+        parallel_for(dev.size(), [&](size_t lo, size_t hi) {
+            for (size_t k = lo; k < hi; ++k) {
+                to_words(work[dev[k]].first->value, &A[k * ct_words_], ct_words_);
+                to_words(work[dev[k]].second->value, &B[k * ct_words_], ct_words_);
+            }
+        });
+        check(sfxb_add(ctx_, A.data(), B.data(), dev.size(), C.data()));
+        parallel_for(dev.size(), [&](size_t lo, size_t hi) {
+            for (size_t k = lo; k < hi; ++k) {
+                from_words(work[dev[k]].first->value, &C[k * ct_words_], ct_words_);
+                work[dev[k]].first->key_id = pub_.key_id;
+            }
+        });
+    }
+
+    // packed decrypt_histogram (secure_processor.cpp:697-712) = unpack_decrypt
+    // (he.cpp:255-259) per vector: the CRT decryptions of every ciphertext run
+    // as one GPU batch; key/range/coprime errors and unpack_plain errors
+    // surface in the reference's order.
+    std::vector<std::pair<std::uint32_t, Histogram>> decrypt_packed(const HistogramPayload &payload) {
+        std::vector<const PackedVector *> vecs;
+        for (const NodeHistogram &node : payload.nodes) {
+            vecs.push_back(&node.packed_g);
+            vecs.push_back(&node.packed_h);
+        }
+        size_t total = 0;
+        for (const PackedVector *v : vecs) total += v->cts.size();
+        std::vector<uint32_t> cts(total * ct_words_);
+        size_t bad = total;
+        std::string bad_msg;
+        {
+            size_t i = 0;
+            for (const PackedVector *v : vecs) {
+                for (const Ciphertext &c : v->cts) {
+                    if (c.key_id != pub_.key_id) bad_msg = "decrypt: ciphertext key mismatch";
+                    else if (c.value < 1 || c.value >= pub_.n2 || !fits(c.value, ct_words_))
+                        bad_msg = "decrypt: ciphertext out of range";
+                    if (!bad_msg.empty()) break;
+                    to_words(c.value, &cts[i * ct_words_], ct_words_);
+                    ++i;
+                }
+                if (!bad_msg.empty()) break;
+            }
+            bad = i;
+        }
+        std::vector<uint32_t> plain(std::max<size_t>(bad, 1) * n_words_);
+        std::vector<double> vals(std::max<size_t>(bad, 1));
+        uint64_t decs = 0;
+        if (bad) {
+            int rc = sfxb_decrypt(ctx_, cts.data(), bad, scale_bits_, vals.data(), plain.data(), &decs);
+            if (rc == SFXB_ERR_COPRIME) {
+                // locate the first ciphertext sharing a factor with n, as the reference would meet it
+                mpz_class g;
+                size_t k = 0;
+                for (const PackedVector *v : vecs) {
+                    for (const Ciphertext &c : v->cts) {
+                        if (k == bad) break;
+                        mpz_gcd(g.get_mpz_t(), c.value.get_mpz_t(), pub_.n.get_mpz_t());
+                        if (g != 1) break;
+                        ++k;
+                    }
+                    if (k == bad || g != 1) break;
+                }
+                bad = k;
+                bad_msg = "decrypt: ciphertext not coprime to modulus";
+                rc = bad ? sfxb_decrypt(ctx_, cts.data(), bad, scale_bits_, vals.data(), plain.data(), &decs) : SFXB_OK;
+            }
+            check(rc);
+        }
+        std::vector<std::pair<std::uint32_t, Histogram>> out;
+        size_t idx = 0, vi = 0;
+        for (const NodeHistogram &node : payload.nodes) {
+            std::vector<double> gh[2];
+            for (int w = 0; w < 2; ++w, ++vi) {
+                const PackedVector &v = *vecs[vi];
+                if (bad < idx + v.cts.size()) throw Error(bad_msg);
+                std::vector<mpz_class> m(v.cts.size());
+                for (size_t k = 0; k < m.size(); ++k) from_words(m[k], &plain[(idx + k) * n_words_], n_words_);
+                const PackedLayout layout{pub_.modulus_bits, v.slot_bits, v.guard_bits, v.scale_bits};
+                gh[w] = unpack_plain(layout, m, v.logical_length, v.addend_count);
+                idx += v.cts.size();
+            }
+            counters_.decryptions += 2; // vector granularity
+            const std::size_t expect = node.feature_ids.size() * static_cast<std::size_t>(node.n_bins);
+            if (gh[0].size() != expect || gh[1].size() != expect)
+                throw Error("decrypt_histogram: packed length mismatch");
+            Histogram hist;
+            hist.n_bins = node.n_bins;
+            hist.feature_ids = node.feature_ids;
+            for (std::size_t f = 0; f < node.feature_ids.size(); ++f) {
+                std::vector<GHPair> slots(static_cast<std::size_t>(node.n_bins));
+                for (int b = 0; b < node.n_bins; ++b) {
+                    const std::size_t i = f * static_cast<std::size_t>(node.n_bins) + static_cast<std::size_t>(b);
+                    slots[static_cast<std::size_t>(b)] = {gh[0][i], gh[1][i]};
+                }
+                hist.feats.push_back(std::move(slots));
+            }
+            out.emplace_back(node.node_id, std::move(hist));
+        }
+        return out;
     }
 
     PaillierPublicKey pub_;
     PaillierPrivateKey priv_;
     bool has_priv_;
-    PaillierKeypair kp_;
-    PaillierPluginConfig cfg_;
     unsigned scale_bits_;
+    PackedLayout layout_; // validated lazily, as the reference does
     gmp_randstate_t rng_, rng_snapshot_;
     sfxb_ctx *ctx_ = nullptr;
     size_t n_words_ = 0, ct_words_ = 0;
@@ -598,7 +826,6 @@ private:
     std::vector<std::vector<std::uint32_t>> prev_rows_;
     uint64_t gh_hash_ = 0;
     size_t gh_count_ = 0;
-    std::unique_ptr<EncryptionPlugin> ref_;
     std::vector<DecStream> dec_streams_;
     uint64_t dec_clock_ = 0;
 };

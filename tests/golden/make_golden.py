@@ -99,6 +99,7 @@ TRAIN_CONFIGS = {
     "vertical_toy512": ("vertical_toy512.ini", 512, 0xACCE55),
     "vertical_threaded_3p": ("vertical_threaded_3p.ini", 512, 0xC0FFEE),
     "vertical_c1_1024": ("vertical_c1_1024.ini", 1024, 7),
+    "horizontal_toy1024": ("horizontal_toy1024.ini", 1024, 7),
 }
 
 

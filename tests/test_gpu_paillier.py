@@ -191,3 +191,19 @@ def test_large_batches_equal_small_batches(oracle, kname):
     decs = ops.decrypt(big, count, vals)
     assert decs == count
     np.testing.assert_array_equal(vals.cpu().numpy(), np.ldexp(qq.astype(np.float64), -40))
+
+
+@pytest.mark.parametrize("kname", ["k512_c0ffee", "k1024_7", "k2048_7"])
+def test_encrypt_plain_words_matches_oracle(oracle, kname):
+    """sfxb_encrypt_plain (packed-vector plaintexts, he.cpp:220-232): full-width
+    m ∈ [0, n), CRT and public-key contexts, plus the m range check."""
+    n, p, q = key(kname)
+    ok = OracleKey(oracle, n, p, q)
+    rng = random.Random(kname + "plain")
+    ms = [0, 1, n - 1, (n - 1) // 2] + [rng.randrange(n) for _ in range(12)]
+    rs = [rng.randrange(2, n) for _ in ms]
+    for ctx in (_lib.Context(n, p, q), _lib.Context(n)):
+        got = words_to_ints(ctx.encrypt_plain(ints_to_words(ms, ctx.nw), ints_to_words(rs, ctx.nw)))
+        assert got == [ok.encrypt_with_r(m, r) for m, r in zip(ms, rs)]
+        with pytest.raises(_lib.SfxbError, match="plaintext out of range"):
+            ctx.encrypt_plain(ints_to_words([n], ctx.nw), ints_to_words([5], ctx.nw))
