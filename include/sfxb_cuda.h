@@ -55,6 +55,33 @@ typedef struct sfxb_ctx sfxb_ctx;
  * federation.cpp:83-85); otherwise pq_words limbs each.  n up to 3072 bits. */
 int sfxb_ctx_create(sfxb_ctx **out, int device, const uint32_t *n, uint32_t n_words,
                     const uint32_t *p, const uint32_t *q, uint32_t pq_words);
+/* One key on several GPUs of this process (SURVEY §8e inside the reference's
+ * single-process plugin; replaces the same factories).  `devices` lists 1–16
+ * CUDA devices, one shard each (a device may repeat: its shards then share
+ * that GPU — the logic check used on one-GPU machines).  Distinct devices need
+ * peer access (NVLink/NVSwitch); otherwise SFXB_ERR_UNSUPPORTED.
+ * The host-buffer entry points use every shard:
+ *   sfxb_encrypt / sfxb_encrypt_plain / sfxb_add / sfxb_decrypt — contiguous
+ *     element ranges, one per GPU (≥ 4096 exponentiations per GPU);
+ *   sfxb_gh_upload — gh rows in contiguous row shards, one per GPU;
+ *   sfxb_accumulate / sfxb_accumulate_gh / sfxb_accumulate_tree_gh — each GPU
+ *     builds partial histograms of its rows (Montgomery form); GPU k then
+ *     multiplies slot slice k of every node across all GPUs, reading the
+ *     peers' partials over NVLink in one kernel (a modular product: no NCCL
+ *     reduction op can combine ciphertexts), applies sibling subtraction on
+ *     its slice and writes its slice of the caller's output;
+ *   sfxb_decrypt_tree — every node's slots in per-GPU slices.
+ * Results and counters are identical to a single-device context.  The
+ * encrypt/decrypt/reduce *_dev entry points act on shard 0 only (device
+ * pointers of devices[0]); sfxb_gh_from_dev and sfxb_accumulate*_dev return
+ * SFXB_ERR_UNSUPPORTED on a group (its gradient handle is host-API only). */
+int sfxb_ctx_create_multi(sfxb_ctx **out, const int *devices, uint32_t n_devices, const uint32_t *n,
+                          uint32_t n_words, const uint32_t *p, const uint32_t *q, uint32_t pq_words);
+/* visible CUDA devices (0 without a driver/GPU) */
+int sfxb_device_count(void);
+/* shards of a context (1 for sfxb_ctx_create) and the device of shard k */
+uint32_t sfxb_ctx_n_shards(const sfxb_ctx *ctx);
+int sfxb_ctx_shard_device(const sfxb_ctx *ctx, uint32_t k);
 void sfxb_ctx_destroy(sfxb_ctx *ctx);
 const char *sfxb_last_error(const sfxb_ctx *ctx);
 /* error text of the last failed sfxb_ctx_create on this thread */

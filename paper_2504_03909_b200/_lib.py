@@ -55,6 +55,11 @@ def load() -> C.CDLL:
     vp, sz = C.c_void_p, C.c_size_t
     sig = {
         "sfxb_ctx_create": (C.c_int, [C.POINTER(vp), C.c_int, _u32p, C.c_uint32, vp, vp, C.c_uint32]),
+        "sfxb_ctx_create_multi": (C.c_int, [C.POINTER(vp), _i32p, C.c_uint32, _u32p, C.c_uint32, vp, vp,
+                                            C.c_uint32]),
+        "sfxb_ctx_n_shards": (C.c_uint32, [vp]),
+        "sfxb_device_count": (C.c_int, []),
+        "sfxb_ctx_shard_device": (C.c_int, [vp, C.c_uint32]),
         "sfxb_ctx_destroy": (None, [vp]),
         "sfxb_last_error": (C.c_char_p, [vp]),
         "sfxb_create_error": (C.c_char_p, []),
@@ -125,21 +130,29 @@ def from_words(w) -> int:
 
 
 class Context:
-    """One Paillier key on one device (sfxb_ctx)."""
+    """One Paillier key on one device (sfxb_ctx), or on a device group when
+    `devices` lists several GPUs (sfxb_ctx_create_multi)."""
 
-    def __init__(self, n: int, p: int | None = None, q: int | None = None, device: int = 0):
+    def __init__(self, n: int, p: int | None = None, q: int | None = None, device: int = 0,
+                 devices: list[int] | None = None):
         lib = load()
         self.lib = lib
         self.n = n
         self.nw = (n.bit_length() + 31) // 32
         h = C.c_void_p()
         nw_arr = to_words(n, self.nw)
+        pa = qa = None
+        pw = 0
         if p is not None:
             pw = max((p.bit_length() + 31) // 32, (q.bit_length() + 31) // 32)
             pa, qa = to_words(p, pw), to_words(q, pw)
-            rc = lib.sfxb_ctx_create(C.byref(h), device, nw_arr, self.nw, pa.ctypes.data, qa.ctypes.data, pw)
+        pp = pa.ctypes.data if pa is not None else None
+        qp = qa.ctypes.data if qa is not None else None
+        if devices is not None:
+            dv = np.ascontiguousarray(devices, dtype=np.int32)
+            rc = lib.sfxb_ctx_create_multi(C.byref(h), dv, len(dv), nw_arr, self.nw, pp, qp, pw)
         else:
-            rc = lib.sfxb_ctx_create(C.byref(h), device, nw_arr, self.nw, None, None, 0)
+            rc = lib.sfxb_ctx_create(C.byref(h), device, nw_arr, self.nw, pp, qp, pw)
         if rc != SFXB_OK:
             raise SfxbError(rc, lib.sfxb_create_error().decode())
         self.h = h
@@ -179,6 +192,10 @@ class Context:
         n, ms, mm = C.c_uint64(), C.c_double(), C.c_uint64()
         self._check(self.lib.sfxb_ctx_kernel_stats(self.h, family, C.byref(n), C.byref(ms), C.byref(mm)))
         return n.value, ms.value, mm.value
+
+    @property
+    def n_shards(self) -> int:
+        return self.lib.sfxb_ctx_n_shards(self.h)
 
     @property
     def launches(self) -> int:

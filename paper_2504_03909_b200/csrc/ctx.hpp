@@ -10,6 +10,8 @@
 
 #include "bignum_host.hpp"
 
+struct sfxb_ctx;
+
 namespace sfxb {
 
 // Device copy of a Montgomery modulus: 4·S words [m | R mod m | R² | R³].
@@ -85,7 +87,8 @@ struct CtxState {
     struct DecCache {
         Buf cts[2], plain[2]; // [cur] = previous level, [cur ^ 1] = this call
         int cur = 0;
-        uint32_t n_nodes = 0, spn = 0;
+        uint32_t n_nodes = 0, spn = 0; // spn: slots of this context's slice per node
+        uint32_t spn_total = 0, j0 = 0; // the caller's slots per node and the slice start
         bool valid = false;
     };
     std::map<uint64_t, DecCache> dec_cache;
@@ -95,6 +98,13 @@ struct CtxState {
     // scratch (grown on demand, freed with the context)
     Buf scratch_table, tmp[4], host_pinned[2], io[6]; // io: host-API staging (grow-only)
     std::vector<void *> owned; // device allocations of constants
+    void *hist = nullptr;      // K2 work buffers (HistBufs, sfxb_cuda.cu), grown on demand
+
+    // device group (sfxb_ctx_create_multi): shard contexts, shards[0] == this;
+    // empty for a single-device context
+    std::vector<::sfxb_ctx *> shards;
+    cudaEvent_t ev_part = nullptr; // this shard's partial histograms are complete
+    uint32_t tree_j0 = 0, tree_jl = 0, tree_G = 0; // group tree cache: this shard's slot slice
     // one spare gh allocation (limbs + flags), recycled by the next upload
     void *spare_gh = nullptr, *spare_flags = nullptr;
     size_t spare_gh_bytes = 0, spare_flags_bytes = 0;

@@ -361,5 +361,63 @@ __global__ void __launch_bounds__(kBlock) k_reduce_parts(ModArg M, const uint32_
     }
 }
 
+// ---------------------------------------------------------------- multi-GPU (one process)
+//
+// A device group holds the gh rows in contiguous row shards, one per GPU.
+// Each shard builds Montgomery-form partial histograms of its own rows; shard k
+// then owns slot slice [j0, j0 + jl) of every node and multiplies the partials
+// of all shards for that slice, reading the peers' buffers directly over
+// NVLink (P2P loads; no staging copy, no NCCL: homomorphic addition is a
+// modular product, which no NCCL reduction op computes).
+
+constexpr int kMaxShards = 16;
+struct PeerSet {
+    const uint32_t *p[kMaxShards];
+    uint32_t n;
+};
+
+// out[node·jl + j] = ∏_shards part[node·spn + j0 + j]   (Montgomery form)
+template <int S, int TPI>
+__global__ void __launch_bounds__(kBlock) k_reduce_peer(ModArg M, PeerSet parts, size_t n_nodes, size_t spn,
+                                                        size_t j0, size_t jl, uint32_t *out) {
+    constexpr int L = S / TPI, NI = kBlock / TPI;
+    __shared__ uint2 sB[S / 2 * NI];
+    const Stage st = make_stage<TPI>(sB);
+    const ModRef mr = M.ref();
+    uint32_t N[L];
+    load_const<S, TPI>(N, mr, kMod);
+    SFXB_UNIFORM_LOOP(e, active, n_nodes * jl) {
+        const size_t src = (e / jl) * spn + j0 + e % jl;
+        uint32_t acc[L], x[L];
+        load_lane<S, TPI>(acc, parts.p[0] + src * S);
+        for (uint32_t p = 1; p < parts.n; ++p) {
+            load_lane<S, TPI>(x, parts.p[p] + src * S);
+            mmul<S, TPI>(acc, acc, x, st, N, M.np);
+        }
+        if (active) store_lane<S, TPI>(out + e * S, acc);
+    }
+}
+
+// per (key, gh): real (non-trivial-zero) ciphertexts folded into the slot
+__global__ void k_hist_real(const uint32_t *count, const uint32_t *ones, size_t nkeys, uint32_t *real) {
+    for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < nkeys; k += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t c = count[k];
+        real[2 * k] = c - (ones ? ones[2 * k] : 0u);
+        real[2 * k + 1] = c - (ones ? ones[2 * k + 1] : 0u);
+    }
+}
+
+// the reference counter over the whole group: Σ_slots max(Σ_shards real − 1, 0)
+__global__ void k_adds_multi(PeerSet real, size_t n, unsigned long long *adds) {
+    unsigned long long local = 0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        unsigned long long t = 0;
+        for (uint32_t p = 0; p < real.n; ++p) t += real.p[p][i];
+        local += t > 0 ? t - 1 : 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(adds, local);
+}
+
 } // namespace dev
 } // namespace sfxb

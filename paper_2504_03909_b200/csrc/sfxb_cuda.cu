@@ -7,7 +7,10 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
+#include <algorithm>
+#include <exception>
 
 #include <dlfcn.h>
 
@@ -85,6 +88,9 @@ struct sfxb_gh {
     uint8_t *flags = nullptr;  // per row: bit0 Enc(g) == 1, bit1 Enc(h) == 1
     uint32_t n_samples = 0;
     size_t bytes = 0, fbytes = 0;
+    // device group: one handle per shard holding rows [row_lo[k], row_lo[k+1])
+    std::vector<sfxb_gh *> parts;
+    std::vector<uint32_t> row_lo;
 };
 
 namespace {
@@ -443,11 +449,25 @@ constexpr int kPiece = 16, kPieceLong = 64;
 
 struct HistBufs {
     Buf node_of, count, ones, cursor, seg_start, sorted, np, piece_start, pieces, part[2], cub, misc, plen, pord,
-        derived, pairs, tree_up, tree_dn;
+        derived, pairs, tree_up, tree_dn,
+        // device group: bins slice, local frontier, partials, real counts, slice staging
+        g_bins, g_offs, g_rows, g_part, g_real, g_hist, g_plain, g_misc;
+    Buf *all() { return &node_of; }
+    static constexpr int kCount = 27;
 };
+static_assert(sizeof(HistBufs) == HistBufs::kCount * sizeof(Buf), "HistBufs is a plain array of Buf");
+// per context (a context is used by one host thread at a time)
 HistBufs &hist_bufs(sfxb_ctx *c) {
-    static thread_local std::map<sfxb_ctx *, HistBufs> m; // per context, per thread
-    return m[c];
+    if (!c->hist) c->hist = new HistBufs();
+    return *static_cast<HistBufs *>(c->hist);
+}
+void free_hist_bufs(sfxb_ctx *c) {
+    if (!c->hist) return;
+    HistBufs *B = static_cast<HistBufs *>(c->hist);
+    for (int i = 0; i < HistBufs::kCount; ++i)
+        if (B->all()[i].p) cudaFree(B->all()[i].p);
+    delete B;
+    c->hist = nullptr;
 }
 
 void gh_prepare(sfxb_ctx *c, sfxb_gh *g) {
@@ -495,14 +515,79 @@ T *bget(Buf &b, size_t n) {
     return (T *)grow(b, n * sizeof(T) + 64);
 }
 
+// Sibling subtraction on a level's Montgomery-form histograms `hist`
+// (n_nodes × spn slots, node-major): for every pair, slots of `derived` =
+// parent_hist[parent] · hist[small]⁻¹ mod n², all inverses from one batch
+// inversion (product tree up on the GPU, root inverse on the host, tree down).
+// Returns false (nothing written) when some small-child slot is not a unit.
+template <int cs>
+bool derive_siblings(sfxb_ctx *c, HistBufs &B, uint32_t *hist, const uint32_t *parent_hist,
+                     const dev::Derived *d_pairs, size_t n_pairs, size_t spn) {
+    using C = Cls<cs>;
+    constexpr int S4 = 4 * cs, NI = dev::kBlock / C::TH;
+    cudaStream_t st = c->stream;
+    const size_t m = n_pairs * spn; // values to invert
+    // level sizes of the product tree
+    std::vector<size_t> lvl_n{m}, lvl_off{0};
+    while (lvl_n.back() > 1) {
+        lvl_off.push_back(lvl_off.back() + lvl_n.back());
+        lvl_n.push_back((lvl_n.back() + 1) / 2);
+    }
+    const size_t total = lvl_off.back() + lvl_n.back();
+    uint32_t *tr = bget<uint32_t>(B.tree_up, total * S4);
+    uint32_t *inv = bget<uint32_t>(B.tree_dn, total * S4);
+    {
+        const size_t words = m * S4;
+        const int gg = (int)std::min<size_t>((words + 255) / 256, (size_t)c->sms * 16);
+        dev::k_gather_small<<<gg, 256, 0, st>>>(hist, d_pairs, n_pairs, spn, S4, tr);
+        check_launch(*c);
+    }
+    auto kup = dev::k_pair_up<S4, C::TH>;
+    for (size_t l = 0; l + 1 < lvl_n.size(); ++l) {
+        const int gu = occupancy_grid(*c, kup, lvl_n[l + 1], NI);
+        ProfScope prof_(*c, 3, lvl_n[l] / 2);
+        kup<<<gu, dev::kBlock, 0, st>>>(arg(c->mod_n2), tr + lvl_off[l] * S4, lvl_n[l], tr + lvl_off[l + 1] * S4);
+        check_launch(*c);
+    }
+    // invert the root on the host (GMP mpz_invert, or binary extended Euclid)
+    std::vector<uint32_t> root(S4);
+    CK(cudaMemcpyAsync(root.data(), tr + lvl_off.back() * S4, S4 * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    host::Big plain = c->mh_n2->from_mont(host::from_words(root.data(), S4)), rinv;
+    if (!host::inv_mod_fast(plain, c->n2, rinv)) return false;
+    host::Big rinv_m = host::pad(c->mh_n2->to_mont(rinv), S4);
+    CK(cudaMemcpyAsync(inv + lvl_off.back() * S4, rinv_m.data(), S4 * 4, cudaMemcpyHostToDevice, st));
+    auto kdn = dev::k_pair_down<S4, C::TH>;
+    for (size_t l = lvl_n.size() - 1; l-- > 0;) {
+        const int gd = occupancy_grid(*c, kdn, lvl_n[l], NI);
+        ProfScope prof_(*c, 3, lvl_n[l]);
+        kdn<<<gd, dev::kBlock, 0, st>>>(arg(c->mod_n2), inv + lvl_off[l + 1] * S4, tr + lvl_off[l] * S4, lvl_n[l],
+                                        inv + lvl_off[l] * S4);
+        check_launch(*c);
+    }
+    CK(cudaStreamSynchronize(st)); // rinv_m is a host temporary
+    auto kd = dev::k_derive<S4, C::TH>;
+    const int gdv = occupancy_grid(*c, kd, m, NI);
+    ProfScope prof_(*c, 3, m);
+    kd<<<gdv, dev::kBlock, 0, st>>>(arg(c->mod_n2), parent_hist, inv, d_pairs, n_pairs, spn, hist);
+    check_launch(*c);
+    return true;
+}
+
 // Tree mode (h_parent != nullptr): h_parent[i] is the index of frontier node
 // i's parent in the PREVIOUS tree-mode call on this context (−1: none).  The
 // context keeps that call's histograms (Montgomery form) as parents; siblings
 // (exactly two children of one cached parent) are split into a directly built
 // small child and a derived large child.
+//
+// Device-group shards (accumulate_group) pass h_skip (nodes not built here:
+// their slots stay the identity, as the group derives them after the
+// cross-shard product) and d_real (2·N·J·K per-slot counts of non-trivial
+// ciphertexts, for the group-wide reference counter).
 void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint32_t J, const uint32_t *d_offsets,
                     uint32_t N, const uint32_t *d_rows, uint32_t R, uint32_t K, uint32_t *d_out, int mont_out,
-                    uint64_t *additions, const int32_t *h_parent = nullptr, const uint32_t *h_offsets = nullptr) {
+                    uint64_t *additions, const int32_t *h_parent = nullptr, const uint32_t *h_offsets = nullptr,
+                    const uint8_t *h_skip = nullptr, uint32_t *d_real = nullptr) {
     if (!g || g->ctx != c) throw ApiError(SFXB_ERR_ARG, "accumulate: gradient handle belongs to another context");
     if (K == 0 || K > 65536) throw ApiError(SFXB_ERR_ARG, "accumulate: n_bins out of range");
     const size_t nkeys = (size_t)N * J * K;
@@ -537,6 +622,13 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
             derived_rows += std::max(na, nb);
         }
     }
+    if (h_skip && !tree) {
+        if (!h_offsets) throw ApiError(SFXB_ERR_ARG, "accumulate: skip mask needs host offsets");
+        derived_flag.assign(h_skip, h_skip + N);
+        for (uint32_t i = 0; i < N; ++i)
+            if (h_skip[i]) derived_rows += h_offsets[i + 1] - h_offsets[i];
+    }
+    const bool any_skip = std::find(derived_flag.begin(), derived_flag.end(), (uint8_t)1) != derived_flag.end();
     if (nkeys >= 0xffffffffull || (size_t)R * J >= 0xffffffffull)
         throw ApiError(SFXB_ERR_ARG, "accumulate: frontier too large for one call");
     HistBufs &B = hist_bufs(c);
@@ -563,12 +655,14 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
     a.status = misc;
     uint8_t *d_derived = nullptr;
     dev::Derived *d_pairs = nullptr;
-    if (!pairs.empty()) {
+    if (any_skip) {
         d_derived = bget<uint8_t>(B.derived, N);
-        d_pairs = bget<dev::Derived>(B.pairs, pairs.size());
         CK(cudaMemcpyAsync(d_derived, derived_flag.data(), N, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(d_pairs, pairs.data(), pairs.size() * sizeof(dev::Derived), cudaMemcpyHostToDevice, st));
         a.derived = d_derived;
+    }
+    if (!pairs.empty()) {
+        d_pairs = bget<dev::Derived>(B.pairs, pairs.size());
+        CK(cudaMemcpyAsync(d_pairs, pairs.data(), pairs.size() * sizeof(dev::Derived), cudaMemcpyHostToDevice, st));
     }
     if (R > 0) {
         uint32_t *node_of = bget<uint32_t>(B.node_of, R);
@@ -591,10 +685,14 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
         int grid = (int)std::min<size_t>((nkeys + 255) / 256, (size_t)c->sms * 8);
         dev::k_hist_adds<<<grid, 256, 0, st>>>(count, ones, nkeys, adds_d);
         check_launch(*c);
+        if (d_real) {
+            dev::k_hist_real<<<grid, 256, 0, st>>>(count, ones, nkeys, d_real);
+            check_launch(*c);
+        }
     }
-    // derived nodes are not built directly
-    for (const dev::Derived &d : pairs)
-        CK(cudaMemsetAsync(count + (size_t)d.derived * J * K, 0, (size_t)J * K * 4, st));
+    // derived / skipped nodes are not built directly
+    for (uint32_t i = 0; i < (uint32_t)derived_flag.size(); ++i)
+        if (derived_flag[i]) CK(cudaMemsetAsync(count + (size_t)i * J * K, 0, (size_t)J * K * 4, st));
     // scan counts -> segment starts; max count -> number of passes
     size_t tmp_bytes = 0, tmp2 = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, count, seg_start, (int)nkeys, st));
@@ -706,59 +804,8 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
         uint32_t *hist = (uint32_t *)grow(c->tree_buf[c->tree_cur ^ 1], (size_t)N * spn * S4 * 4 + 64);
         kf<<<grid, dev::kBlock, 0, st>>>(arg(c->mod_n2), count, final_idx, nkeys, final_part, hist, 1);
         check_launch(*c);
-        bool derived_ok = true;
-        if (!pairs.empty()) {
-            const size_t m = pairs.size() * spn; // values to invert
-            // level sizes of the product tree
-            std::vector<size_t> lvl_n{m}, lvl_off{0};
-            while (lvl_n.back() > 1) {
-                lvl_off.push_back(lvl_off.back() + lvl_n.back());
-                lvl_n.push_back((lvl_n.back() + 1) / 2);
-            }
-            const size_t total = lvl_off.back() + lvl_n.back();
-            uint32_t *tr = bget<uint32_t>(B.tree_up, total * S4);
-            uint32_t *inv = bget<uint32_t>(B.tree_dn, total * S4);
-            {
-                const size_t words = m * S4;
-                const int gg = (int)std::min<size_t>((words + 255) / 256, (size_t)c->sms * 16);
-                dev::k_gather_small<<<gg, 256, 0, st>>>(hist, d_pairs, pairs.size(), spn, S4, tr);
-                check_launch(*c);
-            }
-            auto kup = dev::k_pair_up<S4, C::TH>;
-            for (size_t l = 0; l + 1 < lvl_n.size(); ++l) {
-                const int gu = occupancy_grid(*c, kup, lvl_n[l + 1], NI);
-                ProfScope prof_(*c, 3, lvl_n[l] / 2);
-                kup<<<gu, dev::kBlock, 0, st>>>(arg(c->mod_n2), tr + lvl_off[l] * S4, lvl_n[l],
-                                               tr + lvl_off[l + 1] * S4);
-                check_launch(*c);
-            }
-            // invert the root on the host (plain value, binary extended Euclid)
-            std::vector<uint32_t> root(S4);
-            CK(cudaMemcpyAsync(root.data(), tr + lvl_off.back() * S4, S4 * 4, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            host::Big plain = c->mh_n2->from_mont(host::from_words(root.data(), S4)), rinv;
-            if (!host::inv_mod_fast(plain, c->n2, rinv)) {
-                derived_ok = false; // some slot is not a unit: build those nodes directly below
-            } else {
-                host::Big rinv_m = host::pad(c->mh_n2->to_mont(rinv), S4);
-                CK(cudaMemcpyAsync(inv + lvl_off.back() * S4, rinv_m.data(), S4 * 4, cudaMemcpyHostToDevice, st));
-                auto kdn = dev::k_pair_down<S4, C::TH>;
-                for (size_t l = lvl_n.size() - 1; l-- > 0;) {
-                    const int gd = occupancy_grid(*c, kdn, lvl_n[l], NI);
-                    ProfScope prof_(*c, 3, lvl_n[l]);
-                    kdn<<<gd, dev::kBlock, 0, st>>>(arg(c->mod_n2), inv + lvl_off[l + 1] * S4, tr + lvl_off[l] * S4,
-                                                    lvl_n[l], inv + lvl_off[l] * S4);
-                    check_launch(*c);
-                }
-                CK(cudaStreamSynchronize(st)); // rinv_m is a host temporary
-                auto kd = dev::k_derive<S4, C::TH>;
-                const int gdv = occupancy_grid(*c, kd, m, NI);
-                ProfScope prof_(*c, 3, m);
-                kd<<<gdv, dev::kBlock, 0, st>>>(arg(c->mod_n2), (const uint32_t *)c->tree_buf[c->tree_cur].p, inv,
-                                                d_pairs, pairs.size(), spn, hist);
-                check_launch(*c);
-            }
-        }
+        const bool derived_ok = pairs.empty() ||
+            derive_siblings<cs>(c, B, hist, (const uint32_t *)c->tree_buf[c->tree_cur].p, d_pairs, pairs.size(), spn);
         if (!derived_ok) {
             // exact fallback: rebuild this level without sibling subtraction
             c->tree_valid = false;
@@ -841,6 +888,459 @@ struct DevBuf {
     DevBuf(const DevBuf &) = delete;
     DevBuf &operator=(const DevBuf &) = delete;
 };
+
+// --------------------------------------------------------------- host-buffer operations (one device)
+
+// sfxb_encrypt / sfxb_encrypt_plain: q_fixed xor m_words (count × n_words)
+void encrypt_host(sfxb_ctx *c, const int64_t *q_fixed, const uint32_t *m_words, const uint32_t *r, size_t count,
+                  uint32_t *out_cts, uint8_t *r_flags) {
+    CK(cudaSetDevice(c->device));
+    if (count == 0) return;
+    const size_t Sn = 2 * (size_t)c->s, S4 = 4 * (size_t)c->s;
+    // range checks of encrypt_with_r (he.cpp:88-89), in its order per element
+    for (size_t i = 0; i < count; ++i) {
+        if (m_words && host::cmp(host::from_words(m_words + i * c->nw, c->nw), c->n) >= 0)
+            throw ApiError(SFXB_ERR_RANGE, "encrypt: plaintext out of range [0, n)");
+        const uint32_t *ri = r + i * c->nw;
+        bool small = true;
+        for (uint32_t k = 1; k < c->nw; ++k) small &= ri[k] == 0;
+        if (small && ri[0] < 1) throw ApiError(SFXB_ERR_RANGE, "encrypt: blinding factor out of range");
+        if (host::cmp(host::from_words(ri, c->nw), c->n) >= 0)
+            throw ApiError(SFXB_ERR_RANGE, "encrypt: blinding factor out of range");
+    }
+    IoBuf<int64_t> dq(c->io[0], m_words ? 1 : count);
+    IoBuf<uint32_t> dr(c->io[1], count * Sn), dout(c->io[2], count * S4);
+    IoBuf<uint8_t> dflags(c->io[3], count);
+    IoBuf<uint32_t> dm(c->io[4], m_words ? count * Sn : 1);
+    CK(cudaMemsetAsync(dflags.p, 0, count, c->stream));
+    if (m_words) h2d_padded(c, dm.p, m_words, count, c->nw, Sn);
+    else CK(cudaMemcpyAsync(dq.p, q_fixed, count * 8, cudaMemcpyHostToDevice, c->stream));
+    h2d_padded(c, dr.p, r, count, c->nw, Sn);
+    int st = SFXB_OK;
+    try {
+        encrypt_dev(c, m_words ? nullptr : dq.p, dr.p, count, dout.p, dflags.p, m_words ? dm.p : nullptr);
+    } catch (const ApiError &e) {
+        if (e.code != SFXB_ERR_COPRIME) throw;
+        st = e.code;
+        c->err = e.what();
+    }
+    if (r_flags) {
+        CK(cudaMemcpyAsync(r_flags, dflags.p, count, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    if (st != SFXB_OK) throw ApiError(st, c->err);
+    d2h_padded(c, out_cts, dout.p, count, 2 * c->nw, S4);
+}
+
+// rows × cols values of `words` limbs, taken from column col0 of a host matrix
+// with `pitch` values per row, into a dense device layout of `stride` limbs
+void h2d_cols(sfxb_ctx *c, uint32_t *d, const uint32_t *h, size_t rows, size_t pitch, size_t col0, size_t cols,
+              size_t words, size_t stride) {
+    if (!rows || !cols) return;
+    if (words == stride) {
+        CK(cudaMemcpy2DAsync(d, cols * stride * 4, h + col0 * words, pitch * words * 4, cols * words * 4, rows,
+                             cudaMemcpyHostToDevice, c->stream));
+        return;
+    }
+    std::vector<uint32_t> tmp(rows * cols * stride, 0u);
+    for (size_t r = 0; r < rows; ++r)
+        for (size_t j = 0; j < cols; ++j)
+            std::memcpy(&tmp[(r * cols + j) * stride], h + (r * pitch + col0 + j) * words, words * 4);
+    CK(cudaMemcpyAsync(d, tmp.data(), tmp.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+}
+// the inverse of h2d_cols (synchronous)
+void d2h_cols(sfxb_ctx *c, uint32_t *h, const uint32_t *d, size_t rows, size_t pitch, size_t col0, size_t cols,
+              size_t words, size_t stride) {
+    if (!rows || !cols) return;
+    if (words == stride) {
+        CK(cudaMemcpy2DAsync(h + col0 * words, pitch * words * 4, d, cols * stride * 4, cols * words * 4, rows,
+                             cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return;
+    }
+    std::vector<uint32_t> tmp(rows * cols * stride);
+    CK(cudaMemcpyAsync(tmp.data(), d, tmp.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (size_t r = 0; r < rows; ++r)
+        for (size_t j = 0; j < cols; ++j)
+            std::memcpy(h + (r * pitch + col0 + j) * words, &tmp[(r * cols + j) * stride], words * 4);
+}
+
+void add_host(sfxb_ctx *c, const uint32_t *a, const uint32_t *b, size_t count, uint32_t *out) {
+    CK(cudaSetDevice(c->device));
+    if (count == 0) return;
+    const size_t S4 = 4 * (size_t)c->s, cw = 2 * c->nw;
+    for (size_t i = 0; i < count; ++i)
+        if (host::cmp(host::from_words(a + i * cw, cw), c->n2) >= 0 ||
+            host::cmp(host::from_words(b + i * cw, cw), c->n2) >= 0)
+            throw ApiError(SFXB_ERR_RANGE, "add_ciphertexts: ciphertext out of range");
+    IoBuf<uint32_t> da(c->io[0], count * S4), db(c->io[1], count * S4), dout(c->io[2], count * S4);
+    h2d_padded(c, da.p, a, count, cw, S4);
+    h2d_padded(c, db.p, b, count, cw, S4);
+    add_dev(c, da.p, db.p, count, dout.p);
+    d2h_padded(c, out, dout.p, count, cw, S4);
+}
+
+void decrypt_host(sfxb_ctx *c, const uint32_t *cts, size_t count, uint32_t scale, double *out_values,
+                  uint32_t *out_plain, uint64_t *decryptions) {
+    CK(cudaSetDevice(c->device));
+    if (!c->has_priv) throw ApiError(SFXB_ERR_AUTH, "decrypt requested without private key material");
+    if (count == 0) return;
+    const size_t Sn = 2 * (size_t)c->s, S4 = 4 * (size_t)c->s;
+    IoBuf<uint32_t> dc(c->io[0], count * S4), dplain(c->io[1], out_plain ? count * Sn : 1);
+    IoBuf<double> dv(c->io[2], count);
+    h2d_padded(c, dc.p, cts, count, 2 * c->nw, S4);
+    decrypt_dev(c, dc.p, count, scale, dv.p, out_plain ? dplain.p : nullptr, decryptions);
+    CK(cudaMemcpyAsync(out_values, dv.p, count * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (out_plain) d2h_padded(c, out_plain, dplain.p, count, c->nw, Sn);
+}
+
+// sfxb_decrypt_tree on slot slice [j0, j0 + jl) of every node (the whole node
+// for a single-device context).  The slice's cache entry is this level's
+// ciphertexts and plaintexts; sibling checks compare slot j of a, b and P, so
+// they never leave the slice.
+void decrypt_tree_impl(sfxb_ctx *c, uint64_t tag, const uint32_t *cts, uint32_t n_nodes, uint32_t spn_total,
+                       uint32_t j0, uint32_t jl, const int32_t *parent, uint32_t scale, double *out_values,
+                       uint64_t *decryptions) {
+    CK(cudaSetDevice(c->device));
+    if (!c->has_priv) throw ApiError(SFXB_ERR_AUTH, "decrypt requested without private key material");
+    const uint32_t spn = jl;
+    const size_t count = (size_t)n_nodes * spn;
+    const size_t Sn = 2 * (size_t)c->s, S4 = 4 * (size_t)c->s;
+    CtxState::DecCache &prev = c->dec_cache[tag];
+    // sibling pairs (two children of one cached parent): b = second child
+    std::vector<uint32_t> pairs;
+    if (parent && prev.valid && prev.spn == spn && prev.spn_total == spn_total && prev.j0 == j0) {
+        std::vector<std::vector<uint32_t>> kids(prev.n_nodes);
+        for (uint32_t i = 0; i < n_nodes; ++i)
+            if (parent[i] >= 0 && (uint32_t)parent[i] < prev.n_nodes) kids[parent[i]].push_back(i);
+        for (uint32_t pnode = 0; pnode < prev.n_nodes; ++pnode)
+            if (kids[pnode].size() == 2) {
+                pairs.push_back(kids[pnode][1]);
+                pairs.push_back(kids[pnode][0]);
+                pairs.push_back(pnode);
+            }
+    }
+    const int nx = prev.cur ^ 1;
+    uint32_t *dc = (uint32_t *)grow(prev.cts[nx], count * S4 * 4 + 64);
+    uint32_t *dplain = (uint32_t *)grow(prev.plain[nx], count * Sn * 4 + 64);
+    IoBuf<double> dv(c->io[2], count ? count : 1);
+    if (count) h2d_cols(c, dc, cts, n_nodes, spn_total, j0, jl, 2 * c->nw, S4);
+    uint8_t *skip = nullptr;
+    const size_t np = pairs.size() / 3;
+    uint32_t *dpairs = nullptr;
+    if (np && spn) {
+        skip = (uint8_t *)grow(c->io[4], count + 64);
+        dpairs = (uint32_t *)grow(c->io[5], pairs.size() * 4 + 64);
+        CK(cudaMemsetAsync(skip, 0, count, c->stream));
+        CK(cudaMemcpyAsync(dpairs, pairs.data(), pairs.size() * 4, cudaMemcpyHostToDevice, c->stream));
+        dev::SibArgs sa{dc, (const uint32_t *)prev.cts[prev.cur].p, dpairs, np, spn, skip};
+        dispatch_class(c->s, [&](auto sc) {
+            constexpr int cs = decltype(sc)::value;
+            using C = Cls<cs>;
+            auto k = dev::k_sib_verify<4 * cs, C::TH>;
+            constexpr int NI = dev::kBlock / C::TH;
+            const int grid = occupancy_grid(*c, k, np * spn, NI);
+            k<<<grid, dev::kBlock, 0, c->stream>>>(arg(c->mod_n2), sa);
+            check_launch(*c);
+        });
+    }
+    if (count) decrypt_dev(c, dc, count, scale, dv.p, dplain, decryptions, skip);
+    if (skip) {
+        dispatch_class(c->s, [&](auto sc) {
+            constexpr int cs = decltype(sc)::value;
+            const int grid = (int)std::min<size_t>((np * spn + 127) / 128, (size_t)c->sms * 8);
+            dev::k_sib_derive<2 * cs><<<grid, 128, 0, c->stream>>>(
+                dpairs, np, spn, skip, dplain, (const uint32_t *)prev.plain[prev.cur].p, c->d_n, scale, dplain, dv.p);
+            check_launch(*c);
+        });
+    }
+    if (count)
+        CK(cudaMemcpy2DAsync(out_values + j0, (size_t)spn_total * 8, dv.p, (size_t)jl * 8, (size_t)jl * 8, n_nodes,
+                             cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    // this level becomes the parent level of the tag
+    prev.cur = nx;
+    prev.n_nodes = n_nodes;
+    prev.spn = spn;
+    prev.spn_total = spn_total;
+    prev.j0 = j0;
+    prev.valid = true;
+}
+
+// =================================================================== device group
+//
+// sfxb_ctx_create_multi: one key on several GPUs of this process (SURVEY §8e
+// inside the reference's single-process plugin).  Encrypt, add and decrypt
+// split their elements into contiguous ranges; decrypt_tree splits every
+// node's slots into per-GPU slices; the histogram is row-sharded with a
+// cross-GPU modular-product reduce over NVLink peer memory (accumulate_group).
+// Every shard runs on its own host thread and stream.
+
+bool is_group(const sfxb_ctx *c) { return c->shards.size() > 1; }
+
+// f(k, shard) for k < n on one host thread per shard (shard 0 on the caller's
+// thread); rethrows the error of the lowest failing shard after all finish
+template <typename F>
+void for_shards(sfxb_ctx *c, size_t n, F &&f) {
+    std::vector<std::exception_ptr> errs(n);
+    std::vector<std::thread> th;
+    th.reserve(n);
+    auto run = [&](size_t k) {
+        try {
+            CK(cudaSetDevice(c->shards[k]->device));
+            f(k, c->shards[k]);
+        } catch (...) {
+            errs[k] = std::current_exception();
+        }
+    };
+    for (size_t k = 1; k < n; ++k) th.emplace_back(run, k);
+    run(0);
+    for (auto &t : th) t.join();
+    CK(cudaSetDevice(c->device));
+    for (auto &e : errs)
+        if (e) std::rethrow_exception(e);
+}
+
+// bounds of `parts` near-equal contiguous ranges of `count` items
+std::vector<size_t> split_even(size_t count, size_t parts) {
+    std::vector<size_t> lo(parts + 1, 0);
+    const size_t base = count / parts, extra = count % parts;
+    for (size_t k = 0; k < parts; ++k) lo[k + 1] = lo[k] + base + (k < extra ? 1 : 0);
+    return lo;
+}
+// element-wise batches: no shard gets fewer than `grain` items
+std::vector<size_t> split_batch(size_t count, size_t shards, size_t grain) {
+    return split_even(count, std::max<size_t>(1, std::min(shards, count / std::max<size_t>(1, grain))));
+}
+constexpr size_t kGrainExp = 4096;   // encrypt / decrypt: one exponentiation per item
+constexpr size_t kGrainAdd = 65536;  // ct-add: one multiplication per item
+
+void encrypt_group(sfxb_ctx *c, const int64_t *q, const uint32_t *m, const uint32_t *r, size_t count,
+                   uint32_t *out, uint8_t *flags) {
+    const std::vector<size_t> lo = split_batch(count, c->shards.size(), kGrainExp);
+    const size_t nw = c->nw, cw = 2 * nw;
+    for_shards(c, lo.size() - 1, [&](size_t k, sfxb_ctx *sh) {
+        const size_t a = lo[k], n = lo[k + 1] - a;
+        encrypt_host(sh, q ? q + a : nullptr, m ? m + a * nw : nullptr, r + a * nw, n, out + a * cw,
+                     flags ? flags + a : nullptr);
+    });
+}
+
+void add_group(sfxb_ctx *c, const uint32_t *x, const uint32_t *y, size_t count, uint32_t *out) {
+    const std::vector<size_t> lo = split_batch(count, c->shards.size(), kGrainAdd);
+    const size_t cw = 2 * (size_t)c->nw;
+    for_shards(c, lo.size() - 1, [&](size_t k, sfxb_ctx *sh) {
+        const size_t a = lo[k];
+        add_host(sh, x + a * cw, y + a * cw, lo[k + 1] - a, out + a * cw);
+    });
+}
+
+void decrypt_group(sfxb_ctx *c, const uint32_t *cts, size_t count, uint32_t scale, double *vals, uint32_t *plain,
+                   uint64_t *decryptions) {
+    if (!c->has_priv) throw ApiError(SFXB_ERR_AUTH, "decrypt requested without private key material");
+    const std::vector<size_t> lo = split_batch(count, c->shards.size(), kGrainExp);
+    const size_t nw = c->nw, cw = 2 * nw;
+    std::vector<uint64_t> decs(lo.size() - 1, 0);
+    for_shards(c, lo.size() - 1, [&](size_t k, sfxb_ctx *sh) {
+        const size_t a = lo[k];
+        decrypt_host(sh, cts + a * cw, lo[k + 1] - a, scale, vals + a, plain ? plain + a * nw : nullptr, &decs[k]);
+    });
+    if (decryptions)
+        for (uint64_t d : decs) *decryptions += d;
+}
+
+void decrypt_tree_group(sfxb_ctx *c, uint64_t tag, const uint32_t *cts, uint32_t n_nodes, uint32_t spn,
+                        const int32_t *parent, uint32_t scale, double *vals, uint64_t *decryptions) {
+    if (!c->has_priv) throw ApiError(SFXB_ERR_AUTH, "decrypt requested without private key material");
+    const size_t G = c->shards.size();
+    const std::vector<size_t> jlo = split_even(spn, G);
+    std::vector<uint64_t> decs(G, 0);
+    for_shards(c, G, [&](size_t k, sfxb_ctx *sh) {
+        decrypt_tree_impl(sh, tag, cts, n_nodes, spn, (uint32_t)jlo[k], (uint32_t)(jlo[k + 1] - jlo[k]), parent,
+                          scale, vals, &decs[k]);
+    });
+    if (decryptions)
+        for (uint64_t d : decs) *decryptions += d;
+}
+
+sfxb_gh *gh_upload_group(sfxb_ctx *c, const uint32_t *gh_cts, uint32_t n_samples) {
+    const size_t G = c->shards.size(), cw = 2 * (size_t)c->nw, S4 = 4 * (size_t)c->s;
+    const std::vector<size_t> lo = split_even(n_samples, G);
+    auto g = std::make_unique<sfxb_gh>();
+    g->ctx = c;
+    g->n_samples = n_samples;
+    g->parts.assign(G, nullptr);
+    for (size_t k = 0; k <= G; ++k) g->row_lo.push_back((uint32_t)lo[k]);
+    try {
+        for_shards(c, G, [&](size_t k, sfxb_ctx *sh) {
+            const size_t n = lo[k + 1] - lo[k];
+            g->parts[k] = gh_alloc(sh, (uint32_t)n);
+            if (n) h2d_padded(sh, g->parts[k]->d, gh_cts + 2 * lo[k] * cw, 2 * n, cw, S4);
+            gh_prepare(sh, g->parts[k]);
+            CK(cudaStreamSynchronize(sh->stream));
+        });
+    } catch (...) {
+        for (sfxb_gh *p : g->parts)
+            if (p) sfxb_gh_free(p);
+        throw;
+    }
+    return g.release();
+}
+
+// Row-sharded histogram over the group (sfxb_accumulate_gh /
+// sfxb_accumulate_tree_gh on a multi-device context).
+//   phase 1, every shard: its rows of the frontier, its bin columns, partial
+//     histograms of its rows in Montgomery form (nodes derived by sibling
+//     subtraction are skipped), per-slot real-ciphertext counts;
+//   phase 2, shard k: slot slice k of every node = product of all shards'
+//     partials, read over NVLink (k_reduce_peer); sibling subtraction on the
+//     slice against the slice cached from the previous level; plain form
+//     straight into the caller's output rows.  Shard 0 also forms the
+//     reference counter from all shards' counts (k_adds_multi).
+void accumulate_group(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *bins, uint32_t J, const uint32_t *offs,
+                      uint32_t N, const uint32_t *rows, uint32_t K, const int32_t *parent, uint32_t *out_slots,
+                      uint64_t *additions) {
+    if (!g || g->ctx != c || g->parts.size() != c->shards.size())
+        throw ApiError(SFXB_ERR_ARG, "accumulate: gradient handle belongs to another context");
+    if (K == 0 || K > 65536) throw ApiError(SFXB_ERR_ARG, "accumulate: n_bins out of range");
+    const size_t G = c->shards.size(), S4 = 4 * (size_t)c->s, cw = 2 * (size_t)c->nw;
+    const size_t spn = 2 * (size_t)J * K, nkeys = (size_t)N * J * K;
+    const bool tree = parent != nullptr;
+    if (nkeys == 0) {
+        if (tree)
+            for (sfxb_ctx *sh : c->shards) sh->tree_valid = false;
+        return;
+    }
+    if (nkeys >= 0xffffffffull || (size_t)offs[N] * J >= 0xffffffffull)
+        throw ApiError(SFXB_ERR_ARG, "accumulate: frontier too large for one call");
+    // sibling pairs, chosen on global row counts (identical on every shard)
+    std::vector<dev::Derived> pairs;
+    std::vector<uint8_t> skip(N, 0);
+    if (tree && c->tree_valid && c->tree_gh == g && c->tree_J == J && c->tree_K == K && c->tree_G == G) {
+        std::vector<std::vector<uint32_t>> kids(c->tree_N);
+        for (uint32_t i = 0; i < N; ++i)
+            if (parent[i] >= 0 && (uint32_t)parent[i] < c->tree_N) kids[parent[i]].push_back(i);
+        for (uint32_t pnode = 0; pnode < c->tree_N; ++pnode) {
+            if (kids[pnode].size() != 2) continue;
+            const uint32_t a = kids[pnode][0], b = kids[pnode][1];
+            const uint32_t na = offs[a + 1] - offs[a], nb = offs[b + 1] - offs[b];
+            const uint32_t small = na <= nb ? a : b, large = na <= nb ? b : a;
+            pairs.push_back(dev::Derived{large, small, pnode});
+            skip[large] = 1;
+        }
+    }
+    const std::vector<size_t> jlo = split_even(spn, G);
+    const uint32_t n_samples = g->n_samples;
+    // ---- phase 1: partial histograms of each shard's rows
+    std::vector<const uint32_t *> part_ptr(G), real_ptr(G);
+    for_shards(c, G, [&](size_t k, sfxb_ctx *sh) {
+        const uint32_t lo = g->row_lo[k], hi = g->row_lo[k + 1];
+        std::vector<uint32_t> loffs(N + 1, 0), lrows;
+        lrows.reserve((size_t)offs[N] / G + 1024);
+        for (uint32_t i = 0; i < N; ++i) {
+            for (uint32_t t = offs[i]; t < offs[i + 1]; ++t) {
+                const uint32_t row = rows[t];
+                if (row >= n_samples) throw ApiError(SFXB_ERR_ARG, "row index out of range in accumulate");
+                if (row >= lo && row < hi) lrows.push_back(row - lo);
+            }
+            loffs[i + 1] = (uint32_t)lrows.size();
+        }
+        HistBufs &B = hist_bufs(sh);
+        const size_t nr = hi - lo, R = lrows.size();
+        uint16_t *db = bget<uint16_t>(B.g_bins, (size_t)J * nr);
+        if (nr)
+            CK(cudaMemcpy2DAsync(db, nr * 2, bins + lo, (size_t)n_samples * 2, nr * 2, J, cudaMemcpyHostToDevice,
+                                 sh->stream));
+        uint32_t *doffs = bget<uint32_t>(B.g_offs, N + 1), *drows = bget<uint32_t>(B.g_rows, R ? R : 1);
+        CK(cudaMemcpyAsync(doffs, loffs.data(), (N + 1) * 4, cudaMemcpyHostToDevice, sh->stream));
+        if (R) CK(cudaMemcpyAsync(drows, lrows.data(), R * 4, cudaMemcpyHostToDevice, sh->stream));
+        uint32_t *part = bget<uint32_t>(B.g_part, (size_t)N * spn * S4);
+        uint32_t *real = bget<uint32_t>(B.g_real, 2 * nkeys);
+        accumulate_dev(sh, g->parts[k], db, J, doffs, N, drows, (uint32_t)R, K, part, 1, nullptr, nullptr,
+                       loffs.data(), skip.data(), real);
+        CK(cudaEventRecord(sh->ev_part, sh->stream));
+        // host staging (loffs, lrows) must outlive the async copies
+        CK(cudaStreamSynchronize(sh->stream));
+        part_ptr[k] = part;
+        real_ptr[k] = real;
+    });
+    // ---- phase 2: cross-shard product of slot slices, sibling subtraction, output
+    dev::PeerSet parts{}, reals{};
+    parts.n = reals.n = (uint32_t)G;
+    for (size_t k = 0; k < G; ++k) {
+        parts.p[k] = part_ptr[k];
+        reals.p[k] = real_ptr[k];
+    }
+    std::vector<char> ok(G, 1);
+    unsigned long long adds = 0;
+    for_shards(c, G, [&](size_t k, sfxb_ctx *sh) {
+        for (size_t j = 0; j < G; ++j) CK(cudaStreamWaitEvent(sh->stream, c->shards[j]->ev_part, 0));
+        HistBufs &B = hist_bufs(sh);
+        cudaStream_t st = sh->stream;
+        const size_t j0 = jlo[k], jl = jlo[k + 1] - jlo[k], cnt = (size_t)N * jl;
+        uint32_t *hist = tree ? (uint32_t *)grow(sh->tree_buf[sh->tree_cur ^ 1], cnt * S4 * 4 + 64)
+                              : bget<uint32_t>(B.g_hist, cnt * S4);
+        if (k == 0) {
+            unsigned long long *d_adds = reinterpret_cast<unsigned long long *>(bget<uint32_t>(B.g_misc, 4));
+            CK(cudaMemsetAsync(d_adds, 0, 8, st));
+            const int grid = (int)std::min<size_t>((2 * nkeys + 255) / 256, (size_t)sh->sms * 8);
+            dev::k_adds_multi<<<grid, 256, 0, st>>>(reals, 2 * nkeys, d_adds);
+            check_launch(*sh);
+            CK(cudaMemcpyAsync(&adds, d_adds, 8, cudaMemcpyDeviceToHost, st));
+        }
+        if (cnt) {
+            dispatch_class(sh->s, [&](auto sc) {
+                constexpr int cs = decltype(sc)::value;
+                using C = Cls<cs>;
+                constexpr int NI = dev::kBlock / C::TH;
+                auto kr = dev::k_reduce_peer<4 * cs, C::TH>;
+                kr<<<occupancy_grid(*sh, kr, cnt, NI), dev::kBlock, 0, st>>>(arg(sh->mod_n2), parts, N, spn, j0, jl,
+                                                                            hist);
+                check_launch(*sh);
+                if (!pairs.empty()) {
+                    dev::Derived *d_pairs = bget<dev::Derived>(B.pairs, pairs.size());
+                    CK(cudaMemcpyAsync(d_pairs, pairs.data(), pairs.size() * sizeof(dev::Derived),
+                                       cudaMemcpyHostToDevice, st));
+                    ok[k] = derive_siblings<cs>(sh, B, hist, (const uint32_t *)sh->tree_buf[sh->tree_cur].p, d_pairs,
+                                                pairs.size(), jl);
+                }
+                if (!ok[k]) return;
+                uint32_t *plain = bget<uint32_t>(B.g_plain, cnt * S4);
+                auto kc = dev::k_from_mont_copy<4 * cs, C::TH>;
+                kc<<<occupancy_grid(*sh, kc, cnt, NI), dev::kBlock, 0, st>>>(arg(sh->mod_n2), hist, cnt, plain);
+                check_launch(*sh);
+                d2h_cols(sh, out_slots, plain, N, spn, j0, jl, cw, S4);
+            });
+        }
+        CK(cudaStreamSynchronize(st));
+    });
+    if (std::find(ok.begin(), ok.end(), 0) != ok.end()) {
+        // some small-child slot is not a unit: rebuild this level directly
+        for (sfxb_ctx *sh : c->shards) sh->tree_valid = false;
+        std::vector<int32_t> none(N, -1);
+        accumulate_group(c, g, bins, J, offs, N, rows, K, none.data(), out_slots, additions);
+        return;
+    }
+    if (additions) *additions += adds;
+    if (tree) {
+        for (size_t k = 0; k < G; ++k) {
+            sfxb_ctx *sh = c->shards[k];
+            sh->tree_cur ^= 1;
+            sh->tree_valid = true;
+            sh->tree_gh = g;
+            sh->tree_J = J;
+            sh->tree_K = K;
+            sh->tree_N = N;
+            sh->tree_G = (uint32_t)G;
+            sh->tree_j0 = (uint32_t)jlo[k];
+            sh->tree_jl = (uint32_t)(jlo[k + 1] - jlo[k]);
+        }
+        c->tree_derived_nodes += pairs.size();
+    }
+}
 
 } // namespace
 
@@ -959,9 +1459,87 @@ int sfxb_ctx_create(sfxb_ctx **out, int device, const uint32_t *n, uint32_t n_wo
     return SFXB_OK;
 }
 
+int sfxb_ctx_create_multi(sfxb_ctx **out, const int *devices, uint32_t n_devices, const uint32_t *n,
+                          uint32_t n_words, const uint32_t *p, const uint32_t *q, uint32_t pq_words) {
+    if (!out || !devices || n_devices == 0 || n_devices > (uint32_t)dev::kMaxShards) {
+        g_create_err = "sfxb_ctx_create_multi: bad arguments (1 to 16 devices)";
+        return SFXB_ERR_ARG;
+    }
+    if (n_devices == 1) return sfxb_ctx_create(out, devices[0], n, n_words, p, q, pq_words);
+    std::vector<sfxb_ctx *> sh(n_devices, nullptr);
+    auto undo = [&] {
+        for (sfxb_ctx *x : sh)
+            if (x) {
+                x->shards.clear();
+                sfxb_ctx_destroy(x);
+            }
+    };
+    for (uint32_t k = 0; k < n_devices; ++k) {
+        const int rc = sfxb_ctx_create(&sh[k], devices[k], n, n_words, p, q, pq_words);
+        if (rc != SFXB_OK) {
+            std::string e = g_create_err;
+            undo();
+            g_create_err = e;
+            return rc;
+        }
+    }
+    sfxb_ctx *c = sh[0];
+    const int rc = guard(c, [&] {
+        // the cross-shard reduce reads peer memory directly: every pair of
+        // distinct devices needs P2P access (NVLink / NVSwitch on a B200 box)
+        for (uint32_t i = 0; i < n_devices; ++i) {
+            CK(cudaSetDevice(devices[i]));
+            for (uint32_t j = 0; j < n_devices; ++j) {
+                if (devices[j] == devices[i]) continue;
+                int can = 0;
+                CK(cudaDeviceCanAccessPeer(&can, devices[i], devices[j]));
+                if (!can)
+                    throw ApiError(SFXB_ERR_UNSUPPORTED, "device group: no peer access from device " +
+                                                             std::to_string(devices[i]) + " to " +
+                                                             std::to_string(devices[j]));
+                const cudaError_t e = cudaDeviceEnablePeerAccess(devices[j], 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
+                else CK(e);
+            }
+            CK(cudaEventCreateWithFlags(&sh[i]->ev_part, cudaEventDisableTiming));
+        }
+        CK(cudaSetDevice(devices[0]));
+        c->shards = sh;
+    });
+    if (rc != SFXB_OK) {
+        g_create_err = c->err;
+        undo();
+        return rc;
+    }
+    *out = c;
+    return SFXB_OK;
+}
+
+int sfxb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+uint32_t sfxb_ctx_n_shards(const sfxb_ctx *c) { return c->shards.empty() ? 1u : (uint32_t)c->shards.size(); }
+int sfxb_ctx_shard_device(const sfxb_ctx *c, uint32_t k) {
+    if (c->shards.empty()) return k == 0 ? c->device : -1;
+    return k < c->shards.size() ? c->shards[k]->device : -1;
+}
+
 void sfxb_ctx_destroy(sfxb_ctx *c) {
     if (!c) return;
+    if (!c->shards.empty()) {
+        std::vector<sfxb_ctx *> sh;
+        sh.swap(c->shards);
+        for (size_t k = 1; k < sh.size(); ++k) sfxb_ctx_destroy(sh[k]);
+    }
     cudaSetDevice(c->device);
+    if (c->ev_part) cudaEventDestroy(c->ev_part);
+    free_hist_bufs(c);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (void *d : c->owned) cudaFree(d);
     if (c->scratch_table.p) cudaFree(c->scratch_table.p);
@@ -989,49 +1567,82 @@ uint32_t sfxb_ctx_n_words(const sfxb_ctx *c) { return c->nw; }
 uint32_t sfxb_ctx_ct_words(const sfxb_ctx *c) { return 2 * c->nw; }
 int sfxb_ctx_has_private(const sfxb_ctx *c) { return c->has_priv ? 1 : 0; }
 uint64_t sfxb_ctx_key_id(const sfxb_ctx *c) { return c->key_id; }
-uint64_t sfxb_ctx_launches(const sfxb_ctx *c) { return c->launches; }
-uint64_t sfxb_ctx_dec_derived(const sfxb_ctx *c) { return c->dec_derived; }
+uint64_t sfxb_ctx_launches(const sfxb_ctx *c) {
+    uint64_t t = c->launches;
+    for (size_t k = 1; k < c->shards.size(); ++k) t += c->shards[k]->launches;
+    return t;
+}
+uint64_t sfxb_ctx_dec_derived(const sfxb_ctx *c) {
+    uint64_t t = c->dec_derived;
+    for (size_t k = 1; k < c->shards.size(); ++k) t += c->shards[k]->dec_derived;
+    return t;
+}
 void *sfxb_ctx_stream(sfxb_ctx *c) { return (void *)c->stream; }
 int sfxb_ctx_profile(sfxb_ctx *c, int enable) {
     return guard(c, [&] {
-        CK(cudaStreamSynchronize(c->stream));
-        for (auto &p : c->prof) {
+        const size_t G = std::max<size_t>(1, c->shards.size());
+        for (size_t k = 0; k < G; ++k) {
+            sfxb_ctx *x = G > 1 ? c->shards[k] : c;
+            CK(cudaSetDevice(x->device));
+            CK(cudaStreamSynchronize(x->stream));
+            for (auto &p : x->prof) {
+                for (auto &e : p.ev) {
+                    cudaEventDestroy(e.first);
+                    cudaEventDestroy(e.second);
+                }
+                p = CtxState::Prof{};
+            }
+            x->profile = enable != 0;
+        }
+        CK(cudaSetDevice(c->device));
+    });
+}
+
+// kernel-family totals over the context (all shards of a device group: the
+// times are summed GPU time, not wall time)
+int sfxb_ctx_kernel_stats(sfxb_ctx *c, int family, uint64_t *launches, double *ms, uint64_t *modmuls) {
+    return guard(c, [&] {
+        if (family < 0 || family >= 4) throw ApiError(SFXB_ERR_ARG, "kernel family out of range");
+        const size_t G = std::max<size_t>(1, c->shards.size());
+        uint64_t nl = 0, mm = 0;
+        double t_ms = 0;
+        for (size_t k = 0; k < G; ++k) {
+            sfxb_ctx *x = G > 1 ? c->shards[k] : c;
+            CK(cudaSetDevice(x->device));
+            CK(cudaStreamSynchronize(x->stream));
+            auto &p = x->prof[family];
             for (auto &e : p.ev) {
+                float t = 0;
+                CK(cudaEventElapsedTime(&t, e.first, e.second));
+                p.ms_done += t;
                 cudaEventDestroy(e.first);
                 cudaEventDestroy(e.second);
             }
-            p = CtxState::Prof{};
+            p.ev.clear();
+            nl += p.launches;
+            t_ms += p.ms_done;
+            mm += p.modmuls;
         }
-        c->profile = enable != 0;
+        CK(cudaSetDevice(c->device));
+        if (launches) *launches = nl;
+        if (ms) *ms = t_ms;
+        if (modmuls) *modmuls = mm;
     });
-}
-
-int sfxb_ctx_kernel_stats(sfxb_ctx *c, int family, uint64_t *launches, double *ms, uint64_t *modmuls) {
-    int rc = sfxb_ctx_kernel_time(c, family, launches, ms);
-    if (rc == SFXB_OK && modmuls) *modmuls = c->prof[family].modmuls;
-    return rc;
 }
 
 int sfxb_ctx_kernel_time(sfxb_ctx *c, int family, uint64_t *launches, double *ms) {
-    return guard(c, [&] {
-        if (family < 0 || family >= 4) throw ApiError(SFXB_ERR_ARG, "kernel family out of range");
-        CK(cudaStreamSynchronize(c->stream));
-        auto &p = c->prof[family];
-        for (auto &e : p.ev) {
-            float t = 0;
-            CK(cudaEventElapsedTime(&t, e.first, e.second));
-            p.ms_done += t;
-            cudaEventDestroy(e.first);
-            cudaEventDestroy(e.second);
-        }
-        p.ev.clear();
-        *launches = p.launches;
-        *ms = p.ms_done;
-    });
+    return sfxb_ctx_kernel_stats(c, family, launches, ms, nullptr);
 }
 
 int sfxb_ctx_sync(sfxb_ctx *c) {
-    return guard(c, [&] { CK(cudaStreamSynchronize(c->stream)); });
+    return guard(c, [&] {
+        for (size_t k = 1; k < c->shards.size(); ++k) {
+            CK(cudaSetDevice(c->shards[k]->device));
+            CK(cudaStreamSynchronize(c->shards[k]->stream));
+        }
+        CK(cudaSetDevice(c->device));
+        CK(cudaStreamSynchronize(c->stream));
+    });
 }
 
 int sfxb_encode_check(sfxb_ctx *c, double x, uint32_t scale, int64_t *q_out) {
@@ -1057,73 +1668,27 @@ int sfxb_encrypt_dev(sfxb_ctx *c, const int64_t *d_q, const uint32_t *d_r, size_
     });
 }
 
-namespace {
-// sfxb_encrypt / sfxb_encrypt_plain: q_fixed xor m_words (count × n_words)
-void encrypt_host(sfxb_ctx *c, const int64_t *q_fixed, const uint32_t *m_words, const uint32_t *r, size_t count,
-                  uint32_t *out_cts, uint8_t *r_flags) {
-    CK(cudaSetDevice(c->device));
-    if (count == 0) return;
-    const size_t Sn = 2 * (size_t)c->s, S4 = 4 * (size_t)c->s;
-    // range checks of encrypt_with_r (he.cpp:88-89), in its order per element
-    for (size_t i = 0; i < count; ++i) {
-        if (m_words && host::cmp(host::from_words(m_words + i * c->nw, c->nw), c->n) >= 0)
-            throw ApiError(SFXB_ERR_RANGE, "encrypt: plaintext out of range [0, n)");
-        const uint32_t *ri = r + i * c->nw;
-        bool small = true;
-        for (uint32_t k = 1; k < c->nw; ++k) small &= ri[k] == 0;
-        if (small && ri[0] < 1) throw ApiError(SFXB_ERR_RANGE, "encrypt: blinding factor out of range");
-        if (host::cmp(host::from_words(ri, c->nw), c->n) >= 0)
-            throw ApiError(SFXB_ERR_RANGE, "encrypt: blinding factor out of range");
-    }
-    IoBuf<int64_t> dq(c->io[0], m_words ? 1 : count);
-    IoBuf<uint32_t> dr(c->io[1], count * Sn), dout(c->io[2], count * S4);
-    IoBuf<uint8_t> dflags(c->io[3], count);
-    IoBuf<uint32_t> dm(c->io[4], m_words ? count * Sn : 1);
-    CK(cudaMemsetAsync(dflags.p, 0, count, c->stream));
-    if (m_words) h2d_padded(c, dm.p, m_words, count, c->nw, Sn);
-    else CK(cudaMemcpyAsync(dq.p, q_fixed, count * 8, cudaMemcpyHostToDevice, c->stream));
-    h2d_padded(c, dr.p, r, count, c->nw, Sn);
-    int st = SFXB_OK;
-    try {
-        encrypt_dev(c, m_words ? nullptr : dq.p, dr.p, count, dout.p, dflags.p, m_words ? dm.p : nullptr);
-    } catch (const ApiError &e) {
-        if (e.code != SFXB_ERR_COPRIME) throw;
-        st = e.code;
-        c->err = e.what();
-    }
-    if (r_flags) {
-        CK(cudaMemcpyAsync(r_flags, dflags.p, count, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-    }
-    if (st != SFXB_OK) throw ApiError(st, c->err);
-    d2h_padded(c, out_cts, dout.p, count, 2 * c->nw, S4);
-}
-} // namespace
 
 int sfxb_encrypt(sfxb_ctx *c, const int64_t *q_fixed, const uint32_t *r, size_t count, uint32_t *out_cts,
                  uint8_t *r_flags) {
-    return guard(c, [&] { encrypt_host(c, q_fixed, nullptr, r, count, out_cts, r_flags); });
+    return guard(c, [&] {
+        if (is_group(c)) encrypt_group(c, q_fixed, nullptr, r, count, out_cts, r_flags);
+        else encrypt_host(c, q_fixed, nullptr, r, count, out_cts, r_flags);
+    });
 }
 
 int sfxb_encrypt_plain(sfxb_ctx *c, const uint32_t *m_words, const uint32_t *r, size_t count, uint32_t *out_cts,
                        uint8_t *r_flags) {
-    return guard(c, [&] { encrypt_host(c, nullptr, m_words, r, count, out_cts, r_flags); });
+    return guard(c, [&] {
+        if (is_group(c)) encrypt_group(c, nullptr, m_words, r, count, out_cts, r_flags);
+        else encrypt_host(c, nullptr, m_words, r, count, out_cts, r_flags);
+    });
 }
 
 int sfxb_add(sfxb_ctx *c, const uint32_t *a, const uint32_t *b, size_t count, uint32_t *out) {
     return guard(c, [&] {
-        CK(cudaSetDevice(c->device));
-        if (count == 0) return;
-        const size_t S4 = 4 * (size_t)c->s, cw = 2 * c->nw;
-        for (size_t i = 0; i < count; ++i)
-            if (host::cmp(host::from_words(a + i * cw, cw), c->n2) >= 0 ||
-                host::cmp(host::from_words(b + i * cw, cw), c->n2) >= 0)
-                throw ApiError(SFXB_ERR_RANGE, "add_ciphertexts: ciphertext out of range");
-        IoBuf<uint32_t> da(c->io[0], count * S4), db(c->io[1], count * S4), dout(c->io[2], count * S4);
-        h2d_padded(c, da.p, a, count, cw, S4);
-        h2d_padded(c, db.p, b, count, cw, S4);
-        add_dev(c, da.p, db.p, count, dout.p);
-        d2h_padded(c, out, dout.p, count, cw, S4);
+        if (is_group(c)) add_group(c, a, b, count, out);
+        else add_host(c, a, b, count, out);
     });
 }
 
@@ -1138,89 +1703,25 @@ int sfxb_decrypt_dev(sfxb_ctx *c, const uint32_t *d_cts, size_t count, uint32_t 
 int sfxb_decrypt_tree(sfxb_ctx *c, uint64_t tag, const uint32_t *cts, uint32_t n_nodes, uint32_t spn,
                       const int32_t *parent, uint32_t scale, double *out_values, uint64_t *decryptions) {
     return guard(c, [&] {
-        CK(cudaSetDevice(c->device));
-        if (!c->has_priv) throw ApiError(SFXB_ERR_AUTH, "decrypt requested without private key material");
-        const size_t count = (size_t)n_nodes * spn;
-        const size_t Sn = 2 * (size_t)c->s, S4 = 4 * (size_t)c->s;
-        CtxState::DecCache &prev = c->dec_cache[tag];
-        // sibling pairs (two children of one cached parent): b = second child
-        std::vector<uint32_t> pairs;
-        if (parent && prev.valid && prev.spn == spn) {
-            std::vector<std::vector<uint32_t>> kids(prev.n_nodes);
-            for (uint32_t i = 0; i < n_nodes; ++i)
-                if (parent[i] >= 0 && (uint32_t)parent[i] < prev.n_nodes) kids[parent[i]].push_back(i);
-            for (uint32_t pnode = 0; pnode < prev.n_nodes; ++pnode)
-                if (kids[pnode].size() == 2) {
-                    pairs.push_back(kids[pnode][1]);
-                    pairs.push_back(kids[pnode][0]);
-                    pairs.push_back(pnode);
-                }
-        }
-        const int nx = prev.cur ^ 1;
-        uint32_t *dc = (uint32_t *)grow(prev.cts[nx], count * S4 * 4 + 64);
-        uint32_t *dplain = (uint32_t *)grow(prev.plain[nx], count * Sn * 4 + 64);
-        IoBuf<double> dv(c->io[2], count ? count : 1);
-        if (count) h2d_padded(c, dc, cts, count, 2 * c->nw, S4);
-        uint8_t *skip = nullptr;
-        const size_t np = pairs.size() / 3;
-        uint32_t *dpairs = nullptr;
-        if (np) {
-            skip = (uint8_t *)grow(c->io[4], count + 64);
-            dpairs = (uint32_t *)grow(c->io[5], pairs.size() * 4 + 64);
-            CK(cudaMemsetAsync(skip, 0, count, c->stream));
-            CK(cudaMemcpyAsync(dpairs, pairs.data(), pairs.size() * 4, cudaMemcpyHostToDevice, c->stream));
-            dev::SibArgs sa{dc, (const uint32_t *)prev.cts[prev.cur].p, dpairs, np, spn, skip};
-            dispatch_class(c->s, [&](auto sc) {
-                constexpr int cs = decltype(sc)::value;
-                using C = Cls<cs>;
-                auto k = dev::k_sib_verify<4 * cs, C::TH>;
-                constexpr int NI = dev::kBlock / C::TH;
-                const int grid = occupancy_grid(*c, k, np * spn, NI);
-                k<<<grid, dev::kBlock, 0, c->stream>>>(arg(c->mod_n2), sa);
-                check_launch(*c);
-            });
-        }
-        if (count) decrypt_dev(c, dc, count, scale, dv.p, dplain, decryptions, skip);
-        if (np) {
-            dispatch_class(c->s, [&](auto sc) {
-                constexpr int cs = decltype(sc)::value;
-                const int grid = (int)std::min<size_t>((np * spn + 127) / 128, (size_t)c->sms * 8);
-                dev::k_sib_derive<2 * cs><<<grid, 128, 0, c->stream>>>(
-                    dpairs, np, spn, skip, dplain, (const uint32_t *)prev.plain[prev.cur].p, c->d_n, scale, dplain,
-                    dv.p);
-                check_launch(*c);
-            });
-        }
-        if (count) CK(cudaMemcpyAsync(out_values, dv.p, count * 8, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        // this level becomes the parent level of the tag
-        prev.cur = nx;
-        prev.n_nodes = n_nodes;
-        prev.spn = spn;
-        prev.valid = true;
+        if (is_group(c)) decrypt_tree_group(c, tag, cts, n_nodes, spn, parent, scale, out_values, decryptions);
+        else decrypt_tree_impl(c, tag, cts, n_nodes, spn, 0, spn, parent, scale, out_values, decryptions);
     });
 }
 
 int sfxb_decrypt(sfxb_ctx *c, const uint32_t *cts, size_t count, uint32_t scale, double *out_values,
                  uint32_t *out_plain, uint64_t *decryptions) {
     return guard(c, [&] {
-        CK(cudaSetDevice(c->device));
-        if (!c->has_priv) throw ApiError(SFXB_ERR_AUTH, "decrypt requested without private key material");
-        if (count == 0) return;
-        const size_t Sn = 2 * (size_t)c->s, S4 = 4 * (size_t)c->s;
-        IoBuf<uint32_t> dc(c->io[0], count * S4), dplain(c->io[1], out_plain ? count * Sn : 1);
-        IoBuf<double> dv(c->io[2], count);
-        h2d_padded(c, dc.p, cts, count, 2 * c->nw, S4);
-        decrypt_dev(c, dc.p, count, scale, dv.p, out_plain ? dplain.p : nullptr, decryptions);
-        CK(cudaMemcpyAsync(out_values, dv.p, count * 8, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        if (out_plain) d2h_padded(c, out_plain, dplain.p, count, c->nw, Sn);
+        if (is_group(c)) decrypt_group(c, cts, count, scale, out_values, out_plain, decryptions);
+        else decrypt_host(c, cts, count, scale, out_values, out_plain, decryptions);
     });
 }
 
-
 int sfxb_gh_upload(sfxb_ctx *c, const uint32_t *gh_cts, uint32_t n_samples, sfxb_gh **out) {
     return guard(c, [&] {
+        if (is_group(c)) {
+            *out = gh_upload_group(c, gh_cts, n_samples);
+            return;
+        }
         CK(cudaSetDevice(c->device));
         std::unique_ptr<sfxb_gh> g(gh_alloc(c, n_samples));
         const size_t S4 = 4 * (size_t)c->s;
@@ -1233,6 +1734,7 @@ int sfxb_gh_upload(sfxb_ctx *c, const uint32_t *gh_cts, uint32_t n_samples, sfxb
 
 int sfxb_gh_from_dev(sfxb_ctx *c, const uint32_t *d_gh, uint32_t n_samples, sfxb_gh **out) {
     return guard(c, [&] {
+        if (is_group(c)) throw ApiError(SFXB_ERR_UNSUPPORTED, "gh_from_dev: device-pointer entry points are single-device");
         CK(cudaSetDevice(c->device));
         std::unique_ptr<sfxb_gh> g(gh_alloc(c, n_samples));
         const size_t S4 = 4 * (size_t)c->s;
@@ -1247,6 +1749,13 @@ void sfxb_gh_free(sfxb_gh *g) {
     if (!g) return;
     sfxb_ctx *c = g->ctx;
     if (c->tree_gh == g) c->tree_valid = false;
+    if (!g->parts.empty()) { // device group: one handle per shard
+        for (sfxb_gh *p : g->parts)
+            if (p) sfxb_gh_free(p);
+        cudaSetDevice(c->device);
+        delete g;
+        return;
+    }
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     if (!c->spare_gh) { // keep as the context's spare
@@ -1265,6 +1774,8 @@ int sfxb_accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, u
                         const uint32_t *d_node_offsets, uint32_t n_nodes, const uint32_t *d_rows, uint32_t n_rows,
                         uint32_t n_bins, uint32_t *d_out, int mont_out, uint64_t *additions) {
     return guard(c, [&] {
+        if (g && !g->parts.empty())
+            throw ApiError(SFXB_ERR_UNSUPPORTED, "accumulate: device-pointer entry points take a single-device handle");
         CK(cudaSetDevice(c->device));
         accumulate_dev(c, g, d_bins, n_features, d_node_offsets, n_nodes, d_rows, n_rows, n_bins, d_out, mont_out,
                        additions);
@@ -1287,6 +1798,10 @@ int sfxb_accumulate(sfxb_ctx *c, const uint32_t *gh_cts, uint32_t n_samples, con
             if (rc != SFXB_OK) throw ApiError(rc, c->err);
             g.reset(gp);
         }
+        if (is_group(c)) {
+            accumulate_group(c, g.get(), bins, J, node_offsets, N, rows, K, nullptr, out_slots, additions);
+            return;
+        }
         const size_t S4 = 4 * (size_t)c->s, nslots = 2ull * N * J * K;
         IoBuf<uint16_t> db(c->io[0], (size_t)J * n_samples);
         IoBuf<uint32_t> doff(c->io[1], (size_t)N + 1), drows(c->io[2], R ? R : 1), dout(c->io[3], nslots * S4);
@@ -1307,6 +1822,10 @@ int sfxb_accumulate_gh(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *bins, uint
         for (uint32_t i = 0; i < N; ++i)
             if (node_offsets[i + 1] < node_offsets[i]) throw ApiError(SFXB_ERR_ARG, "accumulate: node offsets decrease");
         if (N && node_offsets[0] != 0) throw ApiError(SFXB_ERR_ARG, "accumulate: node offsets must start at 0");
+        if (is_group(c)) {
+            accumulate_group(c, g, bins, J, node_offsets, N, rows, K, nullptr, out_slots, additions);
+            return;
+        }
         const uint32_t R = N ? node_offsets[N] : 0;
         const size_t S4 = 4 * (size_t)c->s, nslots = 2ull * N * J * K, n_samples = g->n_samples;
         IoBuf<uint16_t> db(c->io[0], (size_t)J * n_samples);
@@ -1325,6 +1844,8 @@ int sfxb_accumulate_tree_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bi
                              const uint32_t *d_rows, uint32_t n_rows, uint32_t n_bins, const int32_t *h_parent,
                              uint32_t *d_out, int mont_out, uint64_t *additions) {
     return guard(c, [&] {
+        if (g && !g->parts.empty())
+            throw ApiError(SFXB_ERR_UNSUPPORTED, "accumulate: device-pointer entry points take a single-device handle");
         CK(cudaSetDevice(c->device));
         if (!h_parent) throw ApiError(SFXB_ERR_ARG, "accumulate_tree: parent indices required");
         accumulate_dev(c, g, d_bins, n_features, d_node_offsets, n_nodes, d_rows, n_rows, n_bins, d_out, mont_out,
@@ -1342,6 +1863,10 @@ int sfxb_accumulate_tree_gh(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *bins,
         for (uint32_t i = 0; i < N; ++i)
             if (node_offsets[i + 1] < node_offsets[i]) throw ApiError(SFXB_ERR_ARG, "accumulate: node offsets decrease");
         if (N && node_offsets[0] != 0) throw ApiError(SFXB_ERR_ARG, "accumulate: node offsets must start at 0");
+        if (is_group(c)) {
+            accumulate_group(c, g, bins, J, node_offsets, N, rows, K, parent, out_slots, additions);
+            return;
+        }
         const uint32_t R = N ? node_offsets[N] : 0;
         const size_t S4 = 4 * (size_t)c->s, nslots = 2ull * N * J * K, n_samples = g->n_samples;
         IoBuf<uint16_t> db(c->io[0], (size_t)J * n_samples);
@@ -1358,7 +1883,10 @@ int sfxb_accumulate_tree_gh(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *bins,
 uint64_t sfxb_ctx_tree_derived(const sfxb_ctx *c) { return c->tree_derived_nodes; }
 
 int sfxb_tree_reset(sfxb_ctx *c) {
-    return guard(c, [&] { c->tree_valid = false; });
+    return guard(c, [&] {
+        c->tree_valid = false;
+        for (sfxb_ctx *x : c->shards) x->tree_valid = false;
+    });
 }
 
 int sfxb_reduce_partials_dev(sfxb_ctx *c, const uint32_t *d_parts, uint32_t parts, size_t n_slots, uint32_t *d_out) {

@@ -144,12 +144,12 @@ public:
     ~CudaPaillierPlugin() override {
         if (std::getenv("SFXB_PLUGIN_VERBOSE") && ctx_)
             std::fprintf(stderr, "[sfxb-cuda-plugin] key=%016llx enc=%llu adds=%llu dec=%llu derived_nodes=%llu "
-                         "derived_slots=%llu launches=%llu\n",
+                         "derived_slots=%llu launches=%llu shards=%u\n",
                          (unsigned long long)pub_.key_id, (unsigned long long)counters_.encryptions,
                          (unsigned long long)counters_.ciphertext_additions,
                          (unsigned long long)counters_.decryptions,
                          (unsigned long long)sfxb_ctx_tree_derived(ctx_), (unsigned long long)sfxb_ctx_dec_derived(ctx_),
-                         (unsigned long long)sfxb_ctx_launches(ctx_));
+                         (unsigned long long)sfxb_ctx_launches(ctx_), sfxb_ctx_n_shards(ctx_));
         if (gh_) sfxb_gh_free(gh_);
         if (ctx_) sfxb_ctx_destroy(ctx_);
         gmp_randclear(rng_);
@@ -472,8 +472,31 @@ public:
     }
 
 private:
+    // SFXB_CUDA_DEVICES="0,1,...,7" spreads the plugin over a device group
+    // (sfxb_ctx_create_multi: row-sharded histograms, element-sharded
+    // encrypt/decrypt); "all" = every visible GPU.  Otherwise one device,
+    // SFXB_CUDA_DEVICE (default 0).
+    static std::vector<int> devices_from_env() {
+        std::vector<int> devs;
+        const char *e = std::getenv("SFXB_CUDA_DEVICES");
+        if (e && std::string(e) == "all") {
+            for (int i = 0, n = sfxb_device_count(); i < n; ++i) devs.push_back(i);
+        } else if (e && *e) {
+            std::string s(e);
+            size_t pos = 0;
+            while (pos <= s.size()) {
+                size_t end = s.find(',', pos);
+                if (end == std::string::npos) end = s.size();
+                if (end > pos) devs.push_back(std::atoi(s.substr(pos, end - pos).c_str()));
+                pos = end + 1;
+            }
+        }
+        if (devs.empty()) devs.push_back(std::getenv("SFXB_CUDA_DEVICE") ? std::atoi(std::getenv("SFXB_CUDA_DEVICE")) : 0);
+        return devs;
+    }
+
     void open_ctx(const PaillierKeypair *kp) {
-        const int dev = std::getenv("SFXB_CUDA_DEVICE") ? std::atoi(std::getenv("SFXB_CUDA_DEVICE")) : 0;
+        const std::vector<int> devs = devices_from_env();
         n_words_ = (mpz_sizeinbase(pub_.n.get_mpz_t(), 2) + 31) / 32;
         std::vector<uint32_t> n(n_words_);
         to_words(pub_.n, n.data(), n_words_);
@@ -483,9 +506,11 @@ private:
             std::vector<uint32_t> p(pw), q(pw);
             to_words(kp->priv.p, p.data(), pw);
             to_words(kp->priv.q, q.data(), pw);
-            rc = sfxb_ctx_create(&ctx_, dev, n.data(), (uint32_t)n_words_, p.data(), q.data(), (uint32_t)pw);
+            rc = sfxb_ctx_create_multi(&ctx_, devs.data(), (uint32_t)devs.size(), n.data(), (uint32_t)n_words_,
+                                       p.data(), q.data(), (uint32_t)pw);
         } else {
-            rc = sfxb_ctx_create(&ctx_, dev, n.data(), (uint32_t)n_words_, nullptr, nullptr, 0);
+            rc = sfxb_ctx_create_multi(&ctx_, devs.data(), (uint32_t)devs.size(), n.data(), (uint32_t)n_words_,
+                                       nullptr, nullptr, 0);
         }
         if (rc != SFXB_OK) throw Error(std::string("CUDA Paillier plugin: ") + sfxb_create_error());
         ct_words_ = sfxb_ctx_ct_words(ctx_);

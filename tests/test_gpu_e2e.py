@@ -25,11 +25,13 @@ def _need(path):
         pytest.skip(f"{path} not built (built in the dev container, travels with the repo)")
 
 
-def _train_with_plugin(name):
+def _train_with_plugin(name, devices=None):
     from make_golden import TRAIN_CONFIGS
 
     ini, bits, seed = TRAIN_CONFIGS[name]
     env = dict(os.environ, LD_PRELOAD=PLUGIN, SFXB_PLUGIN_VERBOSE="1")
+    if devices:
+        env["SFXB_CUDA_DEVICES"] = devices
     out = subprocess.run([sys.executable, os.path.join(HERE, "train_driver.py"), os.path.join(HERE, "configs", ini),
                           str(bits), str(seed)], env=env, capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stderr[-2000:]
@@ -61,6 +63,24 @@ def test_reference_training_loop_with_gpu_plugin(name):
     assert got["counters"] == want["counters"]
     assert got["transcript_bytes"] == want["transcript_bytes"]
     assert got["transcript_fnv"] == want["transcript_fnv"]
+
+
+@pytest.mark.parametrize("name", ["vertical_c1_1024", "vertical_threaded_3p"])
+def test_training_loop_with_device_group_plugin(name):
+    """The same drop-in run with every plugin spread over a device group
+    (SFXB_CUDA_DEVICES; sfxb_ctx_create_multi).  One GPU here, so the group
+    repeats device 0 with 3 shards: row-sharded histograms reduced across
+    shards, element-sharded encrypt/decrypt, sliced decrypt_tree."""
+    _need(PLUGIN)
+    _need(os.path.join(REF, "libsfxb_refcapi.so"))
+    gpath = os.path.join(HERE, "golden", f"train_{name}.json")
+    _need(gpath)
+    want = json.load(open(gpath))
+    got, stats = _train_with_plugin(name, devices="0,0,0")
+    assert stats and all("shards=3" in s for s in stats)
+    assert sum(int(s.split("derived_nodes=")[1].split()[0]) for s in stats) > 0
+    for k in ("forest", "partials", "counters", "transcript_bytes", "transcript_fnv"):
+        assert got[k] == want[k], k
 
 
 @pytest.mark.parametrize("suite", ["test_processor", "test_federation"])
