@@ -93,7 +93,13 @@ struct CtxState {
     };
     std::map<uint64_t, DecCache> dec_cache;
     uint64_t dec_derived = 0;         // slots decrypted by verified sibling reuse
-    uint64_t mm_dec = 0, mm_enc = 0; // per-item multiplications mod p² (CRT decrypt / encrypt)
+    // per-item 32×32 products of the CRT exponentiations (profiling units of
+    // kernel families 1 and 2)
+    uint64_t prod_dec = 0, prod_enc = 0;
+    // mod-p² exponentiations on base-p digits (padic.cuh): both primes fill
+    // their size class (p > 2^(32s−1)); otherwise the CIOS mod-p² kernels
+    bool p2_digits = false;
+    uint32_t *d_cdec[2] = {nullptr, nullptr}; // h_p·R⁻¹ mod p, h_q·R⁻¹ mod q   (s)
 
     // scratch (grown on demand, freed with the context)
     Buf scratch_table, tmp[4], host_pinned[2], io[6]; // io: host-API staging (grow-only)

@@ -170,8 +170,9 @@ __device__ __forceinline__ void store_b(uint2 *sB, int NI, int inst, const uint3
 
 // One CIOS step for limb pair (b_lo at iteration i, b_hi at i+1) is written
 // as two calls of `step` with the E/O roles swapped.
+// Returns q_i (the Montgomery quotient digit of this step).
 template <int L, int TPI>
-__device__ __forceinline__ void cios_step(uint32_t (&E)[L], uint32_t (&Q)[L], uint32_t &Z,
+__device__ __forceinline__ uint32_t cios_step(uint32_t (&E)[L], uint32_t (&Q)[L], uint32_t &Z,
                                           const uint32_t (&A)[L], const uint32_t (&N)[L],
                                           uint32_t bi, uint32_t np, bool first) {
     const int t = inst_lane<TPI>();
@@ -219,6 +220,7 @@ __device__ __forceinline__ void cios_step(uint32_t (&E)[L], uint32_t (&Q)[L], ui
     for (int k = 1; k < L / 2; ++k) madc_w_cc(E[2 * k], E[2 * k + 1], N[2 * k], q, E[2 * k], E[2 * k + 1]);
     Q[L - 1] = addc_cc(Q[L - 1], 0u);
     Z = addc(Zn, 0u);
+    return q;
 }
 
 // Carry-lookahead across the instance's lanes: lane t adds 1 if a carry
@@ -246,8 +248,9 @@ __device__ __forceinline__ uint32_t resolve_carries(uint32_t (&R)[L], uint32_t g
 }
 
 // Canonicalise: V = R + over·2^(32S) with V < 2M; return V mod M in R.
+// Returns whether M was subtracted (instance-uniform).
 template <int L, int TPI>
-__device__ __forceinline__ void final_sub(uint32_t (&R)[L], uint32_t over, const uint32_t (&N)[L]) {
+__device__ __forceinline__ bool final_sub(uint32_t (&R)[L], uint32_t over, const uint32_t (&N)[L]) {
     uint32_t D[L];
     D[0] = sub_cc(R[0], N[0]);
 #pragma unroll
@@ -275,6 +278,41 @@ __device__ __forceinline__ void final_sub(uint32_t (&R)[L], uint32_t over, const
     const bool ge = over != 0 || top_borrow == 0;
 #pragma unroll
     for (int k = 0; k < L; ++k) R[k] = ge ? D[k] : R[k];
+    return ge;
+}
+
+// The end of a CIOS pass: after the last step E = Y (the old even array,
+// still unshifted) and X holds the odd-aligned array, which becomes the
+// even-aligned window; Y shifts down one limb: window limb k = X[k] + Y[k+1]
+// (+ lane t+1's Y[0]).  Then carries across lanes and the final conditional
+// subtraction; returns whether M was subtracted.
+template <int L, int TPI>
+__device__ __forceinline__ bool mont_tail(uint32_t (&r)[L], const uint32_t (&X)[L], const uint32_t (&Y)[L],
+                                          uint32_t Z, const uint32_t (&N)[L]) {
+    const uint32_t u0 = from_above<TPI>(Y[0]);
+    uint32_t R[L];
+    R[0] = add_cc(X[0], Y[1]);
+#pragma unroll
+    for (int k = 1; k < L - 1; ++k) R[k] = addc_cc(X[k], Y[k + 1]);
+    R[L - 1] = addc_cc(X[L - 1], u0);
+    uint32_t C = addc(Z, 0u); // carry word at position t·L+L (into lane t+1)
+    uint32_t over;
+    if constexpr (TPI == 1) {
+        over = C;
+    } else {
+        const uint32_t cin = from_below<TPI>(C);
+        const uint32_t ctop = inst_bcast<TPI>(C, TPI - 1);
+        R[0] = add_cc(R[0], cin);
+#pragma unroll
+        for (int k = 1; k < L; ++k) R[k] = addc_cc(R[k], 0u);
+        uint32_t c2 = addc(0u, 0u);
+        uint32_t ripple = resolve_carries<L, TPI>(R, c2);
+        over = ctop + ripple;
+    }
+    const bool ge = final_sub<L, TPI>(R, over, N);
+#pragma unroll
+    for (int k = 0; k < L; ++k) r[k] = R[k];
+    return ge;
 }
 
 // r = A·B·2^(−32S) mod M.  A, N: this lane's L limbs; B: instance operand in
@@ -301,32 +339,34 @@ __device__ __forceinline__ void mont_mul(uint32_t (&r)[S / TPI], const uint32_t 
         cios_step<L, TPI>(X, Y, Z, A, N, b.x, np, false);
         cios_step<L, TPI>(Y, X, Z, A, N, b.y, np, false);
     }
-    // After the last step E = Y (the old even array, still unshifted) and X
-    // holds the odd-aligned array, which becomes the even-aligned window; Y
-    // shifts down one limb: window limb k = X[k] + Y[k+1] (+ lane t+1's Y[0]).
-    const uint32_t u0 = from_above<TPI>(Y[0]);
-    uint32_t R[L];
-    R[0] = add_cc(X[0], Y[1]);
+    mont_tail<L, TPI>(r, X, Y, Z, N);
+}
+
+// mont_mul that also returns the quotient m = Σ q_i·2^(32i) of the pass
+// (lane t receives limbs [t·L, t·L+L) in Mq) and whether the final
+// subtraction happened:  A·B = (r + ge·M)·2^(32S) − m·M  exactly.
+template <int S, int TPI>
+__device__ __forceinline__ bool mont_mul_m(uint32_t (&r)[S / TPI], uint32_t (&Mq)[S / TPI],
+                                           const uint32_t (&A)[S / TPI], const uint2 *sB, int inst,
+                                           const uint32_t (&N)[S / TPI], uint32_t np) {
+    constexpr int L = S / TPI, NIc = 128 / TPI;
+    const int t = inst_lane<TPI>();
+    uint32_t X[L], Y[L], Z = 0;
 #pragma unroll
-    for (int k = 1; k < L - 1; ++k) R[k] = addc_cc(X[k], Y[k + 1]);
-    R[L - 1] = addc_cc(X[L - 1], u0);
-    uint32_t C = addc(Z, 0u); // carry word at position t·L+L (into lane t+1)
-    uint32_t over;
-    if constexpr (TPI == 1) {
-        over = C;
-    } else {
-        const uint32_t cin = from_below<TPI>(C);
-        const uint32_t ctop = inst_bcast<TPI>(C, TPI - 1);
-        R[0] = add_cc(R[0], cin);
+    for (int k = 0; k < L; ++k) X[k] = Y[k] = 0;
+    for (int tr = 0; tr < TPI; ++tr) {
 #pragma unroll
-        for (int k = 1; k < L; ++k) R[k] = addc_cc(R[k], 0u);
-        uint32_t c2 = addc(0u, 0u);
-        uint32_t ripple = resolve_carries<L, TPI>(R, c2);
-        over = ctop + ripple;
+        for (int j = 0; j < L / 2; ++j) {
+            const uint2 b = sB[b_slot<NIc>(tr * (L / 2) + j, inst)];
+            const uint32_t q0 = cios_step<L, TPI>(X, Y, Z, A, N, b.x, np, false);
+            const uint32_t q1 = cios_step<L, TPI>(Y, X, Z, A, N, b.y, np, false);
+            if (tr == t) {
+                Mq[2 * j] = q0;
+                Mq[2 * j + 1] = q1;
+            }
+        }
     }
-    final_sub<L, TPI>(R, over, N);
-#pragma unroll
-    for (int k = 0; k < L; ++k) r[k] = R[k];
+    return mont_tail<L, TPI>(r, X, Y, Z, N);
 }
 
 // ---------------------------------------------------------------- global <-> lane limbs

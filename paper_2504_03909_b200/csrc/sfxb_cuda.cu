@@ -19,6 +19,7 @@
 #include "ctx.hpp"
 #include "hist.cuh"
 #include "kernels.cuh"
+#include "padic.cuh"
 
 #include <cub/cub.cuh>
 
@@ -187,17 +188,19 @@ dev::ModArg arg(const DevMod &m) { return dev::ModArg{m.w, m.np}; }
 // modulus of that kernel: step1 s, step2 2s, histogram / ct-add 4s.
 template <int s>
 struct Cls;
+// TP: p2_pow (mod-p² exponentiation on base-p digits, S = s); TQ: its
+// mod-p² pre/post conversions (S = 2s)
 template <>
 struct Cls<4> {
-    static constexpr int T1 = 1, T2 = 1, TC = 1, TD = 1, TE = 1, TH = 1, TN = 1;
+    static constexpr int T1 = 1, T2 = 1, TC = 1, TD = 1, TE = 1, TH = 1, TN = 1, TP = 1, TQ = 1;
 };
 template <>
 struct Cls<8> {
-    static constexpr int T1 = 1, T2 = 1, TC = 2, TD = 1, TE = 1, TH = 2, TN = 2;
+    static constexpr int T1 = 1, T2 = 1, TC = 2, TD = 1, TE = 1, TH = 2, TN = 2, TP = 1, TQ = 2;
 };
 template <>
 struct Cls<16> {
-    static constexpr int T1 = 1, T2 = 2, TC = 4, TD = 2, TE = 2, TH = 4, TN = 4;
+    static constexpr int T1 = 1, T2 = 2, TC = 4, TD = 2, TE = 2, TH = 4, TN = 4, TP = 2, TQ = 4;
 };
 #ifndef SFXB_T1_32
 #define SFXB_T1_32 1
@@ -211,13 +214,17 @@ struct Cls<16> {
 #ifndef SFXB_TH_32
 #define SFXB_TH_32 4
 #endif
+#ifndef SFXB_TP_32
+#define SFXB_TP_32 2
+#endif
 template <>
 struct Cls<32> { // 2048-bit keys (tuned on B200, profiles/)
-    static constexpr int T1 = SFXB_T1_32, T2 = SFXB_T2_32, TC = 8, TD = SFXB_TD_32, TE = 4, TH = SFXB_TH_32, TN = 8;
+    static constexpr int T1 = SFXB_T1_32, T2 = SFXB_T2_32, TC = 8, TD = SFXB_TD_32, TE = 4, TH = SFXB_TH_32, TN = 8,
+                         TP = SFXB_TP_32, TQ = 4;
 };
 template <>
 struct Cls<48> {
-    static constexpr int T1 = 2, T2 = 4, TC = 8, TD = 4, TE = 8, TH = 8, TN = 8;
+    static constexpr int T1 = 2, T2 = 4, TC = 8, TD = 4, TE = 8, TH = 8, TN = 8, TP = 4, TQ = 8;
 };
 
 // grid.x for `items` work items spread over `rows` block rows (grid.y)
@@ -316,11 +323,40 @@ void encrypt_dev(sfxb_ctx *c, const int64_t *d_q, const uint32_t *d_r, size_t co
                 constexpr int NI = dev::kBlock / C::T1;
                 int grid = occupancy_grid(*c, k, 2 * count, NI, 2);
                 a.scratch = (uint32_t *)grow(c->scratch_table, 2 * (size_t)grid * NI * ((size_t)cs << kWindow) * 4);
-                ProfScope prof_(*c, 1, c->mm_enc * count);
+                ProfScope prof_(*c, 1, c->prod_enc * count);
                 k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(a);
                 check_launch(*c);
             }
-            {
+            if (c->p2_digits) {
+                // y = x^prime mod prime² on base-prime digits (padic.cuh), then plain
+                dev::P2Args pa{};
+                for (int i = 0; i < 2; ++i) {
+                    pa.mod_p[i] = arg(c->mod_pq[i]);
+                    pa.pinv[i] = c->d_pinv[i];
+                    pa.dig[i] = c->d_dig_pq[i];
+                    pa.nd[i] = c->nd_pq[i];
+                }
+                pa.in = a.x;
+                pa.out = a.y;
+                pa.count = count;
+                {
+                    auto k = dev::k_p2_pow<cs, C::TP, kWindow, 0>;
+                    constexpr int NI = dev::kBlock / C::TP;
+                    int grid = occupancy_grid(*c, k, 2 * count, NI, 2);
+                    pa.scratch = (uint32_t *)grow(c->scratch_table,
+                                                  2 * (size_t)grid * NI * ((size_t)(2 * cs) << kWindow) * 4);
+                    ProfScope prof_(*c, 1);
+                    k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(pa);
+                    check_launch(*c);
+                }
+                {
+                    auto k = dev::k_enc_post<cs, C::TQ>;
+                    constexpr int NI = dev::kBlock / C::TQ;
+                    int grid = occupancy_grid(*c, k, 2 * count, NI, 2);
+                    k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(a);
+                    check_launch(*c);
+                }
+            } else {
                 auto k = dev::k_enc_step2<2 * cs, C::T2, kWindow>;
                 constexpr int NI = dev::kBlock / C::T2;
                 int grid = occupancy_grid(*c, k, 2 * count, NI, 2);
@@ -403,12 +439,42 @@ void decrypt_dev(sfxb_ctx *c, const uint32_t *d_cts, size_t count, uint32_t scal
         if (decryptions) *decryptions += (uint64_t)n_items + hst[2];
         c->dec_derived += hst[2];
         if (n_items == 0) return;
-        {
+        if (c->p2_digits) {
+            // X̃ = c·R² mod prime², then c^(prime−1) on base-prime digits -> m_prime
+            uint32_t *xt = (uint32_t *)grow(c->tmp[1], (size_t)n_items * 2 * (2 * cs) * 4 + 64);
+            ProfScope prof_(*c, 2, c->prod_dec * n_items);
+            {
+                auto k = dev::k_dec_pre<cs, C::TQ>;
+                constexpr int NI = dev::kBlock / C::TQ;
+                int grid = occupancy_grid(*c, k, 2 * (size_t)n_items, NI, 2);
+                k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(a, n_items, xt);
+                check_launch(*c);
+            }
+            dev::P2Args pa{};
+            for (int i = 0; i < 2; ++i) {
+                pa.mod_p[i] = arg(c->mod_pq[i]);
+                pa.pinv[i] = c->d_pinv[i];
+                pa.cdec[i] = c->d_cdec[i];
+                pa.dig[i] = c->d_dig_m1[i];
+                pa.nd[i] = c->nd_m1[i];
+            }
+            pa.in = xt;
+            pa.out = a.mpq;
+            pa.idx = a.idx;
+            pa.count = n_items;
+            pa.status = a.status;
+            auto k = dev::k_p2_pow<cs, C::TP, kWindow, 1>;
+            constexpr int NI = dev::kBlock / C::TP;
+            int grid = occupancy_grid(*c, k, 2 * (size_t)n_items, NI, 2);
+            pa.scratch = (uint32_t *)grow(c->scratch_table, 2 * (size_t)grid * NI * ((size_t)(2 * cs) << kWindow) * 4);
+            k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(pa);
+            check_launch(*c);
+        } else {
             auto k = dev::k_dec_step<cs, C::TD, kWindow>;
             constexpr int NI = dev::kBlock / C::TD;
             int grid = occupancy_grid(*c, k, 2 * (size_t)n_items, NI, 2);
             a.scratch = (uint32_t *)grow(c->scratch_table, 2 * (size_t)grid * NI * ((size_t)(2 * cs) << kWindow) * 4);
-            ProfScope prof_(*c, 2, c->mm_dec * n_items);
+            ProfScope prof_(*c, 2, c->prod_dec * n_items);
             k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(a, n_items);
             check_launch(*c);
         }
@@ -1417,6 +1483,11 @@ int sfxb_ctx_create(sfxb_ctx **out, int device, const uint32_t *n, uint32_t n_wo
             c->p = P;
             c->q = Q;
             const Big PQ[2] = {P, Q};
+            struct Win {
+                uint64_t e1, pr, pm1;
+                std::vector<uint8_t> dig_pr, dig_pm1;
+            } host_window[2];
+            c->p2_digits = host::bit_length(P) == 32u * s && host::bit_length(Q) == 32u * s;
             for (int i = 0; i < 2; ++i) {
                 const Big &pr = PQ[i], &ot = PQ[1 - i];
                 Big pr2 = host::mul(pr, pr);
@@ -1427,14 +1498,29 @@ int sfxb_ctx_create(sfxb_ctx **out, int device, const uint32_t *n, uint32_t n_wo
                 c->d_dig_pq[i] = dev_digits(*c, pr, kWindow, c->nd_pq[i]);
                 c->d_dig_m1[i] = dev_digits(*c, pm1, kWindow, c->nd_m1[i]);
                 // profiling units: multiplications mod p² (step 1 runs mod p: 1/4 of the products)
-                c->mm_dec += pow_mmuls(pm1, kWindow);
-                c->mm_enc += pow_mmuls(host::mod(ot, pm1), kWindow) / 4 + pow_mmuls(pr, kWindow);
+                host_window[i] = {pow_mmuls(host::mod(ot, pm1), kWindow), pow_mmuls(pr, kWindow),
+                                  pow_mmuls(pm1, kWindow), host::window_digits(pr, kWindow),
+                                  host::window_digits(pm1, kWindow)};
                 c->d_pinv[i] = dev_big(*c, host::inv_pow2(pr, s), s);
                 // h = (−other mod prime)^-1 mod prime, in Montgomery form
                 Big negot = host::sub(pr, host::mod(ot, pr));
                 Big h = host::inv_mod_prime(negot, pr, s);
                 host::MontHost mp(pr, s);
                 c->d_hR[i] = dev_big(*c, mp.to_mont(h), s);
+                c->d_cdec[i] = dev_big(*c, mp.from_mont(h), s);
+            }
+            // profiling units: 32×32 products per item of the exponentiation kernels
+            const uint64_t pp = 2ull * s * s + s, pp2 = 2ull * (2 * s) * (2 * s) + 2 * s;
+            for (int i = 0; i < 2; ++i) {
+                const Win &w = host_window[i];
+                c->prod_enc += w.e1 * pp; // step 1 mod p
+                if (c->p2_digits) {
+                    c->prod_enc += (dev::p2_pow_passes(w.dig_pr.data(), (int)w.dig_pr.size(), kWindow) + 2) * pp;
+                    c->prod_dec += (dev::p2_pow_passes(w.dig_pm1.data(), (int)w.dig_pm1.size(), kWindow) + 2) * pp;
+                } else {
+                    c->prod_enc += w.pr * pp2;
+                    c->prod_dec += w.pm1 * pp2;
+                }
             }
             host::MontHost mp(P, s), mp2(host::mul(P, P), 2 * s), mn(N, 2 * s);
             Big P2 = host::mul(P, P), Q2 = host::mul(Q, Q);
