@@ -295,5 +295,53 @@ inline std::vector<uint8_t> window_digits(const Big &e, int w) {
     return d;
 }
 
+// Sliding-window program of e (e > 0), window ≤ w bits: byte pairs
+// (squarings, odd digit d) — the first pair starts the accumulator at x^d,
+// every later pair squares `squarings` times and then multiplies by x^d
+// (d == 0: squarings only).  Uses the table of odd powers x^1, x^3, …,
+// x^(2^w − 1).
+inline std::vector<uint8_t> sliding_ops(const Big &e, int w) {
+    std::vector<uint8_t> ops;
+    long i = (long)bit_length(e) - 1;
+    if (i < 0) return {0, 0};
+    bool first = true;
+    unsigned pend = 0; // squarings not emitted yet
+    while (i >= 0) {
+        if (!bit(e, (size_t)i)) {
+            ++pend;
+            --i;
+            continue;
+        }
+        long lo = std::max<long>(i - w + 1, 0);
+        while (!bit(e, (size_t)lo)) ++lo; // window ends in a 1
+        uint32_t d = 0;
+        for (long k = i; k >= lo; --k) d = (d << 1) | (uint32_t)bit(e, (size_t)k);
+        const unsigned len = (unsigned)(i - lo + 1);
+        if (first) {
+            ops.push_back(0);
+            ops.push_back((uint8_t)d);
+            first = false;
+        } else {
+            pend += len;
+            while (pend > 255) {
+                ops.push_back(255);
+                ops.push_back(0);
+                pend -= 255;
+            }
+            ops.push_back((uint8_t)pend);
+            ops.push_back((uint8_t)d);
+        }
+        pend = 0;
+        i = lo - 1;
+    }
+    while (pend > 0) {
+        const unsigned k = std::min(pend, 255u);
+        ops.push_back((uint8_t)k);
+        ops.push_back(0);
+        pend -= k;
+    }
+    return ops;
+}
+
 } // namespace host
 } // namespace sfxb

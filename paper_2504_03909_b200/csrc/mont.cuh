@@ -345,10 +345,12 @@ __device__ __forceinline__ void mont_mul(uint32_t (&r)[S / TPI], const uint32_t 
 // mont_mul that also returns the quotient m = Σ q_i·2^(32i) of the pass
 // (lane t receives limbs [t·L, t·L+L) in Mq) and whether the final
 // subtraction happened:  A·B = (r + ge·M)·2^(32S) − m·M  exactly.
+// With capture == false, Mq is left untouched (one call site can serve
+// passes with and without the quotient).
 template <int S, int TPI>
 __device__ __forceinline__ bool mont_mul_m(uint32_t (&r)[S / TPI], uint32_t (&Mq)[S / TPI],
                                            const uint32_t (&A)[S / TPI], const uint2 *sB, int inst,
-                                           const uint32_t (&N)[S / TPI], uint32_t np) {
+                                           const uint32_t (&N)[S / TPI], uint32_t np, bool capture = true) {
     constexpr int L = S / TPI, NIc = 128 / TPI;
     const int t = inst_lane<TPI>();
     uint32_t X[L], Y[L], Z = 0;
@@ -360,7 +362,7 @@ __device__ __forceinline__ bool mont_mul_m(uint32_t (&r)[S / TPI], uint32_t (&Mq
             const uint2 b = sB[b_slot<NIc>(tr * (L / 2) + j, inst)];
             const uint32_t q0 = cios_step<L, TPI>(X, Y, Z, A, N, b.x, np, false);
             const uint32_t q1 = cios_step<L, TPI>(Y, X, Z, A, N, b.y, np, false);
-            if (tr == t) {
+            if (capture && tr == t) {
                 Mq[2 * j] = q0;
                 Mq[2 * j + 1] = q1;
             }

@@ -30,115 +30,128 @@ __device__ __forceinline__ void stage_regs(const Stage &st, const uint32_t (&v)[
 }
 
 // One Montgomery product mod p² on digits: (A, B) <- (A, B) ⊛ (A2, B2),
-// or the square when `square` (A2, B2 unused).  Op counts: 2 or 3 CIOS passes
-// through ONE inlined mont_mul_m call site (the hot loop stays one copy of
-// the unrolled CIOS body).
+// or the square when `square` (A2, B2 unused).  2 or 3 CIOS passes through
+// ONE inlined mont_mul_m call site (the hot loop stays one copy of the
+// unrolled CIOS body):
+//   pass 0: v = MM(A, B | B2)
+//   pass 1: t, m, ge = MM_m(A, A | A2);  A <- t (A is not needed any more)
+//   pass 2: v += MM(B, A2)                   (multiply only)
+// then B <- (1 + square)·v + ge·R − m (mod p).  `Rmod` = R mod p (global).
 template <int s, int TPI>
 __device__ __forceinline__ void p2_mul(uint32_t (&A)[s / TPI], uint32_t (&B)[s / TPI], const uint32_t *g2,
                                        bool square, const Stage &st, const uint32_t (&N)[s / TPI], uint32_t np,
-                                       const uint32_t (&Rp)[s / TPI]) {
+                                       const uint32_t *Rmod) {
     constexpr int L = s / TPI;
-    uint32_t t[L], m[L], v1[L], tmp[L], x[L];
+    uint32_t m[L], v[L], x[L];
     bool ge = false;
     const int passes = square ? 2 : 3;
 #pragma unroll 1
     for (int c = 0; c < passes; ++c) {
-        // pass 0: A·(A | A2) -> t, m, ge;  pass 1: A·(B | B2) -> v1;  pass 2: B·A2 -> v2
+        {
+            uint32_t tmp[L];
+            if (square) {
+#pragma unroll
+                for (int k = 0; k < L; ++k) tmp[k] = c == 0 ? B[k] : A[k];
+            } else {
+                load_lane<s, TPI>(tmp, g2 + (c == 0 ? s : 0)); // B2 for pass 0, A2 for passes 1/2
+            }
+            stage_b<s, TPI>(st, tmp);
+        }
 #pragma unroll
         for (int k = 0; k < L; ++k) x[k] = c == 2 ? B[k] : A[k];
-        if (c == 1 && square) {
-#pragma unroll
-            for (int k = 0; k < L; ++k) tmp[k] = B[k];
-        } else if (c == 0 && square) {
-#pragma unroll
-            for (int k = 0; k < L; ++k) tmp[k] = A[k];
-        } else {
-            load_lane<s, TPI>(tmp, g2 + (c == 1 ? s : 0)); // A2 for passes 0/2, B2 for pass 1
-        }
-        stage_regs<s, TPI>(st, tmp);
-        uint32_t r[L], q[L];
-        const bool g = mont_mul_m<s, TPI>(r, q, x, st.sB, st.inst, N, np);
+        uint32_t r[L];
+        const bool g = mont_mul_m<s, TPI>(r, m, x, st.sB, st.inst, N, np, c == 1);
         if (c == 0) {
+#pragma unroll
+            for (int k = 0; k < L; ++k) v[k] = r[k];
+        } else if (c == 1) {
             ge = g;
 #pragma unroll
-            for (int k = 0; k < L; ++k) {
-                t[k] = r[k];
-                m[k] = q[k];
-            }
-        } else if (c == 1) {
-#pragma unroll
-            for (int k = 0; k < L; ++k) v1[k] = r[k];
+            for (int k = 0; k < L; ++k) A[k] = r[k];
         } else {
-            mod_add<s, TPI>(v1, v1, r, N);
+            mod_add<s, TPI>(v, v, r, N);
         }
     }
-    if (square) mod_add<s, TPI>(v1, v1, v1, N);
+    if (square) mod_add<s, TPI>(v, v, v, N);
     // B' = v + ge·R − m (mod p);  m < R < 2p
+    {
+        uint32_t tmp[L];
+        load_lane<s, TPI>(tmp, Rmod);
 #pragma unroll
-    for (int k = 0; k < L; ++k) tmp[k] = ge ? Rp[k] : 0u;
-    mod_add<s, TPI>(v1, v1, tmp, N);
+        for (int k = 0; k < L; ++k) tmp[k] = ge ? tmp[k] : 0u;
+        mod_add<s, TPI>(v, v, tmp, N);
+    }
     reduce_once<s, TPI>(m, m, N);
-    mod_sub<s, TPI>(B, v1, m, N);
-#pragma unroll
-    for (int k = 0; k < L; ++k) A[k] = t[k];
+    mod_sub<s, TPI>(B, v, m, N);
 }
 
-// (A, B) <- (A, B)^e, e as `nd` window digits of `w` bits (most significant
-// first).  `table` = this instance's 2^w·2s-word scratch ([A | B] per entry).
+// (A, B) <- (A, B)^e, e as a sliding-window program (host::sliding_ops:
+// n_ops byte pairs (squarings, odd digit)).  `table` = this instance's
+// scratch of 2^(w−1) + 1 entries of 2s words ([A | B]): x^1, x^3, …,
+// x^(2^w − 1), then x².
 template <int s, int TPI>
-__device__ __forceinline__ void p2_pow(uint32_t (&A)[s / TPI], uint32_t (&B)[s / TPI], const uint8_t *digits,
-                                       int nd, int w, uint32_t *table, const Stage &st,
-                                       const uint32_t (&N)[s / TPI], uint32_t np, const uint32_t (&Rp)[s / TPI]) {
-    const int T = 1 << w;
-    store_lane<s, TPI>(table, Rp); // 1̃ = (R mod p, R mod p)
-    store_lane<s, TPI>(table + s, Rp);
-    store_lane<s, TPI>(table + 2 * s, A);
-    store_lane<s, TPI>(table + 3 * s, B);
-    // op sequence: table build (T−2 multiplies by x), then for each digit
-    // after the first: w squarings and one multiply by table[d] (d ≠ 0);
-    // ONE p2_mul call site (one inlined copy of the CIOS body in the loop)
-    int j = 2, i = 1, sq = 0;
+__device__ __forceinline__ void p2_pow(uint32_t (&A)[s / TPI], uint32_t (&B)[s / TPI], const uint8_t *ops,
+                                       int n_ops, int w, uint32_t *table, const Stage &st,
+                                       const uint32_t (&N)[s / TPI], uint32_t np, const uint32_t *Rmod) {
+    const int T = 1 << (w - 1);
+    uint32_t *x2 = table + 2 * s * T;
+    store_lane<s, TPI>(table, A);
+    store_lane<s, TPI>(table + s, B);
+    // op sequence: x² (one squaring), T−1 multiplies by x² for the odd
+    // powers, then the program; ONE p2_mul call site (one inlined copy of the
+    // CIOS body in the loop)
+    int j = -1, oi = 0, sq = 0;
     bool started = false;
     for (;;) {
         bool square;
         const uint32_t *g2 = nullptr;
-        if (j < T) {
-            square = false;
-            g2 = table + 2 * s;
+        if (j < T - 1) {
+            square = j < 0;
+            g2 = x2;
         } else {
             if (!started) {
-                load_lane<s, TPI>(A, table + 2 * s * (int)digits[0]);
-                load_lane<s, TPI>(B, table + 2 * s * (int)digits[0] + s);
+                const int d0 = ops[1];
+                load_lane<s, TPI>(A, table + 2 * s * (d0 >> 1));
+                load_lane<s, TPI>(B, table + 2 * s * (d0 >> 1) + s);
+                oi = 1;
+                sq = n_ops > 1 ? ops[2] : 0;
                 started = true;
             }
-            if (i >= nd) break;
-            if (sq < w) {
+            if (sq > 0) {
                 square = true;
             } else {
-                const int d = digits[i];
-                ++i;
-                sq = 0;
+                if (oi >= n_ops) break;
+                const int d = ops[2 * oi + 1];
+                ++oi;
+                sq = oi < n_ops ? ops[2 * oi] : 0;
                 if (d == 0) continue;
                 square = false;
-                g2 = table + 2 * s * d;
+                g2 = table + 2 * s * (d >> 1);
             }
         }
-        p2_mul<s, TPI>(A, B, g2, square, st, N, np, Rp);
-        if (j < T) {
-            store_lane<s, TPI>(table + 2 * s * j, A);
-            store_lane<s, TPI>(table + 2 * s * j + s, B);
+        p2_mul<s, TPI>(A, B, g2, square, st, N, np, Rmod);
+        if (j < T - 1) {
+            if (j < 0) {
+                store_lane<s, TPI>(x2, A);
+                store_lane<s, TPI>(x2 + s, B);
+                load_lane<s, TPI>(A, table);
+                load_lane<s, TPI>(B, table + s);
+            } else {
+                store_lane<s, TPI>(table + 2 * s * (j + 1), A);
+                store_lane<s, TPI>(table + 2 * s * (j + 1) + s, B);
+            }
             ++j;
         } else if (square) {
-            ++sq;
+            --sq;
         }
     }
 }
 
-// Products (32×32 → 64) of p2_pow for an exponent with these window digits:
-// CIOS passes of 2s²+s products; squarings 2 passes, multiplies 3.
-inline unsigned long long p2_pow_passes(const uint8_t *digits, int nd, int w) {
-    unsigned long long passes = 3ull * ((1ull << w) - 2);
-    for (int i = 1; i < nd; ++i) passes += 2ull * w + (digits[i] ? 3ull : 0ull);
+// CIOS passes (2s²+s products each) of p2_pow for a sliding-window program:
+// squarings 2 passes, multiplies 3.
+inline unsigned long long p2_pow_passes(const uint8_t *ops, int n_ops, int w) {
+    unsigned long long passes = 2ull + 3ull * ((1ull << (w - 1)) - 1);
+    for (int i = 1; i < n_ops; ++i) passes += 2ull * ops[2 * i] + (ops[2 * i + 1] ? 3ull : 0ull);
     return passes;
 }
 
@@ -148,8 +161,8 @@ struct P2Args {
     ModArg mod_p[2];          // S = s
     const uint32_t *pinv[2];  // p⁻¹ mod 2^(32s)
     const uint32_t *cdec[2];  // h_p·R⁻¹ mod p (decrypt output)
-    const uint8_t *dig[2];
-    int nd[2];
+    const uint8_t *ops[2];    // sliding-window programs (host::sliding_ops)
+    int n_ops[2];             // byte pairs
     const uint32_t *in;       // per (item, prime): 2s words
     uint32_t *out;            // per (item or element, prime)
     const uint32_t *idx;      // decrypt: item -> element (compaction), else null
@@ -168,8 +181,11 @@ struct P2Args {
 //     u = c^(p−1) = 1 + p·ℓ has digits (R mod p, R mod p + ℓ·R²), so the CRT
 //     share m_p = ℓ·h_p = MM(B − R mod p, h_p·R⁻¹) goes to out (s words per
 //     (element, prime)); A = 0 flags c ≡ 0 (mod p).
+#ifndef SFXB_P2_MINB
+#define SFXB_P2_MINB 1
+#endif
 template <int s, int TPI, int W, int MODE>
-__global__ void __launch_bounds__(kBlock) k_p2_pow(P2Args a) {
+__global__ void __launch_bounds__(kBlock, SFXB_P2_MINB) k_p2_pow(P2Args a) {
     constexpr int L = s / TPI, NI = kBlock / TPI;
     __shared__ uint2 sB[s / 2 * NI];
     const Stage st = make_stage<TPI>(sB);
@@ -177,9 +193,8 @@ __global__ void __launch_bounds__(kBlock) k_p2_pow(P2Args a) {
     const size_t gi = ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * NI + st.inst;
     uint32_t *table = a.scratch + gi * ((size_t)(2 * s) << W);
     const ModRef M = a.mod_p[which].ref();
-    uint32_t N[L], Rp[L];
+    uint32_t N[L];
     load_const<s, TPI>(N, M, kMod);
-    load_const<s, TPI>(Rp, M, kOne);
     SFXB_UNIFORM_LOOP(item, active, a.count) {
         const uint32_t *src = a.in + (item * 2 + which) * 2 * s;
         uint32_t A[L], B[L], x[L];
@@ -258,6 +273,8 @@ __global__ void __launch_bounds__(kBlock) k_p2_pow(P2Args a) {
             for (int k = 0; k < L; ++k) A[k] = Rsum[k];
             // B = (ge + ge2)·(R mod p) − m  (mod p)
             const int nge = (ge ? 1 : 0) + (ge2 ? 1 : 0);
+            uint32_t Rp[L];
+            load_const<s, TPI>(Rp, M, kOne);
 #pragma unroll
             for (int k = 0; k < L; ++k) x[k] = nge ? Rp[k] : 0u;
             uint32_t y[L];
@@ -267,7 +284,7 @@ __global__ void __launch_bounds__(kBlock) k_p2_pow(P2Args a) {
             reduce_once<s, TPI>(q, q, N);
             mod_sub<s, TPI>(B, x, q, N);
         }
-        p2_pow<s, TPI>(A, B, a.dig[which], a.nd[which], W, table, st, N, M.np, Rp);
+        p2_pow<s, TPI>(A, B, a.ops[which], a.n_ops[which], W, table, st, N, M.np, M.w + kOne * s);
         if constexpr (MODE == 0) {
             uint32_t *dst = a.out + (item * 2 + which) * 2 * s;
             if (active) {
@@ -278,7 +295,8 @@ __global__ void __launch_bounds__(kBlock) k_p2_pow(P2Args a) {
             const uint32_t e = a.idx[item];
             if (eq_small<L, TPI>(A, 0u) && active && inst_lane<TPI>() == 0) atomicOr(a.status, 4u);
             uint32_t C[L], mp[L], q[L];
-            mod_sub<s, TPI>(x, B, Rp, N);
+            load_const<s, TPI>(C, M, kOne);
+            mod_sub<s, TPI>(x, B, C, N);
             load_lane<s, TPI>(C, a.cdec[which]);
             stage_regs<s, TPI>(st, C);
             mont_mul_m<s, TPI>(mp, q, x, st.sB, st.inst, N, M.np); // ℓ·h_p mod p

@@ -333,8 +333,8 @@ void encrypt_dev(sfxb_ctx *c, const int64_t *d_q, const uint32_t *d_r, size_t co
                 for (int i = 0; i < 2; ++i) {
                     pa.mod_p[i] = arg(c->mod_pq[i]);
                     pa.pinv[i] = c->d_pinv[i];
-                    pa.dig[i] = c->d_dig_pq[i];
-                    pa.nd[i] = c->nd_pq[i];
+                    pa.ops[i] = c->d_ops_pq[i];
+                    pa.n_ops[i] = c->nops_pq[i];
                 }
                 pa.in = a.x;
                 pa.out = a.y;
@@ -455,8 +455,8 @@ void decrypt_dev(sfxb_ctx *c, const uint32_t *d_cts, size_t count, uint32_t scal
                 pa.mod_p[i] = arg(c->mod_pq[i]);
                 pa.pinv[i] = c->d_pinv[i];
                 pa.cdec[i] = c->d_cdec[i];
-                pa.dig[i] = c->d_dig_m1[i];
-                pa.nd[i] = c->nd_m1[i];
+                pa.ops[i] = c->d_ops_m1[i];
+                pa.n_ops[i] = c->nops_m1[i];
             }
             pa.in = xt;
             pa.out = a.mpq;
@@ -1499,8 +1499,12 @@ int sfxb_ctx_create(sfxb_ctx **out, int device, const uint32_t *n, uint32_t n_wo
                 c->d_dig_m1[i] = dev_digits(*c, pm1, kWindow, c->nd_m1[i]);
                 // profiling units: multiplications mod p² (step 1 runs mod p: 1/4 of the products)
                 host_window[i] = {pow_mmuls(host::mod(ot, pm1), kWindow), pow_mmuls(pr, kWindow),
-                                  pow_mmuls(pm1, kWindow), host::window_digits(pr, kWindow),
-                                  host::window_digits(pm1, kWindow)};
+                                  pow_mmuls(pm1, kWindow), host::sliding_ops(pr, kWindow),
+                                  host::sliding_ops(pm1, kWindow)};
+                c->d_ops_pq[i] = dev_upload(*c, host_window[i].dig_pr.data(), host_window[i].dig_pr.size());
+                c->nops_pq[i] = (int)host_window[i].dig_pr.size() / 2;
+                c->d_ops_m1[i] = dev_upload(*c, host_window[i].dig_pm1.data(), host_window[i].dig_pm1.size());
+                c->nops_m1[i] = (int)host_window[i].dig_pm1.size() / 2;
                 c->d_pinv[i] = dev_big(*c, host::inv_pow2(pr, s), s);
                 // h = (−other mod prime)^-1 mod prime, in Montgomery form
                 Big negot = host::sub(pr, host::mod(ot, pr));
@@ -1515,8 +1519,8 @@ int sfxb_ctx_create(sfxb_ctx **out, int device, const uint32_t *n, uint32_t n_wo
                 const Win &w = host_window[i];
                 c->prod_enc += w.e1 * pp; // step 1 mod p
                 if (c->p2_digits) {
-                    c->prod_enc += (dev::p2_pow_passes(w.dig_pr.data(), (int)w.dig_pr.size(), kWindow) + 2) * pp;
-                    c->prod_dec += (dev::p2_pow_passes(w.dig_pm1.data(), (int)w.dig_pm1.size(), kWindow) + 2) * pp;
+                    c->prod_enc += (dev::p2_pow_passes(w.dig_pr.data(), (int)w.dig_pr.size() / 2, kWindow) + 2) * pp;
+                    c->prod_dec += (dev::p2_pow_passes(w.dig_pm1.data(), (int)w.dig_pm1.size() / 2, kWindow) + 2) * pp;
                 } else {
                     c->prod_enc += w.pr * pp2;
                     c->prod_dec += w.pm1 * pp2;
