@@ -2,6 +2,7 @@
 and the reference's golden vectors (bit-exact; decrypted doubles compared
 bitwise).  Reference behaviour pinned: he.cpp:87-143, test_he.cpp:22-41."""
 import json
+import math
 import os
 import random
 
@@ -207,3 +208,50 @@ def test_encrypt_plain_words_matches_oracle(oracle, kname):
         assert got == [ok.encrypt_with_r(m, r) for m, r in zip(ms, rs)]
         with pytest.raises(_lib.SfxbError, match="plaintext out of range"):
             ctx.encrypt_plain(ints_to_words([n], ctx.nw), ints_to_words([5], ctx.nw))
+
+
+def _prime(rng, bits):
+    """Deterministic random prime (Miller-Rabin, 40 bases) for odd-size keys."""
+    while True:
+        c = rng.getrandbits(bits) | (3 << (bits - 2)) | 1
+        d, r = c - 1, 0
+        while d % 2 == 0:
+            d //= 2
+            r += 1
+        ok = True
+        for _ in range(40):
+            x = pow(rng.randrange(2, c - 1), d, c)
+            if x in (1, c - 1):
+                continue
+            for _ in range(r - 1):
+                x = x * x % c
+                if x == c - 1:
+                    break
+            else:
+                ok = False
+                break
+        if ok:
+            return c
+
+
+@pytest.mark.parametrize("pbits", [400, 800, 1200])
+def test_primes_short_of_their_size_class_use_the_mod_p2_kernels(pbits):
+    """Primes that do not fill their limb class (p < 2^(32s−1)) take the
+    mod-p² CIOS exponentiations instead of the base-p digit path; both must
+    agree with Python big integers (encrypt_with_r he.cpp:87-99, decrypt :105-115)."""
+    rng = random.Random(pbits)
+    p, q = _prime(rng, pbits), _prime(rng, pbits)
+    n = p * q
+    lam = (p - 1) * (q - 1) // math.gcd(p - 1, q - 1)
+    mu = pow(lam, -1, n)
+    ctx = _lib.Context(n, p, q)
+    count = 16
+    qs = [rng.randrange(-(1 << 60), 1 << 60) for _ in range(count)]
+    rs = [rng.randrange(2, n) for _ in range(count)]
+    cts = words_to_ints(ctx.encrypt(np.array(qs, np.int64), ints_to_words(rs, ctx.nw)))
+    n2 = n * n
+    for i in range(count):
+        assert cts[i] == (1 + (qs[i] % n) * n) % n2 * pow(rs[i], n, n2) % n2, i
+    _, decs, plain = ctx.decrypt(ints_to_words(cts, ctx.ct_words), want_plain=True)
+    assert decs == count
+    assert words_to_ints(plain) == [((pow(c, lam, n2) - 1) // n) * mu % n for c in cts]
