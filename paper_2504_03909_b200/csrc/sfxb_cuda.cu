@@ -200,7 +200,7 @@ struct Cls<8> {
 };
 template <>
 struct Cls<16> {
-    static constexpr int T1 = 1, T2 = 2, TC = 4, TD = 2, TE = 2, TH = 4, TN = 4, TP = 2, TQ = 4;
+    static constexpr int T1 = 1, T2 = 2, TC = 4, TD = 2, TE = 2, TH = 4, TN = 4, TP = 1, TQ = 4;
 };
 #ifndef SFXB_T1_32
 #define SFXB_T1_32 1
@@ -215,7 +215,7 @@ struct Cls<16> {
 #define SFXB_TH_32 4
 #endif
 #ifndef SFXB_TP_32
-#define SFXB_TP_32 2
+#define SFXB_TP_32 1
 #endif
 template <>
 struct Cls<32> { // 2048-bit keys (tuned on B200, profiles/)
