@@ -103,6 +103,7 @@ struct CtxState {
     // their size class (p > 2^(32s−1)); otherwise the CIOS mod-p² kernels
     bool p2_digits = false;
     uint32_t *d_cdec[2] = {nullptr, nullptr}; // h_p·R⁻¹ mod p, h_q·R⁻¹ mod q   (s)
+    uint32_t *d_negR[2] = {nullptr, nullptr}; // p − R mod p, q − R mod q          (s)
 
     // scratch (grown on demand, freed with the context)
     Buf scratch_table, tmp[4], host_pinned[2], io[6]; // io: host-API staging (grow-only)

@@ -31,11 +31,13 @@ struct Stage {
     int inst;
 };
 
+// (one lane per instance: the slots are private to the thread, so program
+// order suffices and the staging is safe in divergent code)
 template <int S, int TPI>
 __device__ __forceinline__ void stage_b(const Stage &st, const uint32_t (&v)[S / TPI]) {
-    __syncwarp();
+    if constexpr (TPI > 1) __syncwarp();
     store_b<S, TPI>(st.sB, st.NI, st.inst, v);
-    __syncwarp();
+    if constexpr (TPI > 1) __syncwarp();
 }
 
 // r = A·B·R⁻¹ mod M with B given in lane limbs (staged through shared memory)

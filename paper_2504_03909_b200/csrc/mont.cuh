@@ -371,6 +371,40 @@ __device__ __forceinline__ bool mont_mul_m(uint32_t (&r)[S / TPI], uint32_t (&Mq
     return mont_tail<L, TPI>(r, X, Y, Z, N);
 }
 
+// mont_mul that, when `sub`, also subtracts the pass's quotient
+// m = Σ q_i·2^(32i) from V in place (V − m mod 2^(32S), final borrow in
+// `borrow`) instead of storing m: A·B = (r + ge·M)·2^(32S) − m·M exactly.
+// Returns ge.  (The digit arithmetic of padic.cuh only needs V − m.)
+template <int S, int TPI>
+__device__ __forceinline__ bool mont_mul_sub(uint32_t (&r)[S / TPI], uint32_t (&V)[S / TPI],
+                                             const uint32_t (&A)[S / TPI], const uint2 *sB, int inst,
+                                             const uint32_t (&N)[S / TPI], uint32_t np, bool sub,
+                                             uint32_t &borrow) {
+    constexpr int L = S / TPI, NIc = 128 / TPI;
+    const int t = inst_lane<TPI>();
+    uint32_t X[L], Y[L], Z = 0, bw = 0;
+#pragma unroll
+    for (int k = 0; k < L; ++k) X[k] = Y[k] = 0;
+    for (int tr = 0; tr < TPI; ++tr) {
+#pragma unroll
+        for (int j = 0; j < L / 2; ++j) {
+            const uint2 b = sB[b_slot<NIc>(tr * (L / 2) + j, inst)];
+            const uint32_t q0 = cios_step<L, TPI>(X, Y, Z, A, N, b.x, np, false);
+            const uint32_t q1 = cios_step<L, TPI>(Y, X, Z, A, N, b.y, np, false);
+            if (sub && tr == t) {
+                const uint64_t d0 = (uint64_t)V[2 * j] - q0 - bw;
+                V[2 * j] = (uint32_t)d0;
+                const uint64_t d1 = (uint64_t)V[2 * j + 1] - q1 - (uint32_t)(d0 >> 63);
+                V[2 * j + 1] = (uint32_t)d1;
+                bw = (uint32_t)(d1 >> 63);
+            }
+        }
+        if constexpr (TPI > 1) bw = __shfl_sync(0xffffffffu, bw, tr, TPI); // lane tr's borrow moves on
+    }
+    borrow = bw;
+    return mont_tail<L, TPI>(r, X, Y, Z, N);
+}
+
 // ---------------------------------------------------------------- global <-> lane limbs
 
 template <int S, int TPI>

@@ -18,7 +18,7 @@
 //
 // The identity 1̃ = R² mod p² has digits (R mod p, R mod p) when p > R/2.
 #pragma once
-#include "kernels.cuh"
+#include "hist.cuh"
 
 namespace sfxb {
 namespace dev {
@@ -31,19 +31,21 @@ __device__ __forceinline__ void stage_regs(const Stage &st, const uint32_t (&v)[
 
 // One Montgomery product mod p² on digits: (A, B) <- (A, B) ⊛ (A2, B2),
 // or the square when `square` (A2, B2 unused).  2 or 3 CIOS passes through
-// ONE inlined mont_mul_m call site (the hot loop stays one copy of the
+// ONE inlined mont_mul_sub call site (the hot loop stays one copy of the
 // unrolled CIOS body):
-//   pass 0: v = MM(A, B | B2)
-//   pass 1: t, m, ge = MM_m(A, A | A2);  A <- t (A is not needed any more)
-//   pass 2: v += MM(B, A2)                   (multiply only)
-// then B <- (1 + square)·v + ge·R − m (mod p).  `Rmod` = R mod p (global).
+//   pass 0: v = MM(A, B | B2)            (doubled for a square)
+//   pass 1: t, ge = MM(A, A | A2), v -= m on the fly (borrow bw);  A <- t
+//   pass 2: v2 = MM(B, A2)                (multiply only)
+// then B <- v − m + ge·R (+ v2) (mod p): v − m + (ge − bw)·R with v − m
+// (mod R) < R < 2p.  Rmod = R mod p, negR = p − R mod p (global).
 template <int s, int TPI>
 __device__ __forceinline__ void p2_mul(uint32_t (&A)[s / TPI], uint32_t (&B)[s / TPI], const uint32_t *g2,
                                        bool square, const Stage &st, const uint32_t (&N)[s / TPI], uint32_t np,
-                                       const uint32_t *Rmod) {
+                                       const uint32_t *Rmod, const uint32_t *negR) {
     constexpr int L = s / TPI;
-    uint32_t m[L], v[L], x[L];
+    uint32_t v[L], x[L];
     bool ge = false;
+    uint32_t bw = 0;
     const int passes = square ? 2 : 3;
 #pragma unroll 1
     for (int c = 0; c < passes; ++c) {
@@ -59,30 +61,35 @@ __device__ __forceinline__ void p2_mul(uint32_t (&A)[s / TPI], uint32_t (&B)[s /
         }
 #pragma unroll
         for (int k = 0; k < L; ++k) x[k] = c == 2 ? B[k] : A[k];
-        uint32_t r[L];
-        const bool g = mont_mul_m<s, TPI>(r, m, x, st.sB, st.inst, N, np, c == 1);
+        uint32_t r[L], b;
+        const bool g = mont_mul_sub<s, TPI>(r, v, x, st.sB, st.inst, N, np, c == 1, b);
         if (c == 0) {
 #pragma unroll
             for (int k = 0; k < L; ++k) v[k] = r[k];
+            if (square) mod_add<s, TPI>(v, v, v, N);
         } else if (c == 1) {
             ge = g;
+            bw = b;
 #pragma unroll
             for (int k = 0; k < L; ++k) A[k] = r[k];
         } else {
-            mod_add<s, TPI>(v, v, r, N);
+#pragma unroll
+            for (int k = 0; k < L; ++k) x[k] = r[k]; // v2
         }
     }
-    if (square) mod_add<s, TPI>(v, v, v, N);
-    // B' = v + ge·R − m (mod p);  m < R < 2p
+    reduce_once<s, TPI>(v, v, N);
     {
+        // + (ge − bw)·R  (mod p)
+        const int delta = (ge ? 1 : 0) - (int)bw;
         uint32_t tmp[L];
-        load_lane<s, TPI>(tmp, Rmod);
+        load_lane<s, TPI>(tmp, delta > 0 ? Rmod : negR);
 #pragma unroll
-        for (int k = 0; k < L; ++k) tmp[k] = ge ? tmp[k] : 0u;
+        for (int k = 0; k < L; ++k) tmp[k] = delta ? tmp[k] : 0u;
         mod_add<s, TPI>(v, v, tmp, N);
     }
-    reduce_once<s, TPI>(m, m, N);
-    mod_sub<s, TPI>(B, v, m, N);
+    if (!square) mod_add<s, TPI>(v, v, x, N);
+#pragma unroll
+    for (int k = 0; k < L; ++k) B[k] = v[k];
 }
 
 // (A, B) <- (A, B)^e, e as a sliding-window program (host::sliding_ops:
@@ -92,7 +99,8 @@ __device__ __forceinline__ void p2_mul(uint32_t (&A)[s / TPI], uint32_t (&B)[s /
 template <int s, int TPI>
 __device__ __forceinline__ void p2_pow(uint32_t (&A)[s / TPI], uint32_t (&B)[s / TPI], const uint8_t *ops,
                                        int n_ops, int w, uint32_t *table, const Stage &st,
-                                       const uint32_t (&N)[s / TPI], uint32_t np, const uint32_t *Rmod) {
+                                       const uint32_t (&N)[s / TPI], uint32_t np, const uint32_t *Rmod,
+                                       const uint32_t *negR) {
     const int T = 1 << (w - 1);
     uint32_t *x2 = table + 2 * s * T;
     store_lane<s, TPI>(table, A);
@@ -129,7 +137,7 @@ __device__ __forceinline__ void p2_pow(uint32_t (&A)[s / TPI], uint32_t (&B)[s /
                 g2 = table + 2 * s * (d >> 1);
             }
         }
-        p2_mul<s, TPI>(A, B, g2, square, st, N, np, Rmod);
+        p2_mul<s, TPI>(A, B, g2, square, st, N, np, Rmod, negR);
         if (j < T - 1) {
             if (j < 0) {
                 store_lane<s, TPI>(x2, A);
@@ -155,12 +163,63 @@ inline unsigned long long p2_pow_passes(const uint8_t *ops, int n_ops, int w) {
     return passes;
 }
 
+// Digits of X̃ (a canonical residue mod p², 2s limbs: hi·R + lo, hi < p):
+// MM_m(1, lo) gives lo = (t + ge·p)·R − m·p, so A = hi + t (mod p, flag ge2)
+// and B = (ge + ge2)·R − m (mod p).
+template <int s, int TPI>
+__device__ __forceinline__ void p2_split(uint32_t (&A)[s / TPI], uint32_t (&B)[s / TPI], const uint32_t (&lo)[s / TPI],
+                                         const uint32_t (&hi)[s / TPI], const Stage &st,
+                                         const uint32_t (&N)[s / TPI], uint32_t np, const uint32_t *Rmod) {
+    constexpr int L = s / TPI;
+    uint32_t q[L], t[L], one[L], x[L];
+    set_small<L, TPI>(one, 1u);
+    stage_b<s, TPI>(st, lo);
+    const bool ge = mont_mul_m<s, TPI>(t, q, one, st.sB, st.inst, N, np);
+    uint32_t Rsum[L];
+    Rsum[0] = add_cc(hi[0], t[0]);
+#pragma unroll
+    for (int k = 1; k < L; ++k) Rsum[k] = addc_cc(hi[k], t[k]);
+    uint32_t cc = addc(0u, 0u), over;
+    if constexpr (TPI == 1) {
+        over = cc;
+    } else {
+        bool all_ones = true;
+#pragma unroll
+        for (int k = 0; k < L; ++k) all_ones &= (Rsum[k] == 0xffffffffu);
+        const uint32_t G = inst_ballot<TPI>(cc != 0);
+        const uint32_t P = inst_ballot<TPI>(all_ones);
+        const uint64_t sum = (uint64_t)P + ((uint64_t)G << 1);
+        const uint32_t cin = (uint32_t)(sum ^ P);
+        if ((cin >> inst_lane<TPI>()) & 1u) {
+            Rsum[0] = add_cc(Rsum[0], 1u);
+#pragma unroll
+            for (int k = 1; k < L; ++k) Rsum[k] = addc_cc(Rsum[k], 0u);
+        }
+        over = (uint32_t)(sum >> TPI) & 1u;
+    }
+    const bool ge2 = final_sub<L, TPI>(Rsum, over, N);
+#pragma unroll
+    for (int k = 0; k < L; ++k) A[k] = Rsum[k];
+    const int nge = (ge ? 1 : 0) + (ge2 ? 1 : 0);
+    uint32_t Rp[L], y[L];
+    load_lane<s, TPI>(Rp, Rmod);
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+        x[k] = nge ? Rp[k] : 0u;
+        y[k] = nge == 2 ? Rp[k] : 0u;
+    }
+    mod_add<s, TPI>(x, x, y, N);
+    reduce_once<s, TPI>(q, q, N);
+    mod_sub<s, TPI>(B, x, q, N);
+}
+
 // ------------------------------------------------------------------ kernels
 
 struct P2Args {
     ModArg mod_p[2];          // S = s
     const uint32_t *pinv[2];  // p⁻¹ mod 2^(32s)
     const uint32_t *cdec[2];  // h_p·R⁻¹ mod p (decrypt output)
+    const uint32_t *negR[2];  // p − R mod p
     const uint8_t *ops[2];    // sliding-window programs (host::sliding_ops)
     int n_ops[2];             // byte pairs
     const uint32_t *in;       // per (item, prime): 2s words
@@ -239,52 +298,12 @@ __global__ void __launch_bounds__(kBlock, SFXB_P2_MINB) k_p2_pow(P2Args a) {
             stage_regs<s, TPI>(st, tmp);
             mont_mul_m<s, TPI>(B, q, C, st.sB, st.inst, N, M.np);
         } else {
-            uint32_t lo[L], hi[L], q[L], t[L], one[L];
+            uint32_t lo[L], hi[L];
             load_lane<s, TPI>(lo, src);
             load_lane<s, TPI>(hi, src + s);
-            set_small<L, TPI>(one, 1u);
-            stage_regs<s, TPI>(st, lo);
-            const bool ge = mont_mul_m<s, TPI>(t, q, one, st.sB, st.inst, N, M.np);
-            // A = hi + t mod p (hi < p since X̃ < p²), ge2 = subtraction happened
-            uint32_t Rsum[L];
-            Rsum[0] = add_cc(hi[0], t[0]);
-#pragma unroll
-            for (int k = 1; k < L; ++k) Rsum[k] = addc_cc(hi[k], t[k]);
-            uint32_t cc = addc(0u, 0u), over;
-            if constexpr (TPI == 1) {
-                over = cc;
-            } else {
-                bool all_ones = true;
-#pragma unroll
-                for (int k = 0; k < L; ++k) all_ones &= (Rsum[k] == 0xffffffffu);
-                const uint32_t G = inst_ballot<TPI>(cc != 0);
-                const uint32_t P = inst_ballot<TPI>(all_ones);
-                const uint64_t sum = (uint64_t)P + ((uint64_t)G << 1);
-                const uint32_t cin = (uint32_t)(sum ^ P);
-                if ((cin >> inst_lane<TPI>()) & 1u) {
-                    Rsum[0] = add_cc(Rsum[0], 1u);
-#pragma unroll
-                    for (int k = 1; k < L; ++k) Rsum[k] = addc_cc(Rsum[k], 0u);
-                }
-                over = (uint32_t)(sum >> TPI) & 1u;
-            }
-            const bool ge2 = final_sub<L, TPI>(Rsum, over, N);
-#pragma unroll
-            for (int k = 0; k < L; ++k) A[k] = Rsum[k];
-            // B = (ge + ge2)·(R mod p) − m  (mod p)
-            const int nge = (ge ? 1 : 0) + (ge2 ? 1 : 0);
-            uint32_t Rp[L];
-            load_const<s, TPI>(Rp, M, kOne);
-#pragma unroll
-            for (int k = 0; k < L; ++k) x[k] = nge ? Rp[k] : 0u;
-            uint32_t y[L];
-#pragma unroll
-            for (int k = 0; k < L; ++k) y[k] = nge == 2 ? Rp[k] : 0u;
-            mod_add<s, TPI>(x, x, y, N);
-            reduce_once<s, TPI>(q, q, N);
-            mod_sub<s, TPI>(B, x, q, N);
+            p2_split<s, TPI>(A, B, lo, hi, st, N, M.np, M.w + kOne * s);
         }
-        p2_pow<s, TPI>(A, B, a.ops[which], a.n_ops[which], W, table, st, N, M.np, M.w + kOne * s);
+        p2_pow<s, TPI>(A, B, a.ops[which], a.n_ops[which], W, table, st, N, M.np, M.w + kOne * s, a.negR[which]);
         if constexpr (MODE == 0) {
             uint32_t *dst = a.out + (item * 2 + which) * 2 * s;
             if (active) {
@@ -364,6 +383,194 @@ __global__ void __launch_bounds__(kBlock) k_dec_pre(DecArgs a, uint32_t n_items,
         load_lane<S2, TPI>(hi, a.cts + (size_t)e * 2 * S2 + S2);
         to_mont_wide<S2, TPI>(u, lo, hi, M2, st, N2);
         if (active) store_lane<S2, TPI>(xt + (item * 2 + which) * S2, u);
+    }
+}
+
+
+// ------------------------------------------------------------------ K2 at the key holder
+//
+// The active party holds p and q (federation.cpp:83-85), so its encrypted
+// histogram can multiply ciphertexts by CRT: mod p² and mod q² on base-p/q
+// digits (2 × 3 CIOS passes of 2s²+s products = 12,480 at 2048-bit n against
+// one mod-n² pass of 2(4s)²+4s = 32,896), recombined to the unique residue
+// mod n² per output slot — bit-identical to the mod-n² product.
+// gh ciphertexts live as [A_p | B_p | A_q | B_q] (4s words, the ciphertext's
+// own footprint).
+
+struct CrtArgs {
+    ModArg mod_p[2];      // s
+    ModArg mod_p2[2];     // 2s
+    ModArg mod_n2;        // 4s
+    const uint32_t *qq_inv_m; // (q²)⁻¹·R2 mod p²       (2s)
+    const uint32_t *q2R_n2;   // q²·R4 mod n²           (4s)
+    const uint32_t *negR[2];  // p − R mod p            (s)
+};
+
+// plain ciphertexts (4s words each, in place) -> digits of c mod p², c mod q²
+template <int s, int TPI>
+__global__ void __launch_bounds__(kBlock) k_gh_digits(CrtArgs a, uint32_t *gh, size_t count) {
+    constexpr int S2 = 2 * s, L2 = S2 / TPI, L = s / TPI, NI = kBlock / TPI;
+    __shared__ uint2 sB[S2 / 2 * NI];
+    const Stage st = make_stage<TPI>(sB);
+    SFXB_UNIFORM_LOOP(e, active, count) {
+        uint32_t *c = gh + e * 4 * s;
+        uint32_t lo[L2], hi[L2], X[2][L2];
+        load_lane<S2, TPI>(lo, c);
+        load_lane<S2, TPI>(hi, c + S2);
+#pragma unroll
+        for (int pr = 0; pr < 2; ++pr) {
+            const ModRef M2 = a.mod_p2[pr].ref();
+            uint32_t N2[L2], u[L2];
+            load_const<S2, TPI>(N2, M2, kMod);
+            to_mont_wide<S2, TPI>(u, lo, hi, M2, st, N2); // c·R2 mod p² (R2 = 2^(64s) = R²)
+#pragma unroll
+            for (int k = 0; k < L2; ++k) X[pr][k] = u[k];
+        }
+        __syncwarp();
+        if (active) {
+            store_lane<S2, TPI>(c, X[0]);
+            store_lane<S2, TPI>(c + S2, X[1]);
+        }
+        __syncwarp();
+#pragma unroll 1
+        for (int pr = 0; pr < 2; ++pr) {
+            const ModRef M = a.mod_p[pr].ref();
+            uint32_t N[L], xl[L], xh[L], A[L], B[L];
+            load_const<s, TPI>(N, M, kMod);
+            load_lane<s, TPI>(xl, c + pr * S2);
+            load_lane<s, TPI>(xh, c + pr * S2 + s);
+            p2_split<s, TPI>(A, B, xl, xh, st, N, M.np, M.w + kOne * s);
+            __syncwarp();
+            if (active) {
+                store_lane<s, TPI>(c + pr * S2, A);
+                store_lane<s, TPI>(c + pr * S2 + s, B);
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// Segmented product pass on digits (one lane per job; the k_seg_prod
+// protocol).  Job j = 4·rank + 2·gh + prime over the length-sorted pieces.
+template <int s, int C>
+__global__ void __launch_bounds__(kBlock) k_seg_prod_p2(CrtArgs a, const Piece *pieces, const uint32_t *order,
+                                                        size_t n_pieces, const uint32_t *sorted, const uint32_t *src,
+                                                        uint32_t *dst, unsigned long long *next_job) {
+    constexpr int L = s;
+    __shared__ uint2 sB[s / 2 * kBlock];
+    const Stage st = make_stage<1>(sB);
+    const size_t total = 4 * n_pieces;
+    for (;;) {
+        unsigned long long base = 0;
+        if ((threadIdx.x & 31) == 0) base = atomicAdd(next_job, 32ull);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= total) break;
+        const size_t job = base + (threadIdx.x & 31);
+        if (job < total) {
+            const uint32_t pidx = order[job >> 2];
+            const Piece pc = pieces[pidx];
+            const uint32_t g = (uint32_t)((job >> 1) & 1), pr = (uint32_t)(job & 1);
+            const ModRef M = a.mod_p[pr].ref();
+            uint32_t N[L], A[L], B[L];
+            load_const<s, 1>(N, M, kMod);
+            auto item_ptr = [&](uint32_t k) -> const uint32_t * {
+                const size_t idx = sorted ? (2 * (size_t)sorted[pc.start + k] + g) : (2 * (size_t)(pc.start + k) + g);
+                return src + idx * 4 * s + pr * 2 * s;
+            };
+            const uint32_t *p0 = item_ptr(0);
+            load_lane<s, 1>(A, p0);
+            load_lane<s, 1>(B, p0 + s);
+            for (uint32_t k = 1; k < pc.len; ++k) {
+                // the rows are gathered at random from a gh buffer far larger
+                // than L2: fetch the next item while this one is multiplied
+                if (k + 1 < pc.len) {
+                    const uint32_t *nx = item_ptr(k + 1);
+#pragma unroll
+                    for (int o = 0; o < 2 * s; o += 32)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(nx + o));
+                }
+                p2_mul<s, 1>(A, B, item_ptr(k), false, st, N, M.np, M.w + kOne * s, a.negR[pr]);
+            }
+            uint32_t *d = dst + (2 * (size_t)pidx + g) * 4 * s + pr * 2 * s;
+            store_lane<s, 1>(d, A);
+            store_lane<s, 1>(d + s, B);
+        }
+    }
+}
+
+// digits [A | B] of Ũ = u·R2 mod p² (this lane's layout at S2) -> plain u:
+//   u = MM2(A, R) + MM2(B, p)  (mod p²)
+template <int s, int TPI>
+__device__ __forceinline__ void p2_digits_plain(uint32_t (&u)[2 * s / TPI], const uint32_t *ab, const ModRef &M2,
+                                                const ModRef &Mp, const Stage &st, const uint32_t (&N2)[2 * s / TPI]) {
+    constexpr int S2 = 2 * s, L2 = S2 / TPI;
+    const int tl = inst_lane<TPI>();
+    const bool low = tl * L2 < s;
+    uint32_t av[L2], bv[L2], Rc[L2], pc[L2], v[L2];
+    load_lane<S2, TPI>(av, ab);
+    relayout<S2, S2, TPI>(bv, av, st);
+#pragma unroll
+    for (int k = 0; k < L2; ++k) {
+        const int limb = tl * L2 + k;
+        bv[k] = limb < s ? staged_word<TPI>(st, limb + s) : 0u;
+        av[k] = low ? av[k] : 0u;
+        Rc[k] = limb == s ? 1u : 0u;
+        pc[k] = limb < s ? __ldg(Mp.w + limb) : 0u;
+    }
+    __syncwarp();
+    mmul<S2, TPI>(u, av, Rc, st, N2, M2.np);
+    mmul<S2, TPI>(v, bv, pc, st, N2, M2.np);
+    mod_add<S2, TPI>(u, u, v, N2);
+}
+
+// Output slot (key, gh): count == 0 -> 1 (Montgomery one for partials); else
+// CRT of the key's final digit partial: c = c_q + q²·((c_p − c_q)·q⁻² mod p²).
+template <int s, int TPI>
+__global__ void __launch_bounds__(kBlock) k_hist_finalize_p2(CrtArgs a, const uint32_t *count,
+                                                             const uint32_t *final_idx, size_t nkeys,
+                                                             const uint32_t *partial, uint32_t *out, int mont_out) {
+    constexpr int S2 = 2 * s, S4 = 4 * s, L2 = S2 / TPI, L4 = S4 / TPI, NI = kBlock / TPI;
+    __shared__ uint2 sB[S4 / 2 * NI];
+    const Stage st = make_stage<TPI>(sB);
+    const ModRef M4 = a.mod_n2.ref();
+    uint32_t N4[L4];
+    load_const<S4, TPI>(N4, M4, kMod);
+    SFXB_UNIFORM_LOOP(slot, active, 2 * nkeys) {
+        const size_t key = slot >> 1;
+        const uint32_t g = (uint32_t)(slot & 1);
+        uint32_t c4[L4];
+        // warp-uniform: every instance runs the CRT (empty keys on a dummy
+        // but valid operand, their own output slot) and selects afterwards
+        const bool empty = count[key] == 0;
+        {
+            const uint32_t *pp = empty ? out + slot * S4 : partial + (2 * (size_t)final_idx[key] + g) * S4;
+            const ModRef M2 = a.mod_p2[0].ref(), Q2 = a.mod_p2[1].ref();
+            uint32_t N2[L2], yp[L2], yq[L2], d[L2], C2[L2], h[L2];
+            load_const<S2, TPI>(N2, Q2, kMod);
+            p2_digits_plain<s, TPI>(yq, pp + S2, Q2, a.mod_p[1].ref(), st, N2);
+            load_const<S2, TPI>(N2, M2, kMod);
+            p2_digits_plain<s, TPI>(yp, pp, M2, a.mod_p[0].ref(), st, N2);
+            reduce_once<S2, TPI>(d, yq, N2); // c_q mod p² (c_q < q² < 2p²)
+            mod_sub<S2, TPI>(d, yp, d, N2);
+            load_lane<S2, TPI>(C2, a.qq_inv_m);
+            mmul<S2, TPI>(h, C2, d, st, N2, M2.np);
+            uint32_t h4[L4], yq4[L4], C4[L4];
+            relayout<S2, S4, TPI>(h4, h, st);
+            relayout<S2, S4, TPI>(yq4, yq, st);
+            load_lane<S4, TPI>(C4, a.q2R_n2);
+            mmul<S4, TPI>(c4, C4, h4, st, N4, M4.np); // q²·h (< n², exact)
+            mod_add<S4, TPI>(c4, c4, yq4, N4);
+            if (mont_out) {
+                load_const<S4, TPI>(C4, M4, kR2);
+                mmul<S4, TPI>(c4, C4, c4, st, N4, M4.np);
+            }
+        }
+        if (empty) {
+            if (mont_out) load_const<S4, TPI>(c4, M4, kOne);
+            else set_small<L4, TPI>(c4, 1u);
+        }
+        __syncwarp();
+        if (active) store_lane<S4, TPI>(out + slot * S4, c4);
     }
 }
 

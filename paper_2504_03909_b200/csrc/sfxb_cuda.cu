@@ -88,6 +88,7 @@ struct sfxb_gh {
     uint32_t *d = nullptr;     // 2·n_samples × 4s limbs, Montgomery form
     uint8_t *flags = nullptr;  // per row: bit0 Enc(g) == 1, bit1 Enc(h) == 1
     uint32_t n_samples = 0;
+    bool digits = false;       // key holder: [A_p | B_p | A_q | B_q] digits instead (padic.cuh K2)
     size_t bytes = 0, fbytes = 0;
     // device group: one handle per shard holding rows [row_lo[k], row_lo[k+1])
     std::vector<sfxb_gh *> parts;
@@ -333,6 +334,7 @@ void encrypt_dev(sfxb_ctx *c, const int64_t *d_q, const uint32_t *d_r, size_t co
                 for (int i = 0; i < 2; ++i) {
                     pa.mod_p[i] = arg(c->mod_pq[i]);
                     pa.pinv[i] = c->d_pinv[i];
+                    pa.negR[i] = c->d_negR[i];
                     pa.ops[i] = c->d_ops_pq[i];
                     pa.n_ops[i] = c->nops_pq[i];
                 }
@@ -455,6 +457,7 @@ void decrypt_dev(sfxb_ctx *c, const uint32_t *d_cts, size_t count, uint32_t scal
                 pa.mod_p[i] = arg(c->mod_pq[i]);
                 pa.pinv[i] = c->d_pinv[i];
                 pa.cdec[i] = c->d_cdec[i];
+                pa.negR[i] = c->d_negR[i];
                 pa.ops[i] = c->d_ops_m1[i];
                 pa.n_ops[i] = c->nops_m1[i];
             }
@@ -536,6 +539,25 @@ void free_hist_bufs(sfxb_ctx *c) {
     c->hist = nullptr;
 }
 
+// The key holder's histograms multiply by CRT on base-p/q digits (2.6× fewer
+// products than mod n²); SFXB_NO_CRT_HISTOGRAM=1 forces the mod-n² path.
+bool crt_histogram(const sfxb_ctx *c) {
+    static const bool off = std::getenv("SFXB_NO_CRT_HISTOGRAM") != nullptr;
+    return c->has_priv && c->p2_digits && !off;
+}
+dev::CrtArgs crt_args(const sfxb_ctx *c) {
+    dev::CrtArgs a{};
+    for (int i = 0; i < 2; ++i) {
+        a.mod_p[i] = arg(c->mod_pq[i]);
+        a.mod_p2[i] = arg(c->mod_pq2[i]);
+        a.negR[i] = c->d_negR[i];
+    }
+    a.mod_n2 = arg(c->mod_n2);
+    a.qq_inv_m = c->d_qq_inv_m;
+    a.q2R_n2 = c->d_q2R_n2;
+    return a;
+}
+
 void gh_prepare(sfxb_ctx *c, sfxb_gh *g) {
     const size_t S4 = 4 * (size_t)c->s, n2 = 2 * (size_t)g->n_samples;
     dispatch_class(c->s, [&](auto sc) {
@@ -545,11 +567,21 @@ void gh_prepare(sfxb_ctx *c, sfxb_gh *g) {
             int grid = (int)std::min<size_t>((g->n_samples + 255) / 256, (size_t)c->sms * 8);
             dev::k_gh_flags<4 * cs><<<grid, 256, 0, c->stream>>>(g->d, g->n_samples, 2 * c->nw, g->flags);
             check_launch(*c);
-            auto k = dev::k_to_mont<4 * cs, C::TH>;
-            constexpr int NI = dev::kBlock / C::TH;
-            int grid2 = occupancy_grid(*c, k, n2, NI);
-            k<<<grid2, dev::kBlock, 0, c->stream>>>(arg(c->mod_n2), g->d, n2);
-            check_launch(*c);
+            if (crt_histogram(c)) {
+                // key holder: CRT digits mod p², q² (padic.cuh "K2 at the key holder")
+                auto k = dev::k_gh_digits<cs, C::TQ>;
+                constexpr int NI = dev::kBlock / C::TQ;
+                k<<<occupancy_grid(*c, k, n2, NI), dev::kBlock, 0, c->stream>>>(crt_args(c), g->d, n2);
+                check_launch(*c);
+                g->digits = true;
+            } else {
+                auto k = dev::k_to_mont<4 * cs, C::TH>;
+                constexpr int NI = dev::kBlock / C::TH;
+                int grid2 = occupancy_grid(*c, k, n2, NI);
+                k<<<grid2, dev::kBlock, 0, c->stream>>>(arg(c->mod_n2), g->d, n2);
+                check_launch(*c);
+                g->digits = false;
+            }
         }
     });
     (void)S4;
@@ -835,16 +867,31 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
             constexpr int NI = dev::kBlock / C::TH;
             unsigned long long *next_job = reinterpret_cast<unsigned long long *>(misc + 12);
             CK(cudaMemsetAsync(next_job, 0, 8, st));
-            if (Cp == (uint32_t)kPieceLong) {
+            // each piece: len − 1 multiplications, G and H; profiling counts 32×32 products
+            const uint64_t mults = 2 * (items - P);
+            if (g->digits) {
+                // CRT on digits: 2 primes × 3 CIOS passes mod p per multiplication
+                const uint64_t pp = 2ull * cs * cs + cs;
+                ProfScope prof_(*c, 0, mults * 6 * pp);
+                if (Cp == (uint32_t)kPieceLong) {
+                    auto k = dev::k_seg_prod_p2<cs, kPieceLong>;
+                    k<<<occupancy_grid(*c, k, 4 * P, dev::kBlock), dev::kBlock, 0, st>>>(
+                        crt_args(c), pieces, order, P, pass == 0 ? sorted : nullptr, src, dst, next_job);
+                } else {
+                    auto k = dev::k_seg_prod_p2<cs, kPiece>;
+                    k<<<occupancy_grid(*c, k, 4 * P, dev::kBlock), dev::kBlock, 0, st>>>(
+                        crt_args(c), pieces, order, P, pass == 0 ? sorted : nullptr, src, dst, next_job);
+                }
+            } else if (Cp == (uint32_t)kPieceLong) {
                 auto k = dev::k_seg_prod<S4, C::TH, kPieceLong>;
                 const int grid = occupancy_grid(*c, k, 2 * P, NI);
-                ProfScope prof_(*c, 0, 2 * (items - P)); // each piece: len − 1 products, G and H
+                ProfScope prof_(*c, 0, mults * (2ull * S4 * S4 + S4));
                 k<<<grid, dev::kBlock, 0, st>>>(arg(c->mod_n2), pieces, order, P, pass == 0 ? sorted : nullptr, src,
                                                 dst, next_job);
             } else {
                 auto k = dev::k_seg_prod<S4, C::TH, kPiece>;
                 const int grid = occupancy_grid(*c, k, 2 * P, NI);
-                ProfScope prof_(*c, 0, 2 * (items - P));
+                ProfScope prof_(*c, 0, mults * (2ull * S4 * S4 + S4));
                 k<<<grid, dev::kBlock, 0, st>>>(arg(c->mod_n2), pieces, order, P, pass == 0 ? sorted : nullptr, src,
                                                 dst, next_job);
             }
@@ -860,16 +907,25 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
         }
         auto kf = dev::k_hist_finalize<S4, C::TH>;
         constexpr int NI = dev::kBlock / C::TH;
-        const int grid = occupancy_grid(*c, kf, 2 * nkeys, NI);
-        if (!tree) {
-            kf<<<grid, dev::kBlock, 0, st>>>(arg(c->mod_n2), count, final_idx, nkeys, final_part, d_out, mont_out);
+        auto kfd = dev::k_hist_finalize_p2<cs, C::TC>;
+        auto finalize = [&](uint32_t *dst, int mont) {
+            if (g->digits) {
+                // digits -> CRT residue mod n² (a key without rows keeps the literal 1)
+                kfd<<<occupancy_grid(*c, kfd, 2 * nkeys, dev::kBlock / C::TC), dev::kBlock, 0, st>>>(
+                    crt_args(c), count, final_idx, nkeys, final_part, dst, mont);
+            } else {
+                kf<<<occupancy_grid(*c, kf, 2 * nkeys, NI), dev::kBlock, 0, st>>>(arg(c->mod_n2), count, final_idx,
+                                                                                 nkeys, final_part, dst, mont);
+            }
             check_launch(*c);
+        };
+        if (!tree) {
+            finalize(d_out, mont_out);
             return;
         }
         // tree mode: all nodes in Montgomery form in the context's current buffer
         uint32_t *hist = (uint32_t *)grow(c->tree_buf[c->tree_cur ^ 1], (size_t)N * spn * S4 * 4 + 64);
-        kf<<<grid, dev::kBlock, 0, st>>>(arg(c->mod_n2), count, final_idx, nkeys, final_part, hist, 1);
-        check_launch(*c);
+        finalize(hist, 1);
         const bool derived_ok = pairs.empty() ||
             derive_siblings<cs>(c, B, hist, (const uint32_t *)c->tree_buf[c->tree_cur].p, d_pairs, pairs.size(), spn);
         if (!derived_ok) {
@@ -1512,6 +1568,7 @@ int sfxb_ctx_create(sfxb_ctx **out, int device, const uint32_t *n, uint32_t n_wo
                 host::MontHost mp(pr, s);
                 c->d_hR[i] = dev_big(*c, mp.to_mont(h), s);
                 c->d_cdec[i] = dev_big(*c, mp.from_mont(h), s);
+                c->d_negR[i] = dev_big(*c, host::sub(pr, mp.r1), s); // p − (R mod p)
             }
             // profiling units: 32×32 products per item of the exponentiation kernels
             const uint64_t pp = 2ull * s * s + s, pp2 = 2ull * (2 * s) * (2 * s) + 2 * s;

@@ -88,16 +88,17 @@ def test_group_encrypt_flags_non_coprime_blinding():
     assert np.array_equal(f1, fg) and sorted(np.nonzero(fg)[0].tolist()) == [7, 4096 + 11, count - 1]
 
 
+@pytest.mark.parametrize("private", [False, True])
 @pytest.mark.parametrize("kname,shape,shards", [("k512_c0ffee", (5000, 3, 16, 5), 3),
                                                  ("k2048_7", (700, 2, 8, 4), 2),
                                                  ("k512_c0ffee", (5, 2, 4, 3), 4)])
-def test_group_histogram_tree_mode_equals_single(kname, shape, shards):
+def test_group_histogram_tree_mode_equals_single(kname, shape, shards, private):
     """Row-sharded partials + cross-shard product over the slot slices +
     sibling subtraction on the slices == the single-device histogram and its
     reference counter, level by level (leaves, an empty child, trivial-zero
     ciphertexts, rows outside the frontier, a shard without rows)."""
     n_samples, J, K, depth = shape
-    grp, one = _group(kname, shards, private=False)
+    grp, one = _group(kname, shards, private=private)
     n, _, _ = key(kname)
     rng = random.Random(str(shape))
     cts = [rng.randrange(2, n * n) for _ in range(2 * n_samples)]

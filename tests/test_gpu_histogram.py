@@ -227,3 +227,67 @@ def test_decrypt_tree_sibling_reuse_is_bit_exact(kname, shape):
     h0, nn0, _ = hists[1]
     got, _ = ctx.decrypt_tree(11, h0, nn0, np.zeros(nn0, np.int32))
     assert np.array_equal(got.view(np.int64), ctx.decrypt(h0)[0].view(np.int64))
+
+
+# ---------------------------------------------------------------------------
+# Key holder (active party) histograms: CRT mod p², q² on base-p digits
+# (padic.cuh "K2 at the key holder") must equal the mod-n² product exactly.
+
+@pytest.mark.parametrize("kname", ["k512_c0ffee", "k2048_7"])
+@pytest.mark.parametrize("fx", ["fixture4", "random50"])
+def test_key_holder_accumulate_matches_reference_golden(kname, fx):
+    g = golden(kname)[fx]
+    n, p, q = key(kname)
+    ctx = _lib.Context(n, p, q)
+    cts = ints_to_words([int(x, 16) for x in g["cts"]], ctx.ct_words)
+    bins = np.array(g["inputs"]["bins"], np.uint16)
+    offs, rows = frontier(g["inputs"]["nodes"])
+    slots, adds = ctx.accumulate(cts, bins, offs, rows, g["inputs"]["n_bins"])
+    assert words_to_ints(slots) == [int(x, 16) for x in g["slots"]]
+    assert adds == g["counters_after_accumulate"][1]
+
+
+@pytest.mark.parametrize("kname,shape", [("k512_c0ffee", (700, 3, 16, 5, 0.02)), ("k2048_7", (300, 2, 8, 3, 0.05)),
+                                         ("k1024_7", (900, 1, 64, 2, 0.0))])
+def test_key_holder_histogram_equals_public_key_histogram(kname, shape):
+    """Direct, tree-mode and partial (Montgomery) histograms of the key holder
+    equal the passive party's mod-n² histograms bit for bit, incl. trivial
+    zeros, empty bins, leaves and an empty child; counters identical."""
+    import torch
+
+    n_samples, J, K, depth, ones = shape
+    n, p, q = key(kname)
+    priv, pub = _lib.Context(n, p, q), _lib.Context(n)
+    rng = random.Random(kname + "crt")
+    cts = [rng.randrange(2, n * n) for _ in range(2 * n_samples)]
+    for i in range(len(cts)):
+        if rng.random() < ones:
+            cts[i] = 1
+    cw = ints_to_words(cts, pub.ct_words)
+    bins = np.array([[rng.randrange(K) for _ in range(n_samples)] for _ in range(J)], np.uint16)
+    o_priv, o_pub = _lib.DeviceOps(priv), _lib.DeviceOps(pub)
+    g_priv, g_pub = o_priv.gh_upload(cw), o_pub.gh_upload(cw)
+    for nodes, parents in _random_tree(rng, n_samples, depth):
+        offs, rows = frontier(nodes)
+        par = np.array(parents, np.int32)
+        want, want_adds = o_pub.accumulate_tree_host(g_pub, bins, offs, rows, K, par)
+        got, adds = o_priv.accumulate_tree_host(g_priv, bins, offs, rows, K, par)
+        assert np.array_equal(got, want) and adds == want_adds
+        got2, adds2 = priv.accumulate(cw, bins, offs, rows, K)
+        assert np.array_equal(got2, want) and adds2 == want_adds
+    # Montgomery-form partials of two row halves reduce (K4) to the full histogram
+    nodes = [list(range(n_samples))]
+    offs, rows = frontier(nodes)
+    full, _ = pub.accumulate(cw, bins, offs, rows, K)
+    dev = torch.device("cuda:0")
+    d_bins = torch.from_numpy(bins.astype(np.int16).copy()).to(dev)
+    n_slots = J * K * 2
+    parts = torch.zeros((2, n_slots, priv.ct_words), dtype=torch.int32, device=dev)
+    for s_ in range(2):
+        sub = [[r for r in nodes[0] if r % 2 == s_]]
+        so, sr = frontier(sub)
+        o_priv.accumulate(g_priv, d_bins, J, torch.from_numpy(so.astype(np.int32)).to(dev), 1,
+                          torch.from_numpy(sr.astype(np.int32)).to(dev), len(sr), K, parts[s_], mont_out=True)
+    out = torch.zeros((n_slots, priv.ct_words), dtype=torch.int32, device=dev)
+    o_pub.reduce_partials(parts, 2, n_slots, out)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), full)

@@ -112,7 +112,8 @@ def main():
                 rate = units / dt if dt > 0 else None
                 rec.update({"per_s": rate, "seconds": dt, "units": int(units)})
                 if stats and stats[1] > 0:
-                    rec["roofline_frac"] = stats[2] * unit_products / (stats[1] / 1e3) / peak
+                    # kernel families count the 32x32->64 products their launches executed
+                    rec["roofline_frac"] = stats[2] / (stats[1] / 1e3) / peak
                     rec["kernel_ms"] = stats[1]
                 print(json.dumps(rec), flush=True)
     print(json.dumps({"imad_peak_products_per_s": peak, "sm_clock_mhz": mhz}), flush=True)
