@@ -104,6 +104,10 @@ struct CtxState {
     bool p2_digits = false;
     uint32_t *d_cdec[2] = {nullptr, nullptr}; // h_p·R⁻¹ mod p, h_q·R⁻¹ mod q   (s)
     uint32_t *d_negR[2] = {nullptr, nullptr}; // p − R mod p, q − R mod q          (s)
+    // passive-party K2 on base-n digits (padic.cuh): n fills its 2s limbs
+    bool n_digits = false;
+    uint32_t *d_negR_n = nullptr; // n − R mod n, R = 2^(64s)   (2s)
+    uint32_t *d_one_nd = nullptr; // digits of 1̃ [R mod n | R mod n]  (4s)
 
     // scratch (grown on demand, freed with the context)
     Buf scratch_table, tmp[4], host_pinned[2], io[6]; // io: host-API staging (grow-only)

@@ -574,5 +574,139 @@ __global__ void __launch_bounds__(kBlock) k_hist_finalize_p2(CrtArgs a, const ui
     }
 }
 
+
+// ------------------------------------------------------------------ K2 at a passive party
+//
+// Without the factorisation the same digit arithmetic works with n in the
+// role of p (nothing above needs primality, only n odd and n > R/2 for
+// R = 2^(64s)): X̃ = X·R² mod n² ≡ A·R + B·n, a multiplication mod n² is 3
+// CIOS passes mod n, 3·(2(2s)²+2s) = 24,768 products at 2048-bit n against
+// 2(4s)²+4s = 32,896 for one CIOS pass mod n².  The gh ciphertexts are
+// already in Montgomery form mod n² (= X̃); k_gh_split_n splits them into
+// [A | B] in place.
+
+struct NdArgs {
+    ModArg mod_n;            // 2s
+    ModArg mod_n2;           // 4s
+    const uint32_t *negR;    // n − R mod n              (2s)
+    const uint32_t *one;     // digits of 1̃: [R mod n | R mod n]   (4s)
+    const uint32_t *n4;      // n zero-extended           (4s)
+};
+
+template <int S, int TPI>
+__global__ void __launch_bounds__(kBlock) k_gh_split_n(NdArgs a, uint32_t *gh, size_t count) {
+    constexpr int L = S / TPI, NI = kBlock / TPI;
+    __shared__ uint2 sB[S / 2 * NI];
+    const Stage st = make_stage<TPI>(sB);
+    const ModRef M = a.mod_n.ref();
+    uint32_t N[L];
+    load_const<S, TPI>(N, M, kMod);
+    SFXB_UNIFORM_LOOP(e, active, count) {
+        uint32_t *c = gh + e * 2 * S;
+        uint32_t lo[L], hi[L], A[L], B[L];
+        load_lane<S, TPI>(lo, c);
+        load_lane<S, TPI>(hi, c + S);
+        p2_split<S, TPI>(A, B, lo, hi, st, N, M.np, M.w + kOne * S);
+        if (active) { // each lane rewrites exactly the limbs it read
+            store_lane<S, TPI>(c, A);
+            store_lane<S, TPI>(c + S, B);
+        }
+    }
+}
+
+// Segmented product pass on base-n digits (the k_seg_prod protocol; an
+// instance past the end of its piece multiplies by the digits of 1̃, which
+// leaves (A, B) unchanged, so every instance runs the same passes).
+template <int S, int TPI, int C>
+__global__ void __launch_bounds__(kBlock) k_seg_prod_nd(NdArgs a, const Piece *pieces, const uint32_t *order,
+                                                        size_t n_pieces, const uint32_t *sorted, const uint32_t *src,
+                                                        uint32_t *dst, unsigned long long *next_job) {
+    constexpr int L = S / TPI, NI = kBlock / TPI, NIW = 32 / TPI;
+    __shared__ uint2 sB[S / 2 * NI];
+    const Stage st = make_stage<TPI>(sB);
+    const ModRef M = a.mod_n.ref();
+    uint32_t N[L];
+    load_const<S, TPI>(N, M, kMod);
+    const size_t total = 2 * n_pieces;
+    for (;;) {
+        unsigned long long base = 0;
+        if ((threadIdx.x & 31) == 0) base = atomicAdd(next_job, (unsigned long long)NIW);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= total) break;
+        const size_t mine = base + (threadIdx.x & 31) / TPI;
+        const bool active = mine < total;
+        const size_t job = active ? mine : total - 1;
+        const uint32_t pidx = order[job >> 1];
+        const Piece pc = pieces[pidx];
+        const uint32_t g = (uint32_t)(job & 1);
+        auto item_ptr = [&](uint32_t k) -> const uint32_t * {
+            const size_t idx = sorted ? (2 * (size_t)sorted[pc.start + k] + g) : (2 * (size_t)(pc.start + k) + g);
+            return src + idx * 2 * S;
+        };
+        uint32_t A[L], B[L];
+        const uint32_t *p0 = item_ptr(0);
+        load_lane<S, TPI>(A, p0);
+        load_lane<S, TPI>(B, p0 + S);
+        for (int k = 1; k < C; ++k) {
+            const bool more = active && (uint32_t)k < pc.len;
+            if (!__any_sync(0xffffffffu, more)) break; // warp-uniform exit
+            p2_mul<S, TPI>(A, B, more ? item_ptr((uint32_t)k) : a.one, false, st, N, M.np, M.w + kOne * S, a.negR);
+        }
+        if (active) {
+            uint32_t *d = dst + (2 * (size_t)pidx + g) * 2 * S;
+            store_lane<S, TPI>(d, A);
+            store_lane<S, TPI>(d + S, B);
+        }
+    }
+}
+
+// Output slot: count == 0 -> 1 (Montgomery one for partials); else the
+// key's final digits [A | B] -> plain c = MM4(A, R) + MM4(B, n) (mod n²),
+// Montgomery form c·R4 for partials.
+template <int s, int TPI>
+__global__ void __launch_bounds__(kBlock) k_hist_finalize_nd(NdArgs a, const uint32_t *count,
+                                                             const uint32_t *final_idx, size_t nkeys,
+                                                             const uint32_t *partial, uint32_t *out, int mont_out) {
+    constexpr int S2 = 2 * s, S4 = 4 * s, L4 = S4 / TPI, NI = kBlock / TPI;
+    __shared__ uint2 sB[S4 / 2 * NI];
+    const Stage st = make_stage<TPI>(sB);
+    const ModRef M4 = a.mod_n2.ref();
+    uint32_t N4[L4];
+    load_const<S4, TPI>(N4, M4, kMod);
+    const int tl = inst_lane<TPI>();
+    const bool low = tl * L4 < S2;
+    SFXB_UNIFORM_LOOP(slot, active, 2 * nkeys) {
+        const size_t key = slot >> 1;
+        const uint32_t g = (uint32_t)(slot & 1);
+        const bool empty = count[key] == 0;
+        const uint32_t *pp = empty ? out + slot * S4 : partial + (2 * (size_t)final_idx[key] + g) * S4;
+        uint32_t av[L4], bv[L4], Rc[L4], nc[L4], u[L4], v[L4];
+        load_lane<S4, TPI>(av, pp);
+        relayout<S4, S4, TPI>(bv, av, st);
+#pragma unroll
+        for (int k = 0; k < L4; ++k) {
+            const int limb = tl * L4 + k;
+            bv[k] = limb < S2 ? staged_word<TPI>(st, limb + S2) : 0u;
+            av[k] = low ? av[k] : 0u;
+            Rc[k] = limb == S2 ? 1u : 0u;
+        }
+        __syncwarp();
+        load_lane<S4, TPI>(nc, a.n4);
+        mmul<S4, TPI>(u, av, Rc, st, N4, M4.np);
+        mmul<S4, TPI>(v, bv, nc, st, N4, M4.np);
+        mod_add<S4, TPI>(u, u, v, N4);
+        if (mont_out) {
+            load_const<S4, TPI>(v, M4, kR2);
+            mmul<S4, TPI>(u, v, u, st, N4, M4.np);
+        }
+        if (empty) {
+            if (mont_out) load_const<S4, TPI>(u, M4, kOne);
+            else set_small<L4, TPI>(u, 1u);
+        }
+        __syncwarp();
+        if (active) store_lane<S4, TPI>(out + slot * S4, u);
+    }
+}
+
 } // namespace dev
 } // namespace sfxb
