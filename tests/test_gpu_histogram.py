@@ -291,3 +291,33 @@ def test_key_holder_histogram_equals_public_key_histogram(kname, shape):
     out = torch.zeros((n_slots, priv.ct_words), dtype=torch.int32, device=dev)
     o_pub.reduce_partials(parts, 2, n_slots, out)
     assert np.array_equal(out.cpu().numpy().view(np.uint32), full)
+
+
+@pytest.mark.parametrize("private", [False, True])
+def test_histogram_mod_n2_path_for_keys_short_of_their_class(private):
+    """n (and p, q) short of their limb class: K2 falls back to the mod-n²
+    CIOS segmented product; residues equal Python's products mod n²."""
+    from test_gpu_paillier import _prime
+
+    rng = random.Random("short-n")
+    p, q = _prime(rng, 400), _prime(rng, 400)
+    n = p * q
+    ctx = _lib.Context(n, p, q) if private else _lib.Context(n)
+    n_samples, J, K = 300, 2, 8
+    cts = [rng.randrange(2, n * n) for _ in range(2 * n_samples)]
+    cts[5] = 1
+    cw = ints_to_words(cts, ctx.ct_words)
+    bins = np.array([[rng.randrange(K) for _ in range(n_samples)] for _ in range(J)], np.uint16)
+    nodes = [sorted(rng.sample(range(n_samples), 120)), sorted(rng.sample(range(n_samples), 90))]
+    offs, rows = frontier(nodes)
+    slots, _ = ctx.accumulate(cw, bins, offs, rows, K)
+    got = words_to_ints(slots)
+    for ni, nd in enumerate(nodes):
+        for f in range(J):
+            for b in range(K):
+                for g in range(2):
+                    want = 1
+                    for r in nd:
+                        if bins[f][r] == b:
+                            want = want * cts[2 * r + g] % (n * n)
+                    assert got[((ni * J + f) * K + b) * 2 + g] == want
