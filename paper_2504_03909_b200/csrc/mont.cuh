@@ -223,6 +223,55 @@ __device__ __forceinline__ uint32_t cios_step(uint32_t (&E)[L], uint32_t (&Q)[L]
     return q;
 }
 
+// CIOS step of the two-product pass: acc += A·b_i + C·d_i, then q_i·M and
+// the shift (cios_step with a second E/O chain pair; the accumulator stays
+// below 3M, its extra bit lives in Z).
+template <int L, int TPI>
+__device__ __forceinline__ void cios_step2(uint32_t (&E)[L], uint32_t (&Q)[L], uint32_t &Z,
+                                           const uint32_t (&A)[L], const uint32_t (&C)[L], const uint32_t (&N)[L],
+                                           uint32_t bi, uint32_t di, uint32_t np) {
+    const int t = inst_lane<TPI>();
+    uint32_t Zn;
+    const uint32_t u0 = from_above<TPI>(Q[0]);
+    const uint32_t u1 = from_above<TPI>(Q[1]);
+    const uint32_t x = (t == 0) ? Q[1] : 0u;
+    E[0] = add_cc(E[0], x);
+#pragma unroll
+    for (int k = 0; k < L / 2 - 1; ++k)
+        madc_w_cc(Q[2 * k], Q[2 * k + 1], A[2 * k + 1], bi, Q[2 * k + 2], Q[2 * k + 3]);
+    madc_w_cc(Q[L - 2], Q[L - 1], A[L - 1], bi, u0, u1);
+    Zn = addc(0u, 0u);
+    Q[L - 1] = add_cc(Q[L - 1], Z);
+    Zn = addc(Zn, 0u);
+    // O += C_odd·d_i
+    mad_w_cc(Q[0], Q[1], C[1], di, Q[0], Q[1]);
+#pragma unroll
+    for (int k = 1; k < L / 2; ++k) madc_w_cc(Q[2 * k], Q[2 * k + 1], C[2 * k + 1], di, Q[2 * k], Q[2 * k + 1]);
+    Zn = addc(Zn, 0u);
+    // E += A_even·b_i
+    mad_w_cc(E[0], E[1], A[0], bi, E[0], E[1]);
+#pragma unroll
+    for (int k = 1; k < L / 2; ++k) madc_w_cc(E[2 * k], E[2 * k + 1], A[2 * k], bi, E[2 * k], E[2 * k + 1]);
+    Q[L - 1] = addc_cc(Q[L - 1], 0u);
+    Zn = addc(Zn, 0u);
+    // E += C_even·d_i
+    mad_w_cc(E[0], E[1], C[0], di, E[0], E[1]);
+#pragma unroll
+    for (int k = 1; k < L / 2; ++k) madc_w_cc(E[2 * k], E[2 * k + 1], C[2 * k], di, E[2 * k], E[2 * k + 1]);
+    Q[L - 1] = addc_cc(Q[L - 1], 0u);
+    Zn = addc(Zn, 0u);
+    const uint32_t q = inst_bcast<TPI>(E[0] * np, 0);
+    mad_w_cc(Q[0], Q[1], N[1], q, Q[0], Q[1]);
+#pragma unroll
+    for (int k = 1; k < L / 2; ++k) madc_w_cc(Q[2 * k], Q[2 * k + 1], N[2 * k + 1], q, Q[2 * k], Q[2 * k + 1]);
+    Zn = addc(Zn, 0u);
+    mad_w_cc(E[0], E[1], N[0], q, E[0], E[1]);
+#pragma unroll
+    for (int k = 1; k < L / 2; ++k) madc_w_cc(E[2 * k], E[2 * k + 1], N[2 * k], q, E[2 * k], E[2 * k + 1]);
+    Q[L - 1] = addc_cc(Q[L - 1], 0u);
+    Z = addc(Zn, 0u);
+}
+
 // Carry-lookahead across the instance's lanes: lane t adds 1 if a carry
 // reaches it.  g = lane generates a carry out, p = lane propagates (all ones).
 // Returns the carry out of the top lane.
@@ -281,12 +330,45 @@ __device__ __forceinline__ bool final_sub(uint32_t (&R)[L], uint32_t over, const
     return ge;
 }
 
+// V = R + over·2^(32S) (over small): subtract M once when V >= M, keeping
+// the overflow word (the two-product pass ends below 3M).
+template <int L, int TPI>
+__device__ __forceinline__ void cond_sub_wide(uint32_t (&R)[L], uint32_t &over, const uint32_t (&N)[L]) {
+    uint32_t D[L];
+    D[0] = sub_cc(R[0], N[0]);
+#pragma unroll
+    for (int k = 1; k < L; ++k) D[k] = subc_cc(R[k], N[k]);
+    uint32_t bout = subc(0u, 0u) & 1u;
+    uint32_t top_borrow;
+    if constexpr (TPI == 1) {
+        top_borrow = bout;
+    } else {
+        bool zero = true;
+#pragma unroll
+        for (int k = 0; k < L; ++k) zero &= (D[k] == 0u);
+        const uint32_t G = inst_ballot<TPI>(bout != 0);
+        const uint32_t P = inst_ballot<TPI>(zero);
+        const uint64_t sum = (uint64_t)P + ((uint64_t)G << 1);
+        const uint32_t bin = (uint32_t)(sum ^ P);
+        if ((bin >> inst_lane<TPI>()) & 1u) {
+            D[0] = sub_cc(D[0], 1u);
+#pragma unroll
+            for (int k = 1; k < L; ++k) D[k] = subc_cc(D[k], 0u);
+        }
+        top_borrow = (uint32_t)(sum >> TPI) & 1u;
+    }
+    const bool ge = over != 0 || top_borrow == 0;
+#pragma unroll
+    for (int k = 0; k < L; ++k) R[k] = ge ? D[k] : R[k];
+    over = ge ? over - top_borrow : over;
+}
+
 // The end of a CIOS pass: after the last step E = Y (the old even array,
 // still unshifted) and X holds the odd-aligned array, which becomes the
 // even-aligned window; Y shifts down one limb: window limb k = X[k] + Y[k+1]
 // (+ lane t+1's Y[0]).  Then carries across lanes and the final conditional
 // subtraction; returns whether M was subtracted.
-template <int L, int TPI>
+template <int L, int TPI, bool WIDE = false>
 __device__ __forceinline__ bool mont_tail(uint32_t (&r)[L], const uint32_t (&X)[L], const uint32_t (&Y)[L],
                                           uint32_t Z, const uint32_t (&N)[L]) {
     const uint32_t u0 = from_above<TPI>(Y[0]);
@@ -309,6 +391,7 @@ __device__ __forceinline__ bool mont_tail(uint32_t (&r)[L], const uint32_t (&X)[
         uint32_t ripple = resolve_carries<L, TPI>(R, c2);
         over = ctop + ripple;
     }
+    if constexpr (WIDE) cond_sub_wide<L, TPI>(R, over, N); // < 3M -> < 2M
     const bool ge = final_sub<L, TPI>(R, over, N);
 #pragma unroll
     for (int k = 0; k < L; ++k) r[k] = R[k];
@@ -403,6 +486,28 @@ __device__ __forceinline__ bool mont_mul_sub(uint32_t (&r)[S / TPI], uint32_t (&
     }
     borrow = bw;
     return mont_tail<L, TPI>(r, X, Y, Z, N);
+}
+
+// r = (A·B + C·D)·2^(−32S) mod M with A, C < M in registers and B, D staged
+// in shared memory (sB, sD; store_b layout): one CIOS pass with two products
+// per step — 3S²+S products instead of 2·(2S²+S) for two passes.
+template <int S, int TPI>
+__device__ __forceinline__ void mont_mul2(uint32_t (&r)[S / TPI], const uint32_t (&A)[S / TPI],
+                                          const uint32_t (&C)[S / TPI], const uint2 *sB, const uint2 *sD, int inst,
+                                          const uint32_t (&N)[S / TPI], uint32_t np) {
+    constexpr int L = S / TPI, NIc = 128 / TPI;
+    constexpr int U = L / 2;
+    uint32_t X[L], Y[L], Z = 0;
+#pragma unroll
+    for (int k = 0; k < L; ++k) X[k] = Y[k] = 0;
+#pragma unroll U
+    for (int i = 0; i < S / 2; ++i) {
+        const uint2 b = sB[b_slot<NIc>(i, inst)];
+        const uint2 d = sD[b_slot<NIc>(i, inst)];
+        cios_step2<L, TPI>(X, Y, Z, A, C, N, b.x, d.x, np);
+        cios_step2<L, TPI>(Y, X, Z, A, C, N, b.y, d.y, np);
+    }
+    mont_tail<L, TPI, true>(r, X, Y, Z, N);
 }
 
 // ---------------------------------------------------------------- global <-> lane limbs

@@ -30,51 +30,49 @@ __device__ __forceinline__ void stage_regs(const Stage &st, const uint32_t (&v)[
 }
 
 // One Montgomery product mod p² on digits: (A, B) <- (A, B) ⊛ (A2, B2),
-// or the square when `square` (A2, B2 unused).  2 or 3 CIOS passes through
-// ONE inlined mont_mul_sub call site (the hot loop stays one copy of the
-// unrolled CIOS body):
-//   pass 0: v = MM(A, B | B2)            (doubled for a square)
+// or the square when `square` (A2, B2 unused).  Two CIOS passes:
+//   pass 0: square:   v = 2·MM(A, B)
+//           multiply: v = MM2(A·B2 + A2·B)   (one two-product pass, mont_mul2)
 //   pass 1: t, ge = MM(A, A | A2), v -= m on the fly (borrow bw);  A <- t
-//   pass 2: v2 = MM(B, A2)                (multiply only)
-// then B <- v − m + ge·R (+ v2) (mod p): v − m + (ge − bw)·R with v − m
-// (mod R) < R < 2p.  Rmod = R mod p, negR = p − R mod p (global).
+// then B <- v − m + ge·R (mod p): v − m + (ge − bw)·R with v − m (mod R)
+// < R < 2p.  Rmod = R mod p, negR = p − R mod p (global).  Products: square
+// 2·(2s²+s), multiply (3s²+s) + (2s²+s).  One inlined copy of each CIOS body.
 template <int s, int TPI>
 __device__ __forceinline__ void p2_mul(uint32_t (&A)[s / TPI], uint32_t (&B)[s / TPI], const uint32_t *g2,
-                                       bool square, const Stage &st, const uint32_t (&N)[s / TPI], uint32_t np,
-                                       const uint32_t *Rmod, const uint32_t *negR) {
+                                       bool square, const Stage &st, uint2 *sD, const uint32_t (&N)[s / TPI],
+                                       uint32_t np, const uint32_t *Rmod, const uint32_t *negR) {
     constexpr int L = s / TPI;
     uint32_t v[L], x[L];
     bool ge = false;
     uint32_t bw = 0;
-    const int passes = square ? 2 : 3;
 #pragma unroll 1
-    for (int c = 0; c < passes; ++c) {
-        {
-            uint32_t tmp[L];
-            if (square) {
-#pragma unroll
-                for (int k = 0; k < L; ++k) tmp[k] = c == 0 ? B[k] : A[k];
-            } else {
-                load_lane<s, TPI>(tmp, g2 + (c == 0 ? s : 0)); // B2 for pass 0, A2 for passes 1/2
+    for (int c = 0; c < 2; ++c) {
+        if (c == 0 && !square) {
+            {
+                uint32_t tmp[L];
+                load_lane<s, TPI>(tmp, g2 + s); // B2
+                stage_b<s, TPI>(st, tmp);
             }
-            stage_b<s, TPI>(st, tmp);
-        }
-#pragma unroll
-        for (int k = 0; k < L; ++k) x[k] = c == 2 ? B[k] : A[k];
-        uint32_t r[L], b;
-        const bool g = mont_mul_sub<s, TPI>(r, v, x, st.sB, st.inst, N, np, c == 1, b);
-        if (c == 0) {
-#pragma unroll
-            for (int k = 0; k < L; ++k) v[k] = r[k];
-            if (square) mod_add<s, TPI>(v, v, v, N);
-        } else if (c == 1) {
-            ge = g;
-            bw = b;
-#pragma unroll
-            for (int k = 0; k < L; ++k) A[k] = r[k];
+            stage_b<s, TPI>(Stage{sD, st.NI, st.inst}, B);
+            load_lane<s, TPI>(x, g2); // A2 (register operand, and pass 1's scanned operand)
+            mont_mul2<s, TPI>(v, A, x, st.sB, sD, st.inst, N, np);
         } else {
+            {
+                uint32_t tmp[L];
 #pragma unroll
-            for (int k = 0; k < L; ++k) x[k] = r[k]; // v2
+                for (int k = 0; k < L; ++k) tmp[k] = c == 0 ? B[k] : (square ? A[k] : x[k]);
+                stage_b<s, TPI>(st, tmp);
+            }
+            uint32_t r[L], b;
+            const bool g = mont_mul_sub<s, TPI>(r, v, A, st.sB, st.inst, N, np, c == 1, b);
+            if (c == 0) {
+                mod_add<s, TPI>(v, r, r, N);
+            } else {
+                ge = g;
+                bw = b;
+#pragma unroll
+                for (int k = 0; k < L; ++k) A[k] = r[k];
+            }
         }
     }
     reduce_once<s, TPI>(v, v, N);
@@ -87,7 +85,6 @@ __device__ __forceinline__ void p2_mul(uint32_t (&A)[s / TPI], uint32_t (&B)[s /
         for (int k = 0; k < L; ++k) tmp[k] = delta ? tmp[k] : 0u;
         mod_add<s, TPI>(v, v, tmp, N);
     }
-    if (!square) mod_add<s, TPI>(v, v, x, N);
 #pragma unroll
     for (int k = 0; k < L; ++k) B[k] = v[k];
 }
@@ -98,7 +95,7 @@ __device__ __forceinline__ void p2_mul(uint32_t (&A)[s / TPI], uint32_t (&B)[s /
 // x^(2^w − 1), then x².
 template <int s, int TPI>
 __device__ __forceinline__ void p2_pow(uint32_t (&A)[s / TPI], uint32_t (&B)[s / TPI], const uint8_t *ops,
-                                       int n_ops, int w, uint32_t *table, const Stage &st,
+                                       int n_ops, int w, uint32_t *table, const Stage &st, uint2 *sD,
                                        const uint32_t (&N)[s / TPI], uint32_t np, const uint32_t *Rmod,
                                        const uint32_t *negR) {
     const int T = 1 << (w - 1);
@@ -137,7 +134,7 @@ __device__ __forceinline__ void p2_pow(uint32_t (&A)[s / TPI], uint32_t (&B)[s /
                 g2 = table + 2 * s * (d >> 1);
             }
         }
-        p2_mul<s, TPI>(A, B, g2, square, st, N, np, Rmod, negR);
+        p2_mul<s, TPI>(A, B, g2, square, st, sD, N, np, Rmod, negR);
         if (j < T - 1) {
             if (j < 0) {
                 store_lane<s, TPI>(x2, A);
@@ -155,12 +152,13 @@ __device__ __forceinline__ void p2_pow(uint32_t (&A)[s / TPI], uint32_t (&B)[s /
     }
 }
 
-// CIOS passes (2s²+s products each) of p2_pow for a sliding-window program:
-// squarings 2 passes, multiplies 3.
-inline unsigned long long p2_pow_passes(const uint8_t *ops, int n_ops, int w) {
-    unsigned long long passes = 2ull + 3ull * ((1ull << (w - 1)) - 1);
-    for (int i = 1; i < n_ops; ++i) passes += 2ull * ops[2 * i] + (ops[2 * i + 1] ? 3ull : 0ull);
-    return passes;
+// 32×32 products of p2_pow for a sliding-window program at s limbs
+// (p2_mul: square 2·(2s²+s), multiply (3s²+s) + (2s²+s)).
+inline unsigned long long p2_pow_products(const uint8_t *ops, int n_ops, int w, int s) {
+    const unsigned long long sq = 2ull * (2ull * s * s + s), mul = (3ull * s * s + s) + (2ull * s * s + s);
+    unsigned long long prod = sq + mul * ((1ull << (w - 1)) - 1);
+    for (int i = 1; i < n_ops; ++i) prod += sq * ops[2 * i] + (ops[2 * i + 1] ? mul : 0ull);
+    return prod;
 }
 
 // Digits of X̃ (a canonical residue mod p², 2s limbs: hi·R + lo, hi < p):
@@ -246,7 +244,7 @@ struct P2Args {
 template <int s, int TPI, int W, int MODE>
 __global__ void __launch_bounds__(kBlock, SFXB_P2_MINB) k_p2_pow(P2Args a) {
     constexpr int L = s / TPI, NI = kBlock / TPI;
-    __shared__ uint2 sB[s / 2 * NI];
+    __shared__ uint2 sB[s / 2 * NI], sD[s / 2 * NI];
     const Stage st = make_stage<TPI>(sB);
     const int which = (int)blockIdx.y; // one prime per block row: uniform digits
     const size_t gi = ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * NI + st.inst;
@@ -303,7 +301,8 @@ __global__ void __launch_bounds__(kBlock, SFXB_P2_MINB) k_p2_pow(P2Args a) {
             load_lane<s, TPI>(hi, src + s);
             p2_split<s, TPI>(A, B, lo, hi, st, N, M.np, M.w + kOne * s);
         }
-        p2_pow<s, TPI>(A, B, a.ops[which], a.n_ops[which], W, table, st, N, M.np, M.w + kOne * s, a.negR[which]);
+        p2_pow<s, TPI>(A, B, a.ops[which], a.n_ops[which], W, table, st, sD, N, M.np, M.w + kOne * s,
+                       a.negR[which]);
         if constexpr (MODE == 0) {
             uint32_t *dst = a.out + (item * 2 + which) * 2 * s;
             if (active) {
@@ -457,7 +456,7 @@ __global__ void __launch_bounds__(kBlock) k_seg_prod_p2(CrtArgs a, const Piece *
                                                         size_t n_pieces, const uint32_t *sorted, const uint32_t *src,
                                                         uint32_t *dst, unsigned long long *next_job) {
     constexpr int L = s;
-    __shared__ uint2 sB[s / 2 * kBlock];
+    __shared__ uint2 sB[s / 2 * kBlock], sD[s / 2 * kBlock];
     const Stage st = make_stage<1>(sB);
     const size_t total = 4 * n_pieces;
     for (;;) {
@@ -489,7 +488,7 @@ __global__ void __launch_bounds__(kBlock) k_seg_prod_p2(CrtArgs a, const Piece *
                     for (int o = 0; o < 2 * s; o += 32)
                         asm volatile("prefetch.global.L2 [%0];" ::"l"(nx + o));
                 }
-                p2_mul<s, 1>(A, B, item_ptr(k), false, st, N, M.np, M.w + kOne * s, a.negR[pr]);
+                p2_mul<s, 1>(A, B, item_ptr(k), false, st, sD, N, M.np, M.w + kOne * s, a.negR[pr]);
             }
             uint32_t *d = dst + (2 * (size_t)pidx + g) * 4 * s + pr * 2 * s;
             store_lane<s, 1>(d, A);
@@ -622,7 +621,7 @@ __global__ void __launch_bounds__(kBlock) k_seg_prod_nd(NdArgs a, const Piece *p
                                                         size_t n_pieces, const uint32_t *sorted, const uint32_t *src,
                                                         uint32_t *dst, unsigned long long *next_job) {
     constexpr int L = S / TPI, NI = kBlock / TPI, NIW = 32 / TPI;
-    __shared__ uint2 sB[S / 2 * NI];
+    __shared__ uint2 sB[S / 2 * NI], sD[S / 2 * NI];
     const Stage st = make_stage<TPI>(sB);
     const ModRef M = a.mod_n.ref();
     uint32_t N[L];
@@ -650,7 +649,8 @@ __global__ void __launch_bounds__(kBlock) k_seg_prod_nd(NdArgs a, const Piece *p
         for (int k = 1; k < C; ++k) {
             const bool more = active && (uint32_t)k < pc.len;
             if (!__any_sync(0xffffffffu, more)) break; // warp-uniform exit
-            p2_mul<S, TPI>(A, B, more ? item_ptr((uint32_t)k) : a.one, false, st, N, M.np, M.w + kOne * S, a.negR);
+            p2_mul<S, TPI>(A, B, more ? item_ptr((uint32_t)k) : a.one, false, st, sD, N, M.np, M.w + kOne * S,
+                           a.negR);
         }
         if (active) {
             uint32_t *d = dst + (2 * (size_t)pidx + g) * 2 * S;

@@ -899,9 +899,9 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
             // each piece: len − 1 multiplications, G and H; profiling counts 32×32 products
             const uint64_t mults = 2 * (items - P);
             if (g->digits) {
-                // CRT on digits: 2 primes × 3 CIOS passes mod p per multiplication
-                const uint64_t pp = 2ull * cs * cs + cs;
-                ProfScope prof_(*c, 0, mults * 6 * pp);
+                // CRT on digits: 2 primes × (two-product pass + one pass) mod p per multiplication
+                const uint64_t pp = 5ull * cs * cs + 2 * cs;
+                ProfScope prof_(*c, 0, mults * 2 * pp);
                 if (Cp == (uint32_t)kPieceLong) {
                     auto k = dev::k_seg_prod_p2<cs, kPieceLong>;
                     k<<<occupancy_grid(*c, k, 4 * P, dev::kBlock), dev::kBlock, 0, st>>>(
@@ -912,9 +912,9 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
                         crt_args(c), pieces, order, P, pass == 0 ? sorted : nullptr, src, dst, next_job);
                 }
             } else if (g->digits_n) {
-                // base-n digits: 3 CIOS passes mod n per multiplication
-                const uint64_t pn = 2ull * (2 * cs) * (2 * cs) + 2 * cs;
-                ProfScope prof_(*c, 0, mults * 3 * pn);
+                // base-n digits: two-product pass + one pass mod n per multiplication
+                const uint64_t pn = 5ull * (2 * cs) * (2 * cs) + 2 * (2 * cs);
+                ProfScope prof_(*c, 0, mults * pn);
                 constexpr int NIn = dev::kBlock / C::TND;
                 if (Cp == (uint32_t)kPieceLong) {
                     auto k = dev::k_seg_prod_nd<2 * cs, C::TND, kPieceLong>;
@@ -1633,8 +1633,8 @@ int sfxb_ctx_create(sfxb_ctx **out, int device, const uint32_t *n, uint32_t n_wo
                 const Win &w = host_window[i];
                 c->prod_enc += w.e1 * pp; // step 1 mod p
                 if (c->p2_digits) {
-                    c->prod_enc += (dev::p2_pow_passes(w.dig_pr.data(), (int)w.dig_pr.size() / 2, kWindow) + 2) * pp;
-                    c->prod_dec += (dev::p2_pow_passes(w.dig_pm1.data(), (int)w.dig_pm1.size() / 2, kWindow) + 2) * pp;
+                    c->prod_enc += dev::p2_pow_products(w.dig_pr.data(), (int)w.dig_pr.size() / 2, kWindow, s) + 2 * pp;
+                    c->prod_dec += dev::p2_pow_products(w.dig_pm1.data(), (int)w.dig_pm1.size() / 2, kWindow, s) + 2 * pp;
                 } else {
                     c->prod_enc += w.pr * pp2;
                     c->prod_dec += w.pm1 * pp2;
