@@ -104,6 +104,7 @@ struct CtxState {
     bool p2_digits = false;
     uint32_t *d_cdec[2] = {nullptr, nullptr}; // h_p·R⁻¹ mod p, h_q·R⁻¹ mod q   (s)
     uint32_t *d_negR[2] = {nullptr, nullptr}; // p − R mod p, q − R mod q          (s)
+    uint32_t *d_one_p2[2] = {nullptr, nullptr}; // digits of 1̃ mod p², q²: [R mod p | R mod p]  (2s)
     // passive-party K2 on base-n digits (padic.cuh): n fills its 2s limbs
     bool n_digits = false;
     uint32_t *d_negR_n = nullptr; // n − R mod n, R = 2^(64s)   (2s)

@@ -403,6 +403,7 @@ struct CrtArgs {
     const uint32_t *qq_inv_m; // (q²)⁻¹·R2 mod p²       (2s)
     const uint32_t *q2R_n2;   // q²·R4 mod n²           (4s)
     const uint32_t *negR[2];  // p − R mod p            (s)
+    const uint32_t *one[2];   // digits of 1̃ mod p²: [R mod p | R mod p]  (2s)
 };
 
 // plain ciphertexts (4s words each, in place) -> digits of c mod p², c mod q²
@@ -449,50 +450,58 @@ __global__ void __launch_bounds__(kBlock) k_gh_digits(CrtArgs a, uint32_t *gh, s
     }
 }
 
-// Segmented product pass on digits (one lane per job; the k_seg_prod
-// protocol).  Job j = 4·rank + 2·gh + prime over the length-sorted pieces.
-template <int s, int C>
+// Segmented product pass on digits (the k_seg_prod protocol).  Job j =
+// 4·rank + 2·gh + prime over the length-sorted pieces; TPI lanes per job (the
+// prime may differ between the instances of a warp: each loads its own
+// modulus).  An instance past the end of its piece multiplies by the digits
+// of 1̃, so every instance of a warp runs the same passes.
+template <int s, int TPI, int C>
 __global__ void __launch_bounds__(kBlock) k_seg_prod_p2(CrtArgs a, const Piece *pieces, const uint32_t *order,
                                                         size_t n_pieces, const uint32_t *sorted, const uint32_t *src,
                                                         uint32_t *dst, unsigned long long *next_job) {
-    constexpr int L = s;
-    __shared__ uint2 sB[s / 2 * kBlock], sD[s / 2 * kBlock];
-    const Stage st = make_stage<1>(sB);
+    constexpr int L = s / TPI, NI = kBlock / TPI, NIW = 32 / TPI;
+    __shared__ uint2 sB[s / 2 * NI], sD[s / 2 * NI];
+    const Stage st = make_stage<TPI>(sB);
     const size_t total = 4 * n_pieces;
     for (;;) {
         unsigned long long base = 0;
-        if ((threadIdx.x & 31) == 0) base = atomicAdd(next_job, 32ull);
+        if ((threadIdx.x & 31) == 0) base = atomicAdd(next_job, (unsigned long long)NIW);
         base = __shfl_sync(0xffffffffu, base, 0);
         if (base >= total) break;
-        const size_t job = base + (threadIdx.x & 31);
-        if (job < total) {
-            const uint32_t pidx = order[job >> 2];
-            const Piece pc = pieces[pidx];
-            const uint32_t g = (uint32_t)((job >> 1) & 1), pr = (uint32_t)(job & 1);
-            const ModRef M = a.mod_p[pr].ref();
-            uint32_t N[L], A[L], B[L];
-            load_const<s, 1>(N, M, kMod);
-            auto item_ptr = [&](uint32_t k) -> const uint32_t * {
-                const size_t idx = sorted ? (2 * (size_t)sorted[pc.start + k] + g) : (2 * (size_t)(pc.start + k) + g);
-                return src + idx * 4 * s + pr * 2 * s;
-            };
-            const uint32_t *p0 = item_ptr(0);
-            load_lane<s, 1>(A, p0);
-            load_lane<s, 1>(B, p0 + s);
-            for (uint32_t k = 1; k < pc.len; ++k) {
-                // the rows are gathered at random from a gh buffer far larger
-                // than L2: fetch the next item while this one is multiplied
-                if (k + 1 < pc.len) {
-                    const uint32_t *nx = item_ptr(k + 1);
+        const size_t mine = base + (threadIdx.x & 31) / TPI;
+        const bool active = mine < total;
+        const size_t job = active ? mine : total - 1;
+        const uint32_t pidx = order[job >> 2];
+        const Piece pc = pieces[pidx];
+        const uint32_t g = (uint32_t)((job >> 1) & 1), pr = (uint32_t)(job & 1);
+        // (selects, not a dynamic index into the parameter arrays: no local copy)
+        const ModRef M = (pr ? a.mod_p[1] : a.mod_p[0]).ref();
+        const uint32_t *one = pr ? a.one[1] : a.one[0], *negR = pr ? a.negR[1] : a.negR[0];
+        uint32_t N[L], A[L], B[L];
+        load_const<s, TPI>(N, M, kMod);
+        auto item_ptr = [&](uint32_t k) -> const uint32_t * {
+            const size_t idx = sorted ? (2 * (size_t)sorted[pc.start + k] + g) : (2 * (size_t)(pc.start + k) + g);
+            return src + idx * 4 * s + pr * 2 * s;
+        };
+        const uint32_t *p0 = item_ptr(0);
+        load_lane<s, TPI>(A, p0);
+        load_lane<s, TPI>(B, p0 + s);
+        for (int k = 1; k < C; ++k) {
+            const bool more = active && (uint32_t)k < pc.len;
+            if (!__any_sync(0xffffffffu, more)) break; // warp-uniform exit
+            // the rows are gathered at random from a gh buffer far larger
+            // than L2: fetch the next item while this one is multiplied
+            if (more && (uint32_t)k + 1 < pc.len && inst_lane<TPI>() == 0) {
+                const uint32_t *nx = item_ptr((uint32_t)k + 1);
 #pragma unroll
-                    for (int o = 0; o < 2 * s; o += 32)
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(nx + o));
-                }
-                p2_mul<s, 1>(A, B, item_ptr(k), false, st, sD, N, M.np, M.w + kOne * s, a.negR[pr]);
+                for (int o = 0; o < 2 * s; o += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(nx + o));
             }
+            p2_mul<s, TPI>(A, B, more ? item_ptr((uint32_t)k) : one, false, st, sD, N, M.np, M.w + kOne * s, negR);
+        }
+        if (active) {
             uint32_t *d = dst + (2 * (size_t)pidx + g) * 4 * s + pr * 2 * s;
-            store_lane<s, 1>(d, A);
-            store_lane<s, 1>(d + s, B);
+            store_lane<s, TPI>(d, A);
+            store_lane<s, TPI>(d + s, B);
         }
     }
 }

@@ -194,15 +194,15 @@ struct Cls;
 // mod-p² pre/post conversions (S = 2s)
 template <>
 struct Cls<4> {
-    static constexpr int T1 = 1, T2 = 1, TC = 1, TD = 1, TE = 1, TH = 1, TN = 1, TP = 1, TQ = 1, TND = 1;
+    static constexpr int T1 = 1, T2 = 1, TC = 1, TD = 1, TE = 1, TH = 1, TN = 1, TP = 1, TQ = 1, TND = 1, TK = 1;
 };
 template <>
 struct Cls<8> {
-    static constexpr int T1 = 1, T2 = 1, TC = 2, TD = 1, TE = 1, TH = 2, TN = 2, TP = 1, TQ = 2, TND = 1;
+    static constexpr int T1 = 1, T2 = 1, TC = 2, TD = 1, TE = 1, TH = 2, TN = 2, TP = 1, TQ = 2, TND = 1, TK = 1;
 };
 template <>
 struct Cls<16> {
-    static constexpr int T1 = 1, T2 = 2, TC = 4, TD = 2, TE = 2, TH = 4, TN = 4, TP = 1, TQ = 4, TND = 2;
+    static constexpr int T1 = 1, T2 = 2, TC = 4, TD = 2, TE = 2, TH = 4, TN = 4, TP = 1, TQ = 4, TND = 2, TK = 1;
 };
 #ifndef SFXB_T1_32
 #define SFXB_T1_32 1
@@ -219,17 +219,20 @@ struct Cls<16> {
 #ifndef SFXB_TP_32
 #define SFXB_TP_32 1
 #endif
+#ifndef SFXB_TK_32
+#define SFXB_TK_32 1
+#endif
 #ifndef SFXB_TND_32
 #define SFXB_TND_32 4
 #endif
 template <>
 struct Cls<32> { // 2048-bit keys (tuned on B200, profiles/)
     static constexpr int T1 = SFXB_T1_32, T2 = SFXB_T2_32, TC = 8, TD = SFXB_TD_32, TE = 4, TH = SFXB_TH_32, TN = 8,
-                         TP = SFXB_TP_32, TQ = 4, TND = SFXB_TND_32;
+                         TP = SFXB_TP_32, TQ = 4, TND = SFXB_TND_32, TK = SFXB_TK_32;
 };
 template <>
 struct Cls<48> {
-    static constexpr int T1 = 2, T2 = 4, TC = 8, TD = 4, TE = 8, TH = 8, TN = 8, TP = 4, TQ = 8, TND = 4;
+    static constexpr int T1 = 2, T2 = 4, TC = 8, TD = 4, TE = 8, TH = 8, TN = 8, TP = 4, TQ = 8, TND = 4, TK = 4;
 };
 
 // grid.x for `items` work items spread over `rows` block rows (grid.y)
@@ -555,6 +558,7 @@ dev::CrtArgs crt_args(const sfxb_ctx *c) {
         a.mod_p[i] = arg(c->mod_pq[i]);
         a.mod_p2[i] = arg(c->mod_pq2[i]);
         a.negR[i] = c->d_negR[i];
+        a.one[i] = c->d_one_p2[i];
     }
     a.mod_n2 = arg(c->mod_n2);
     a.qq_inv_m = c->d_qq_inv_m;
@@ -902,13 +906,14 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
                 // CRT on digits: 2 primes × (two-product pass + one pass) mod p per multiplication
                 const uint64_t pp = 5ull * cs * cs + 2 * cs;
                 ProfScope prof_(*c, 0, mults * 2 * pp);
+                constexpr int NIp = dev::kBlock / C::TK;
                 if (Cp == (uint32_t)kPieceLong) {
-                    auto k = dev::k_seg_prod_p2<cs, kPieceLong>;
-                    k<<<occupancy_grid(*c, k, 4 * P, dev::kBlock), dev::kBlock, 0, st>>>(
+                    auto k = dev::k_seg_prod_p2<cs, C::TK, kPieceLong>;
+                    k<<<occupancy_grid(*c, k, 4 * P, NIp), dev::kBlock, 0, st>>>(
                         crt_args(c), pieces, order, P, pass == 0 ? sorted : nullptr, src, dst, next_job);
                 } else {
-                    auto k = dev::k_seg_prod_p2<cs, kPiece>;
-                    k<<<occupancy_grid(*c, k, 4 * P, dev::kBlock), dev::kBlock, 0, st>>>(
+                    auto k = dev::k_seg_prod_p2<cs, C::TK, kPiece>;
+                    k<<<occupancy_grid(*c, k, 4 * P, NIp), dev::kBlock, 0, st>>>(
                         crt_args(c), pieces, order, P, pass == 0 ? sorted : nullptr, src, dst, next_job);
                 }
             } else if (g->digits_n) {
@@ -1626,6 +1631,12 @@ int sfxb_ctx_create(sfxb_ctx **out, int device, const uint32_t *n, uint32_t n_wo
                 c->d_hR[i] = dev_big(*c, mp.to_mont(h), s);
                 c->d_cdec[i] = dev_big(*c, mp.from_mont(h), s);
                 c->d_negR[i] = dev_big(*c, host::sub(pr, mp.r1), s); // p − (R mod p)
+                {
+                    std::vector<uint32_t> one(2 * (size_t)s);
+                    std::copy(mp.r1.begin(), mp.r1.end(), one.begin());
+                    std::copy(mp.r1.begin(), mp.r1.end(), one.begin() + s);
+                    c->d_one_p2[i] = dev_upload(*c, one.data(), one.size());
+                }
             }
             // profiling units: 32×32 products per item of the exponentiation kernels
             const uint64_t pp = 2ull * s * s + s, pp2 = 2ull * (2 * s) * (2 * s) + 2 * s;
