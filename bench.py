@@ -604,12 +604,14 @@ def run_ours(a):
             # ncu --set full capture (profiles/r01_summary.md): a depth-0 pass-1 launch at
             # 200k rows gathering 2.8M ciphertexts (1.43 GB algorithmic) read 2.07 GB + wrote 0.05 GB
             "traffic": 2.12e9, "traffic_algorithmic": 1.43e9,
-            "kernel": "k_seg_prod (K2 segmented Montgomery product mod n^2)",
+            "kernel": "K2 segmented product: k_seg_prod_nd (passive party) + k_seg_prod_p2 (key holder)",
             "work": f"K2 executed {k2_modmuls:.4g} 32x32->64 products in the timed steps: passive party "
-                    f"{PRODUCTS_PER_ADD} per multiplication mod n^2, key holder 6*(2s^2+s) = "
-                    f"{6 * (2 * (cw // 4) ** 2 + cw // 4)} per multiplication (CRT mod p^2, q^2 on base-p digits); "
-                    f"{int(adds_timed)} reference additions (+{kt_modmuls} multiplications mod n^2 in the "
-                    f"sibling-subtraction inversion, {kt_ms:.1f} ms)",
+                    f"5S^2+2S = {5 * (cw // 2) ** 2 + 2 * (cw // 2)} per ciphertext multiplication (base-n "
+                    f"digits, S = {cw // 2} limbs of n), key holder 2*(5s^2+2s) = "
+                    f"{2 * (5 * (cw // 4) ** 2 + 2 * (cw // 4))} (CRT mod p^2, q^2 on base-p digits), vs "
+                    f"{PRODUCTS_PER_ADD} for the reference's multiplication mod n^2; {int(adds_timed)} reference "
+                    f"additions (+{kt_modmuls} multiplications mod n^2 in the sibling-subtraction inversion, "
+                    f"{kt_ms:.1f} ms)",
             "kernel_launches": k2_launches, "kernel_ms": k2_ms, "kernel_share_of_step": k2_ms / ms,
             "peak_source": "sfxb_imad_peak: IMAD.WIDE.U32(.X) carry chains on all SMs, measured in this process "
                            "before the timed region (SM clock: see clocks)",
