@@ -187,12 +187,27 @@ __global__ void k_piece_keys(const Piece *pieces, size_t n, uint32_t *len, uint3
     }
 }
 
-// Output slot (key, gh): count == 0 -> literal 1 (or Montgomery one for
-// partials); else from_mont of the key's single final partial.
+// Finalize outputs shared by the K2 variants: the Montgomery form (tree cache
+// / partials) and/or the plain residue of every slot.  Slots of nodes flagged
+// in `skip_node` (derived later by sibling subtraction) are not computed when
+// the whole warp's instances belong to such nodes (their values are rewritten
+// by k_derive, so computing them anyway is harmless).
+struct FinOut {
+    uint32_t *mont;          // may be null
+    uint32_t *plain;         // may be null
+    const uint8_t *skip_node; // may be null
+    uint32_t slots_per_node; // 2·J·K
+};
+__device__ __forceinline__ bool fin_skip(const FinOut &o, size_t slot) {
+    const bool sk = o.skip_node != nullptr && o.skip_node[slot / o.slots_per_node];
+    return __all_sync(0xffffffffu, sk);
+}
+
+// Output slot (key, gh): count == 0 -> literal 1 (Montgomery one for the
+// Montgomery output); else the key's single final partial.
 template <int S, int TPI>
 __global__ void __launch_bounds__(kBlock) k_hist_finalize(ModArg M, const uint32_t *count, const uint32_t *final_idx,
-                                                          size_t nkeys, const uint32_t *partial, uint32_t *out,
-                                                          int mont_out) {
+                                                          size_t nkeys, const uint32_t *partial, FinOut o) {
     constexpr int L = S / TPI, NI = kBlock / TPI;
     __shared__ uint2 sB[S / 2 * NI];
     const Stage st = make_stage<TPI>(sB);
@@ -201,6 +216,7 @@ __global__ void __launch_bounds__(kBlock) k_hist_finalize(ModArg M, const uint32
     load_const<S, TPI>(N, mr, kMod);
     load_const<S, TPI>(one_m, mr, kOne);
     SFXB_UNIFORM_LOOP(slot, active, 2 * nkeys) {
+        if (fin_skip(o, slot)) continue;
         const size_t key = slot >> 1;
         const uint32_t g = (uint32_t)(slot & 1);
         const bool empty = count[key] == 0;
@@ -209,8 +225,11 @@ __global__ void __launch_bounds__(kBlock) k_hist_finalize(ModArg M, const uint32
         else
 #pragma unroll
             for (int w = 0; w < L; ++w) v[w] = one_m[w];
-        if (!mont_out) from_mont<S, TPI>(v, v, st, N, M.np); // Montgomery one -> 1
-        if (active) store_lane<S, TPI>(out + slot * S, v);
+        if (o.mont && active) store_lane<S, TPI>(o.mont + slot * S, v);
+        if (o.plain) {
+            from_mont<S, TPI>(v, v, st, N, M.np); // Montgomery one -> 1
+            if (active) store_lane<S, TPI>(o.plain + slot * S, v);
+        }
     }
 }
 
@@ -302,6 +321,25 @@ __global__ void __launch_bounds__(kBlock) k_derive(ModArg M, const uint32_t *par
         load_lane<S, TPI>(b, inv_small + j * S);
         mmul<S, TPI>(a, a, b, st, N, M.np);
         if (active) store_lane<S, TPI>(hist + ((size_t)d.derived * spn + k) * S, a);
+    }
+}
+
+// out[d·spn + k] = from_mont(hist[d·spn + k]) for the derived nodes d
+template <int S, int TPI>
+__global__ void __launch_bounds__(kBlock) k_from_mont_nodes(ModArg M, const uint32_t *hist, const Derived *dv,
+                                                            size_t n_derived, size_t spn, uint32_t *out) {
+    constexpr int L = S / TPI, NI = kBlock / TPI;
+    __shared__ uint2 sB[S / 2 * NI];
+    const Stage st = make_stage<TPI>(sB);
+    const ModRef mr = M.ref();
+    uint32_t N[L];
+    load_const<S, TPI>(N, mr, kMod);
+    SFXB_UNIFORM_LOOP(j, active, n_derived * spn) {
+        const size_t e = (size_t)dv[j / spn].derived * spn + j % spn;
+        uint32_t v[L];
+        load_lane<S, TPI>(v, hist + e * S);
+        from_mont<S, TPI>(v, v, st, N, M.np);
+        if (active) store_lane<S, TPI>(out + e * S, v);
     }
 }
 

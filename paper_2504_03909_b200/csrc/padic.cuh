@@ -455,8 +455,14 @@ __global__ void __launch_bounds__(kBlock) k_gh_digits(CrtArgs a, uint32_t *gh, s
 // prime may differ between the instances of a warp: each loads its own
 // modulus).  An instance past the end of its piece multiplies by the digits
 // of 1̃, so every instance of a warp runs the same passes.
+#ifndef SFXB_ND_MINB
+#define SFXB_ND_MINB 1
+#endif
+#ifndef SFXB_K_MINB
+#define SFXB_K_MINB 1
+#endif
 template <int s, int TPI, int C>
-__global__ void __launch_bounds__(kBlock) k_seg_prod_p2(CrtArgs a, const Piece *pieces, const uint32_t *order,
+__global__ void __launch_bounds__(kBlock, (TPI > 1 ? SFXB_K_MINB : 1)) k_seg_prod_p2(CrtArgs a, const Piece *pieces, const uint32_t *order,
                                                         size_t n_pieces, const uint32_t *sorted, const uint32_t *src,
                                                         uint32_t *dst, unsigned long long *next_job) {
     constexpr int L = s / TPI, NI = kBlock / TPI, NIW = 32 / TPI;
@@ -536,7 +542,7 @@ __device__ __forceinline__ void p2_digits_plain(uint32_t (&u)[2 * s / TPI], cons
 template <int s, int TPI>
 __global__ void __launch_bounds__(kBlock) k_hist_finalize_p2(CrtArgs a, const uint32_t *count,
                                                              const uint32_t *final_idx, size_t nkeys,
-                                                             const uint32_t *partial, uint32_t *out, int mont_out) {
+                                                             const uint32_t *partial, FinOut o) {
     constexpr int S2 = 2 * s, S4 = 4 * s, L2 = S2 / TPI, L4 = S4 / TPI, NI = kBlock / TPI;
     __shared__ uint2 sB[S4 / 2 * NI];
     const Stage st = make_stage<TPI>(sB);
@@ -544,14 +550,17 @@ __global__ void __launch_bounds__(kBlock) k_hist_finalize_p2(CrtArgs a, const ui
     uint32_t N4[L4];
     load_const<S4, TPI>(N4, M4, kMod);
     SFXB_UNIFORM_LOOP(slot, active, 2 * nkeys) {
+        if (fin_skip(o, slot)) continue;
         const size_t key = slot >> 1;
         const uint32_t g = (uint32_t)(slot & 1);
         uint32_t c4[L4];
-        // warp-uniform: every instance runs the CRT (empty keys on a dummy
-        // but valid operand, their own output slot) and selects afterwards
+        // warp-uniform: every instance runs the CRT (empty keys on a dummy but
+        // valid operand) and selects afterwards
         const bool empty = count[key] == 0;
         {
-            const uint32_t *pp = empty ? out + slot * S4 : partial + (2 * (size_t)final_idx[key] + g) * S4;
+            // (an empty key reads its own output slot: valid memory, result discarded)
+            const uint32_t *pp = empty ? (o.mont ? o.mont : o.plain) + slot * S4
+                                       : partial + (2 * (size_t)final_idx[key] + g) * S4;
             const ModRef M2 = a.mod_p2[0].ref(), Q2 = a.mod_p2[1].ref();
             uint32_t N2[L2], yp[L2], yq[L2], d[L2], C2[L2], h[L2];
             load_const<S2, TPI>(N2, Q2, kMod);
@@ -568,17 +577,15 @@ __global__ void __launch_bounds__(kBlock) k_hist_finalize_p2(CrtArgs a, const ui
             load_lane<S4, TPI>(C4, a.q2R_n2);
             mmul<S4, TPI>(c4, C4, h4, st, N4, M4.np); // q²·h (< n², exact)
             mod_add<S4, TPI>(c4, c4, yq4, N4);
-            if (mont_out) {
-                load_const<S4, TPI>(C4, M4, kR2);
-                mmul<S4, TPI>(c4, C4, c4, st, N4, M4.np);
-            }
         }
-        if (empty) {
-            if (mont_out) load_const<S4, TPI>(c4, M4, kOne);
-            else set_small<L4, TPI>(c4, 1u);
+        if (empty) set_small<L4, TPI>(c4, 1u);
+        if (o.plain && active) store_lane<S4, TPI>(o.plain + slot * S4, c4);
+        if (o.mont) {
+            uint32_t C4[L4];
+            load_const<S4, TPI>(C4, M4, kR2);
+            mmul<S4, TPI>(c4, C4, c4, st, N4, M4.np); // 1 -> Montgomery one
+            if (active) store_lane<S4, TPI>(o.mont + slot * S4, c4);
         }
-        __syncwarp();
-        if (active) store_lane<S4, TPI>(out + slot * S4, c4);
     }
 }
 
@@ -626,7 +633,7 @@ __global__ void __launch_bounds__(kBlock) k_gh_split_n(NdArgs a, uint32_t *gh, s
 // instance past the end of its piece multiplies by the digits of 1̃, which
 // leaves (A, B) unchanged, so every instance runs the same passes).
 template <int S, int TPI, int C>
-__global__ void __launch_bounds__(kBlock) k_seg_prod_nd(NdArgs a, const Piece *pieces, const uint32_t *order,
+__global__ void __launch_bounds__(kBlock, SFXB_ND_MINB) k_seg_prod_nd(NdArgs a, const Piece *pieces, const uint32_t *order,
                                                         size_t n_pieces, const uint32_t *sorted, const uint32_t *src,
                                                         uint32_t *dst, unsigned long long *next_job) {
     constexpr int L = S / TPI, NI = kBlock / TPI, NIW = 32 / TPI;
@@ -675,7 +682,7 @@ __global__ void __launch_bounds__(kBlock) k_seg_prod_nd(NdArgs a, const Piece *p
 template <int s, int TPI>
 __global__ void __launch_bounds__(kBlock) k_hist_finalize_nd(NdArgs a, const uint32_t *count,
                                                              const uint32_t *final_idx, size_t nkeys,
-                                                             const uint32_t *partial, uint32_t *out, int mont_out) {
+                                                             const uint32_t *partial, FinOut o) {
     constexpr int S2 = 2 * s, S4 = 4 * s, L4 = S4 / TPI, NI = kBlock / TPI;
     __shared__ uint2 sB[S4 / 2 * NI];
     const Stage st = make_stage<TPI>(sB);
@@ -685,10 +692,12 @@ __global__ void __launch_bounds__(kBlock) k_hist_finalize_nd(NdArgs a, const uin
     const int tl = inst_lane<TPI>();
     const bool low = tl * L4 < S2;
     SFXB_UNIFORM_LOOP(slot, active, 2 * nkeys) {
+        if (fin_skip(o, slot)) continue;
         const size_t key = slot >> 1;
         const uint32_t g = (uint32_t)(slot & 1);
         const bool empty = count[key] == 0;
-        const uint32_t *pp = empty ? out + slot * S4 : partial + (2 * (size_t)final_idx[key] + g) * S4;
+        const uint32_t *pp = empty ? (o.mont ? o.mont : o.plain) + slot * S4
+                                   : partial + (2 * (size_t)final_idx[key] + g) * S4;
         uint32_t av[L4], bv[L4], Rc[L4], nc[L4], u[L4], v[L4];
         load_lane<S4, TPI>(av, pp);
         relayout<S4, S4, TPI>(bv, av, st);
@@ -704,16 +713,13 @@ __global__ void __launch_bounds__(kBlock) k_hist_finalize_nd(NdArgs a, const uin
         mmul<S4, TPI>(u, av, Rc, st, N4, M4.np);
         mmul<S4, TPI>(v, bv, nc, st, N4, M4.np);
         mod_add<S4, TPI>(u, u, v, N4);
-        if (mont_out) {
+        if (empty) set_small<L4, TPI>(u, 1u);
+        if (o.plain && active) store_lane<S4, TPI>(o.plain + slot * S4, u);
+        if (o.mont) {
             load_const<S4, TPI>(v, M4, kR2);
-            mmul<S4, TPI>(u, v, u, st, N4, M4.np);
+            mmul<S4, TPI>(u, v, u, st, N4, M4.np); // 1 -> Montgomery one
+            if (active) store_lane<S4, TPI>(o.mont + slot * S4, u);
         }
-        if (empty) {
-            if (mont_out) load_const<S4, TPI>(u, M4, kOne);
-            else set_small<L4, TPI>(u, 1u);
-        }
-        __syncwarp();
-        if (active) store_lane<S4, TPI>(out + slot * S4, u);
     }
 }
 

@@ -957,27 +957,30 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
         constexpr int NI = dev::kBlock / C::TH;
         auto kfd = dev::k_hist_finalize_p2<cs, C::TC>;
         auto kfn = dev::k_hist_finalize_nd<cs, C::TC>;
-        auto finalize = [&](uint32_t *dst, int mont) {
+        auto finalize = [&](dev::FinOut o) {
+            o.slots_per_node = (uint32_t)spn;
             if (g->digits_n) {
                 kfn<<<occupancy_grid(*c, kfn, 2 * nkeys, dev::kBlock / C::TC), dev::kBlock, 0, st>>>(
-                    nd_args(c), count, final_idx, nkeys, final_part, dst, mont);
+                    nd_args(c), count, final_idx, nkeys, final_part, o);
             } else if (g->digits) {
                 // digits -> CRT residue mod n² (a key without rows keeps the literal 1)
                 kfd<<<occupancy_grid(*c, kfd, 2 * nkeys, dev::kBlock / C::TC), dev::kBlock, 0, st>>>(
-                    crt_args(c), count, final_idx, nkeys, final_part, dst, mont);
+                    crt_args(c), count, final_idx, nkeys, final_part, o);
             } else {
                 kf<<<occupancy_grid(*c, kf, 2 * nkeys, NI), dev::kBlock, 0, st>>>(arg(c->mod_n2), count, final_idx,
-                                                                                 nkeys, final_part, dst, mont);
+                                                                                 nkeys, final_part, o);
             }
             check_launch(*c);
         };
         if (!tree) {
-            finalize(d_out, mont_out);
+            finalize(mont_out ? dev::FinOut{d_out, nullptr, nullptr, 0} : dev::FinOut{nullptr, d_out, nullptr, 0});
             return;
         }
-        // tree mode: all nodes in Montgomery form in the context's current buffer
+        // tree mode: all nodes in Montgomery form in the context's current
+        // buffer (the parents of the next level); directly built nodes also
+        // go to the plain output now, derived nodes after k_derive
         uint32_t *hist = (uint32_t *)grow(c->tree_buf[c->tree_cur ^ 1], (size_t)N * spn * S4 * 4 + 64);
-        finalize(hist, 1);
+        finalize(dev::FinOut{hist, mont_out ? nullptr : d_out, pairs.empty() ? nullptr : d_derived, 0});
         const bool derived_ok = pairs.empty() ||
             derive_siblings<cs>(c, B, hist, (const uint32_t *)c->tree_buf[c->tree_cur].p, d_pairs, pairs.size(), spn);
         if (!derived_ok) {
@@ -990,10 +993,10 @@ void accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint3
         }
         if (mont_out) {
             CK(cudaMemcpyAsync(d_out, hist, (size_t)N * spn * S4 * 4, cudaMemcpyDeviceToDevice, st));
-        } else {
-            auto kc = dev::k_from_mont_copy<S4, C::TH>;
-            const int gc = occupancy_grid(*c, kc, (size_t)N * spn, NI);
-            kc<<<gc, dev::kBlock, 0, st>>>(arg(c->mod_n2), hist, (size_t)N * spn, d_out);
+        } else if (!pairs.empty()) {
+            auto kc = dev::k_from_mont_nodes<S4, C::TH>;
+            const int gc = occupancy_grid(*c, kc, pairs.size() * spn, NI);
+            kc<<<gc, dev::kBlock, 0, st>>>(arg(c->mod_n2), hist, d_pairs, pairs.size(), spn, d_out);
             check_launch(*c);
         }
         c->tree_derived_nodes += pairs.size();
