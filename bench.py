@@ -368,6 +368,32 @@ def run_ours(a):
     pad = [pdist.padded_slots(s, world) for s in n_slots]
     outs = [[torch.empty((pad[d], cw), dtype=torch.int32, device=dev) for _ in range(a.parties)] for d in range(D)]
     finals = [[None] * a.parties for _ in range(D)]
+    # tree mode on N>1 ranks: column slices (sfxb_accumulate_part_dev / all_to_all /
+    # sfxb_combine_slices_dev); global node sizes pick the same smaller sibling everywhere
+    sliced = world > 1 and not a.no_tree
+    sizes = [np.diff(o).astype(np.uint32) for o, _ in fronts_full]
+    jl = ops[0].slice_width(J, K, world)
+    if sliced:
+        sends = [[torch.empty((world * (1 << d) * jl, cw), dtype=torch.int32, device=dev) for _ in range(a.parties)]
+                 for d in range(D)]
+        reals = [[torch.zeros(2 * (1 << d) * J * K, dtype=torch.int32, device=dev) for _ in range(a.parties)]
+                 for d in range(D)]
+        slices = [[torch.empty(((1 << d) * jl, cw), dtype=torch.int32, device=dev) for _ in range(a.parties)]
+                  for d in range(D)]
+
+    def sliced_level(pi, g, d, N):
+        """One level of one party on N>1 ranks (tree mode): partial slices,
+        all_to_all, count all_reduce, product + sibling subtraction per slice.
+        Returns the reference addition count (on rank 0; 0 elsewhere)."""
+        offs, rows = d_front[d]
+        ops[pi].accumulate_part(g, d_bins[pi], J, offs, fronts[d][0], N, rows, rows.shape[0], K, parents[d],
+                                sizes[d], world, sends[d][pi], reals[d][pi], sync=False)
+        ctxs[pi].lib.sfxb_ctx_sync(ctxs[pi].h)
+        recv = pdist.exchange(sends[d][pi], world)
+        pdist.all_reduce_counts(reals[d][pi])
+        adds = ops[pi].count_additions(reals[d][pi], 2 * N * J * K) if rank == 0 else 0
+        ops[pi].combine_slices(g, recv, world, rank, N, J, K, parents[d], sizes[d], slices[d][pi], sync=False)
+        return adds
     stream = torch.cuda.ExternalStream(ctxs[0].lib.sfxb_ctx_stream(ctxs[0].h), device=dev)
 
     # parent of node i at depth d is node i // 2 of depth d−1 (frontiers() builds
@@ -380,6 +406,9 @@ def run_ours(a):
             offs, rows = d_front[d]
             N = offs.shape[0] - 1
             for pi in range(a.parties):
+                if sliced:
+                    adds += sliced_level(pi, gh[pi], d, N)
+                    continue
                 if a.no_tree:
                     adds += ops[pi].accumulate(gh[pi], d_bins[pi], J, offs, N, rows, rows.shape[0], K, outs[d][pi],
                                                mont_out=world > 1, sync=False)
@@ -452,10 +481,18 @@ def run_ours(a):
         h2d_p, d2h_p = gh_np.nbytes, 0
         for d in range(D):
             offs, rows = h_front[d]
-            if world > 1:
+            if sliced:
+                N = len(offs) - 1
+                sliced_level(pi, g, d, N)
+                ctxs[pi].lib.sfxb_ctx_sync(ctxs[pi].h)
+                full = pdist.gather_columns(slices[d][pi], N, 2 * J * K, world)
+                if rank == 0:
+                    h_out[pi][d][:] = full.cpu().numpy().view(np.uint32)
+                    d2h_p += h_out[pi][d].nbytes
+            elif world > 1:
                 outp = outs[d][pi]
-                ops[pi].accumulate_tree(g, d_bins[pi], J, d_front[d][0], offs, len(offs) - 1, d_front[d][1],
-                                        len(rows), K, parents[d], outp, mont_out=True)
+                ops[pi].accumulate(g, d_bins[pi], J, d_front[d][0], len(offs) - 1, d_front[d][1], len(rows), K,
+                                   outp, mont_out=True)
                 recv = pdist.exchange(outp, world)
                 fin = pdist.reduce_slice(recv, lambda parts, k, sl, out: ops[pi].reduce_partials(parts, k, sl, out))
                 full = pdist.gather_slices(fin, n_slots[d], world)

@@ -194,6 +194,37 @@ uint64_t sfxb_ctx_tree_derived(const sfxb_ctx *ctx);
 int sfxb_reduce_partials_dev(sfxb_ctx *ctx, const uint32_t *d_parts, uint32_t parts,
                              size_t n_slots, uint32_t *d_out);
 
+/* ---- rank-sliced histograms (one process per GPU; SURVEY §8e under torchrun) ----
+ * The device group's algorithm with the exchange left to the caller's
+ * collective (NCCL all_to_all).  Per level and party, on every rank:
+ *   1. sfxb_accumulate_part_dev: Montgomery-form partial histograms of this
+ *      rank's rows (frontier renumbered to the rank's gh rows; host offsets
+ *      h_node_offsets), nodes that sibling subtraction will derive skipped,
+ *      written as `world` slot slices, rank-major:
+ *      d_send[k][node][j] = partial slot k·jl + j of node, jl =
+ *      sfxb_slice_width(J, K, world), world × n_nodes × jl ciphertexts;
+ *      d_real: 2·n_nodes·J·K per-slot counts of non-trivial ciphertexts.
+ *   2. the caller: all_to_all of d_send (slice k to rank k) and a SUM
+ *      all_reduce of d_real; sfxb_count_additions_dev on the summed counts
+ *      gives the reference's ciphertext_additions.
+ *   3. sfxb_combine_slices_dev: product of the world received slices
+ *      (d_recv, rank-major), sibling subtraction on this rank's slice against
+ *      the slice it cached at the previous level, plain slice n_nodes × jl to
+ *      d_out.
+ * h_parent (tree mode, NULL = direct) indexes the previous level's nodes;
+ * h_node_sizes are the GLOBAL row counts of this level's nodes (every rank
+ * must choose the same smaller sibling).  All device pointers on the
+ * context's device; synchronous. */
+uint32_t sfxb_slice_width(uint32_t n_features, uint32_t n_bins, uint32_t world);
+int sfxb_accumulate_part_dev(sfxb_ctx *ctx, const sfxb_gh *gh, const uint16_t *d_bins, uint32_t n_features,
+                             const uint32_t *d_node_offsets, const uint32_t *h_node_offsets, uint32_t n_nodes,
+                             const uint32_t *d_rows, uint32_t n_rows, uint32_t n_bins, const int32_t *h_parent,
+                             const uint32_t *h_node_sizes, uint32_t world, uint32_t *d_send, uint32_t *d_real);
+int sfxb_combine_slices_dev(sfxb_ctx *ctx, const sfxb_gh *gh, const uint32_t *d_recv, uint32_t world, uint32_t rank,
+                            uint32_t n_nodes, uint32_t n_features, uint32_t n_bins, const int32_t *h_parent,
+                            const uint32_t *h_node_sizes, uint32_t *d_out);
+int sfxb_count_additions_dev(sfxb_ctx *ctx, const uint32_t *d_real, size_t n, uint64_t *additions);
+
 /* ---- decrypt -----------------------------------------------------------------
  * PaillierPlugin::decrypt_histogram / decrypt_slot (secure_processor.cpp:
  * 679-719, :734-738) + decrypt (he.cpp:105-115) + decode_fixed (:138-143):

@@ -92,6 +92,12 @@ def load() -> C.CDLL:
         "sfxb_tree_reset": (C.c_int, [vp]),
         "sfxb_ctx_tree_derived": (C.c_uint64, [vp]),
         "sfxb_reduce_partials_dev": (C.c_int, [vp, vp, C.c_uint32, sz, vp]),
+        "sfxb_slice_width": (C.c_uint32, [C.c_uint32, C.c_uint32, C.c_uint32]),
+        "sfxb_accumulate_part_dev": (C.c_int, [vp, vp, vp, C.c_uint32, vp, _u32p, C.c_uint32, vp, C.c_uint32,
+                                               C.c_uint32, vp, vp, C.c_uint32, vp, vp]),
+        "sfxb_combine_slices_dev": (C.c_int, [vp, vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                              C.c_uint32, vp, vp, vp]),
+        "sfxb_count_additions_dev": (C.c_int, [vp, vp, sz, C.POINTER(C.c_uint64)]),
         "sfxb_decrypt": (C.c_int, [vp, _u32p, sz, C.c_uint32, _f64p, vp, C.POINTER(C.c_uint64)]),
         "sfxb_decrypt_dev": (C.c_int, [vp, vp, sz, C.c_uint32, vp, vp, C.POINTER(C.c_uint64)]),
         "sfxb_decrypt_tree": (C.c_int, [vp, C.c_uint64, _u32p, C.c_uint32, C.c_uint32, vp, C.c_uint32, _f64p,
@@ -384,6 +390,45 @@ class DeviceOps:
             np.ascontiguousarray(rows, dtype=np.uint32), n_bins, np.ascontiguousarray(parent, dtype=np.int32),
             out.reshape(-1), C.byref(adds)))
         return out, adds.value
+
+    def slice_width(self, n_features: int, n_bins: int, world: int) -> int:
+        return self.ctx.lib.sfxb_slice_width(n_features, n_bins, world)
+
+    def accumulate_part(self, gh: GhHandle, d_bins, n_features: int, d_offsets, h_offsets, n_nodes: int, d_rows,
+                        n_rows: int, n_bins: int, parent, sizes, world: int, d_send, d_real, sync: bool = True):
+        """Rank-sliced partials (sfxb_accumulate_part_dev): d_send = world x n_nodes x jl
+        Montgomery-form slices, d_real = 2*n_nodes*J*K real-ciphertext counts."""
+        if sync:
+            self._pre()
+        par = None if parent is None else np.ascontiguousarray(parent, dtype=np.int32)
+        siz = None if sizes is None else np.ascontiguousarray(sizes, dtype=np.uint32)
+        self.ctx._check(self.ctx.lib.sfxb_accumulate_part_dev(
+            self.ctx.h, gh.h, _ptr(d_bins), n_features, _ptr(d_offsets),
+            np.ascontiguousarray(h_offsets, dtype=np.uint32), n_nodes, _ptr(d_rows), n_rows, n_bins,
+            None if par is None else par.ctypes.data, None if siz is None else siz.ctypes.data, world,
+            _ptr(d_send), _ptr(d_real)))
+        if sync:
+            self._post()
+
+    def combine_slices(self, gh: GhHandle, d_recv, world: int, rank: int, n_nodes: int, n_features: int,
+                       n_bins: int, parent, sizes, d_out, sync: bool = True):
+        """Product of the received slices + sibling subtraction on this rank's
+        slice (sfxb_combine_slices_dev) -> plain n_nodes x jl slice in d_out."""
+        if sync:
+            self._pre()
+        par = None if parent is None else np.ascontiguousarray(parent, dtype=np.int32)
+        siz = None if sizes is None else np.ascontiguousarray(sizes, dtype=np.uint32)
+        self.ctx._check(self.ctx.lib.sfxb_combine_slices_dev(
+            self.ctx.h, gh.h, _ptr(d_recv), world, rank, n_nodes, n_features, n_bins,
+            None if par is None else par.ctypes.data, None if siz is None else siz.ctypes.data, _ptr(d_out)))
+        if sync:
+            self._post()
+
+    def count_additions(self, d_real, n: int) -> int:
+        self._pre()
+        adds = C.c_uint64(0)
+        self.ctx._check(self.ctx.lib.sfxb_count_additions_dev(self.ctx.h, _ptr(d_real), n, C.byref(adds)))
+        return adds.value
 
     def tree_reset(self):
         self.ctx._check(self.ctx.lib.sfxb_tree_reset(self.ctx.h))

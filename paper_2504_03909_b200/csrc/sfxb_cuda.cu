@@ -1367,6 +1367,120 @@ sfxb_gh *gh_upload_group(sfxb_ctx *c, const uint32_t *gh_cts, uint32_t n_samples
     return g.release();
 }
 
+// Sibling pairs of a level against the context's cached parent level (valid
+// for gradient handle g, J, K and slice geometry G), the smaller child (by
+// the callers' GLOBAL row counts `sizes`) built directly, the larger derived.
+// Every shard / rank computes the same plan from the same inputs.
+void plan_pairs(const sfxb_ctx *c, const sfxb_gh *g, uint32_t J, uint32_t K, uint32_t G, const int32_t *parent,
+                const uint32_t *sizes, uint32_t N, std::vector<dev::Derived> &pairs, std::vector<uint8_t> &skip) {
+    pairs.clear();
+    skip.assign(N, 0);
+    if (!parent || !(c->tree_valid && c->tree_gh == g && c->tree_J == J && c->tree_K == K && c->tree_G == G)) return;
+    std::vector<std::vector<uint32_t>> kids(c->tree_N);
+    for (uint32_t i = 0; i < N; ++i)
+        if (parent[i] >= 0 && (uint32_t)parent[i] < c->tree_N) kids[parent[i]].push_back(i);
+    for (uint32_t pnode = 0; pnode < c->tree_N; ++pnode) {
+        if (kids[pnode].size() != 2) continue;
+        const uint32_t a = kids[pnode][0], b = kids[pnode][1];
+        const uint32_t small = sizes[a] <= sizes[b] ? a : b, large = sizes[a] <= sizes[b] ? b : a;
+        pairs.push_back(dev::Derived{large, small, pnode});
+        skip[large] = 1;
+    }
+}
+
+// ---- rank-sliced histograms (one process per GPU, bench.py under torchrun)
+//
+// The device group's algorithm with the peer reads replaced by a collective
+// the caller runs (NCCL all_to_all): sfxb_accumulate_part_dev builds this
+// rank's Montgomery partials (nodes to be derived skipped) already cut into
+// `world` slot slices, rank-major; after the exchange sfxb_combine_slices_dev
+// multiplies the received slices, derives the larger siblings on the slice
+// against the slice cached at the previous level and writes the plain slice.
+
+// slice width: every node's 2·J·K slots in `world` column blocks of jl
+uint32_t slice_width(uint32_t J, uint32_t K, uint32_t world) {
+    const uint32_t spn = 2 * J * K;
+    return (spn + world - 1) / world;
+}
+
+void accumulate_part(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint32_t J, const uint32_t *d_offs,
+                     const uint32_t *h_offs, uint32_t N, const uint32_t *d_rows, uint32_t R, uint32_t K,
+                     const int32_t *h_parent, const uint32_t *h_sizes, uint32_t world, uint32_t *d_send,
+                     uint32_t *d_real) {
+    if (!g || g->ctx != c || !g->parts.empty())
+        throw ApiError(SFXB_ERR_ARG, "accumulate: gradient handle belongs to another context");
+    if (world == 0 || world > (uint32_t)dev::kMaxShards) throw ApiError(SFXB_ERR_ARG, "accumulate: bad world size");
+    const size_t S4 = 4 * (size_t)c->s, spn = 2 * (size_t)J * K, jl = slice_width(J, K, world);
+    std::vector<dev::Derived> pairs;
+    std::vector<uint8_t> skip;
+    plan_pairs(c, g, J, K, world, h_parent, h_sizes, N, pairs, skip);
+    HistBufs &B = hist_bufs(c);
+    uint32_t *part = bget<uint32_t>(B.g_part, (size_t)N * spn * S4);
+    accumulate_dev(c, g, d_bins, J, d_offs, N, d_rows, R, K, part, 1, nullptr, nullptr, h_offs, skip.data(), d_real);
+    cudaStream_t st = c->stream;
+    if (jl * world != spn) CK(cudaMemsetAsync(d_send, 0, (size_t)world * N * jl * S4 * 4, st));
+    for (uint32_t k = 0; k < world && N; ++k) {
+        const size_t lo = (size_t)k * jl, w = lo < spn ? std::min<size_t>(jl, spn - lo) : 0;
+        if (w)
+            CK(cudaMemcpy2DAsync(d_send + (size_t)k * N * jl * S4, jl * S4 * 4, part + lo * S4, spn * S4 * 4,
+                                 w * S4 * 4, N, cudaMemcpyDeviceToDevice, st));
+    }
+}
+
+void combine_slices(sfxb_ctx *c, const sfxb_gh *g, const uint32_t *d_recv, uint32_t world, uint32_t rank, uint32_t N,
+                    uint32_t J, uint32_t K, const int32_t *h_parent, const uint32_t *h_sizes, uint32_t *d_out) {
+    if (world == 0 || world > (uint32_t)dev::kMaxShards || rank >= world)
+        throw ApiError(SFXB_ERR_ARG, "combine: bad world size or rank");
+    const size_t S4 = 4 * (size_t)c->s, jl = slice_width(J, K, world), cnt = (size_t)N * jl;
+    const bool tree = h_parent != nullptr;
+    std::vector<dev::Derived> pairs;
+    std::vector<uint8_t> skip;
+    plan_pairs(c, g, J, K, world, h_parent, h_sizes, N, pairs, skip);
+    HistBufs &B = hist_bufs(c);
+    cudaStream_t st = c->stream;
+    uint32_t *hist = tree ? (uint32_t *)grow(c->tree_buf[c->tree_cur ^ 1], cnt * S4 * 4 + 64)
+                          : bget<uint32_t>(B.g_hist, cnt * S4);
+    dev::PeerSet parts{};
+    parts.n = world;
+    for (uint32_t k = 0; k < world; ++k) parts.p[k] = d_recv + (size_t)k * cnt * S4;
+    if (cnt) {
+        dispatch_class(c->s, [&](auto sc) {
+            constexpr int cs = decltype(sc)::value;
+            using C = Cls<cs>;
+            constexpr int NI = dev::kBlock / C::TH;
+            auto kr = dev::k_reduce_peer<4 * cs, C::TH>;
+            kr<<<occupancy_grid(*c, kr, cnt, NI), dev::kBlock, 0, st>>>(arg(c->mod_n2), parts, N, jl, 0, jl, hist);
+            check_launch(*c);
+            if (!pairs.empty()) {
+                dev::Derived *d_pairs = bget<dev::Derived>(B.pairs, pairs.size());
+                CK(cudaMemcpyAsync(d_pairs, pairs.data(), pairs.size() * sizeof(dev::Derived), cudaMemcpyHostToDevice,
+                                   st));
+                if (!derive_siblings<cs>(c, B, hist, (const uint32_t *)c->tree_buf[c->tree_cur].p, d_pairs,
+                                         pairs.size(), jl)) {
+                    c->tree_valid = false;
+                    throw ApiError(SFXB_ERR_COPRIME, "accumulate: a histogram slot shares a factor with n; "
+                                                     "rerun the level without sibling subtraction");
+                }
+            }
+            auto kc = dev::k_from_mont_copy<4 * cs, C::TH>;
+            kc<<<occupancy_grid(*c, kc, cnt, NI), dev::kBlock, 0, st>>>(arg(c->mod_n2), hist, cnt, d_out);
+            check_launch(*c);
+        });
+    }
+    if (tree) {
+        c->tree_cur ^= 1;
+        c->tree_valid = true;
+        c->tree_gh = g;
+        c->tree_J = J;
+        c->tree_K = K;
+        c->tree_N = N;
+        c->tree_G = world;
+        c->tree_j0 = rank * (uint32_t)jl;
+        c->tree_jl = (uint32_t)jl;
+        c->tree_derived_nodes += pairs.size();
+    }
+}
+
 // Row-sharded histogram over the group (sfxb_accumulate_gh /
 // sfxb_accumulate_tree_gh on a multi-device context).
 //   phase 1, every shard: its rows of the frontier, its bin columns, partial
@@ -1395,19 +1509,11 @@ void accumulate_group(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *bins, uint3
         throw ApiError(SFXB_ERR_ARG, "accumulate: frontier too large for one call");
     // sibling pairs, chosen on global row counts (identical on every shard)
     std::vector<dev::Derived> pairs;
-    std::vector<uint8_t> skip(N, 0);
-    if (tree && c->tree_valid && c->tree_gh == g && c->tree_J == J && c->tree_K == K && c->tree_G == G) {
-        std::vector<std::vector<uint32_t>> kids(c->tree_N);
-        for (uint32_t i = 0; i < N; ++i)
-            if (parent[i] >= 0 && (uint32_t)parent[i] < c->tree_N) kids[parent[i]].push_back(i);
-        for (uint32_t pnode = 0; pnode < c->tree_N; ++pnode) {
-            if (kids[pnode].size() != 2) continue;
-            const uint32_t a = kids[pnode][0], b = kids[pnode][1];
-            const uint32_t na = offs[a + 1] - offs[a], nb = offs[b + 1] - offs[b];
-            const uint32_t small = na <= nb ? a : b, large = na <= nb ? b : a;
-            pairs.push_back(dev::Derived{large, small, pnode});
-            skip[large] = 1;
-        }
+    std::vector<uint8_t> skip;
+    {
+        std::vector<uint32_t> sizes(N);
+        for (uint32_t i = 0; i < N; ++i) sizes[i] = offs[i + 1] - offs[i];
+        plan_pairs(c, g, J, K, (uint32_t)G, parent, sizes.data(), N, pairs, skip);
     }
     const std::vector<size_t> jlo = split_even(spn, G);
     const uint32_t n_samples = g->n_samples;
@@ -2104,6 +2210,53 @@ int sfxb_tree_reset(sfxb_ctx *c) {
     return guard(c, [&] {
         c->tree_valid = false;
         for (sfxb_ctx *x : c->shards) x->tree_valid = false;
+    });
+}
+
+int sfxb_accumulate_part_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint32_t n_features,
+                             const uint32_t *d_node_offsets, const uint32_t *h_node_offsets, uint32_t n_nodes,
+                             const uint32_t *d_rows, uint32_t n_rows, uint32_t n_bins, const int32_t *h_parent,
+                             const uint32_t *h_node_sizes, uint32_t world, uint32_t *d_send, uint32_t *d_real) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (!h_node_offsets) throw ApiError(SFXB_ERR_ARG, "accumulate_part: host node offsets required");
+        if (h_parent && !h_node_sizes) throw ApiError(SFXB_ERR_ARG, "accumulate_part: node sizes required");
+        accumulate_part(c, g, d_bins, n_features, d_node_offsets, h_node_offsets, n_nodes, d_rows, n_rows, n_bins,
+                        h_parent, h_node_sizes, world, d_send, d_real);
+    });
+}
+
+int sfxb_combine_slices_dev(sfxb_ctx *c, const sfxb_gh *g, const uint32_t *d_recv, uint32_t world, uint32_t rank,
+                            uint32_t n_nodes, uint32_t n_features, uint32_t n_bins, const int32_t *h_parent,
+                            const uint32_t *h_node_sizes, uint32_t *d_out) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (h_parent && !h_node_sizes) throw ApiError(SFXB_ERR_ARG, "combine_slices: node sizes required");
+        combine_slices(c, g, d_recv, world, rank, n_nodes, n_features, n_bins, h_parent, h_node_sizes, d_out);
+    });
+}
+
+uint32_t sfxb_slice_width(uint32_t n_features, uint32_t n_bins, uint32_t world) {
+    return world ? slice_width(n_features, n_bins, world) : 0;
+}
+
+int sfxb_count_additions_dev(sfxb_ctx *c, const uint32_t *d_real, size_t n, uint64_t *additions) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        unsigned long long *d_adds = reinterpret_cast<unsigned long long *>(bget<uint32_t>(hist_bufs(c).g_misc, 4));
+        CK(cudaMemsetAsync(d_adds, 0, 8, c->stream));
+        dev::PeerSet one{};
+        one.p[0] = d_real;
+        one.n = 1;
+        if (n) {
+            const int grid = (int)std::min<size_t>((n + 255) / 256, (size_t)c->sms * 8);
+            dev::k_adds_multi<<<grid, 256, 0, c->stream>>>(one, n, d_adds);
+            check_launch(*c);
+        }
+        unsigned long long h = 0;
+        CK(cudaMemcpyAsync(&h, d_adds, 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (additions) *additions += h;
     });
 }
 

@@ -15,6 +15,13 @@ modular product, so the partials cannot be combined by an NCCL sum; instead
 The collective and the layout logic are independent of the reduce, so the
 CPU tests drive the same functions with the gloo backend and an oracle
 reduce (tests/test_dist_cpu.py).
+
+Tree mode (sibling subtraction) uses column slices instead (the device
+group's order, include/sfxb_cuda.h "rank-sliced histograms"): every node's
+2·J·K slots are cut into `world` column blocks of jl, rank k owns block k of
+every node, builds only the smaller siblings' partials, and derives the
+larger ones on its own block after the exchange — the batch inversion and
+the per-slot work shard with the ranks.
 """
 from __future__ import annotations
 
@@ -76,3 +83,55 @@ def gather_slices(local: torch.Tensor, n_slots: int, world: int, group=None) -> 
     parts = [torch.empty_like(local) for _ in range(world)]
     dist.all_gather(parts, local.contiguous(), group=group)
     return torch.cat(parts, 0)[:n_slots]
+
+
+def column_blocks(spn: int, world: int) -> tuple[int, list[tuple[int, int]]]:
+    """Slot-column blocks of every node: width jl = ceil(spn / world) and the
+    [lo, hi) columns of block k (the last may be short or empty)."""
+    jl = (spn + world - 1) // world
+    return jl, [(min(k * jl, spn), min((k + 1) * jl, spn)) for k in range(world)]
+
+
+def to_column_slices(part, n_nodes: int, spn: int, world: int):
+    """Reference layout of sfxb_accumulate_part_dev's output: [n_nodes*spn, cw]
+    -> [world, n_nodes*jl, cw], block k = columns of block k of every node
+    (zero padding past spn).  Used by the CPU tests."""
+    import numpy as np
+
+    jl, blocks = column_blocks(spn, world)
+    cw = part.shape[1]
+    p3 = np.asarray(part).reshape(n_nodes, spn, cw)
+    out = np.zeros((world, n_nodes, jl, cw), dtype=p3.dtype)
+    for k, (lo, hi) in enumerate(blocks):
+        out[k, :, : hi - lo] = p3[:, lo:hi]
+    return out.reshape(world, n_nodes * jl, cw)
+
+
+def gather_columns(local: torch.Tensor, n_nodes: int, spn: int, world: int, group=None) -> torch.Tensor:
+    """Every rank's plain block [n_nodes*jl, cw] -> the full [n_nodes*spn, cw]
+    histogram (node-major, as accumulate_rows returns it)."""
+    jl = (spn + world - 1) // world
+    cw = local.shape[1]
+    if world == 1:
+        parts = [local]
+    elif local.is_cuda and dist.get_backend(group) == "gloo":
+        parts = [torch.empty(local.shape, dtype=local.dtype) for _ in range(world)]
+        dist.all_gather(parts, local.cpu().contiguous(), group=group)
+        parts = [x.to(local.device) for x in parts]
+    else:
+        parts = [torch.empty_like(local) for _ in range(world)]
+        dist.all_gather(parts, local.contiguous(), group=group)
+    full = torch.stack([x.view(n_nodes, jl, cw) for x in parts], 1)  # [n_nodes, world, jl, cw]
+    return full.reshape(n_nodes, world * jl, cw)[:, :spn].reshape(n_nodes * spn, cw)
+
+
+def all_reduce_counts(real: torch.Tensor, group=None) -> torch.Tensor:
+    """SUM of the per-slot real-ciphertext counts over ranks (int32)."""
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        if real.is_cuda and dist.get_backend(group) == "gloo":
+            host = real.cpu()
+            dist.all_reduce(host, group=group)
+            real.copy_(host)
+        else:
+            dist.all_reduce(real, group=group)
+    return real
