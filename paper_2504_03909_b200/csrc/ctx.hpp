@@ -119,6 +119,8 @@ struct CtxState {
     // empty for a single-device context
     std::vector<::sfxb_ctx *> shards;
     cudaEvent_t ev_part = nullptr; // this shard's partial histograms are complete
+    cudaStream_t copy_stream = nullptr; // pipelined gh upload (sfxb_gh_upload)
+    cudaEvent_t ev_chunk[8] = {};
     uint32_t tree_j0 = 0, tree_jl = 0, tree_G = 0; // group tree cache: this shard's slot slice
     // one spare gh allocation (limbs + flags), recycled by the next upload
     void *spare_gh = nullptr, *spare_flags = nullptr;

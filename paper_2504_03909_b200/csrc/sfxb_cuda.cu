@@ -583,41 +583,76 @@ dev::NdArgs nd_args(const sfxb_ctx *c) {
     return a;
 }
 
-void gh_prepare(sfxb_ctx *c, sfxb_gh *g) {
-    const size_t S4 = 4 * (size_t)c->s, n2 = 2 * (size_t)g->n_samples;
+void h2d_padded(sfxb_ctx *c, uint32_t *d, const uint32_t *h, size_t count, size_t words, size_t stride);
+
+// Trivial-zero flags and the resident form (digits / Montgomery) of gh rows
+// [lo, hi), on the context stream.
+void gh_prepare_range(sfxb_ctx *c, sfxb_gh *g, size_t lo, size_t hi) {
+    if (hi <= lo) return;
+    const size_t S4 = 4 * (size_t)c->s, rows = hi - lo, n2 = 2 * rows;
+    uint32_t *d = g->d + 2 * lo * S4;
     dispatch_class(c->s, [&](auto sc) {
         constexpr int cs = decltype(sc)::value;
         using C = Cls<cs>;
-        if (g->n_samples) {
-            int grid = (int)std::min<size_t>((g->n_samples + 255) / 256, (size_t)c->sms * 8);
-            dev::k_gh_flags<4 * cs><<<grid, 256, 0, c->stream>>>(g->d, g->n_samples, 2 * c->nw, g->flags);
+        int grid = (int)std::min<size_t>((rows + 255) / 256, (size_t)c->sms * 8);
+        dev::k_gh_flags<4 * cs><<<grid, 256, 0, c->stream>>>(d, (uint32_t)rows, 2 * c->nw, g->flags + lo);
+        check_launch(*c);
+        if (g->digits) {
+            // key holder: CRT digits mod p², q² (padic.cuh "K2 at the key holder")
+            auto k = dev::k_gh_digits<cs, C::TQ>;
+            constexpr int NI = dev::kBlock / C::TQ;
+            k<<<occupancy_grid(*c, k, n2, NI), dev::kBlock, 0, c->stream>>>(crt_args(c), d, n2);
             check_launch(*c);
-            if (crt_histogram(c)) {
-                // key holder: CRT digits mod p², q² (padic.cuh "K2 at the key holder")
-                auto k = dev::k_gh_digits<cs, C::TQ>;
-                constexpr int NI = dev::kBlock / C::TQ;
-                k<<<occupancy_grid(*c, k, n2, NI), dev::kBlock, 0, c->stream>>>(crt_args(c), g->d, n2);
+        } else {
+            auto k = dev::k_to_mont<4 * cs, C::TH>;
+            constexpr int NI = dev::kBlock / C::TH;
+            k<<<occupancy_grid(*c, k, n2, NI), dev::kBlock, 0, c->stream>>>(arg(c->mod_n2), d, n2);
+            check_launch(*c);
+            if (g->digits_n) {
+                auto ks = dev::k_gh_split_n<2 * cs, C::TND>;
+                constexpr int NIs = dev::kBlock / C::TND;
+                ks<<<occupancy_grid(*c, ks, n2, NIs), dev::kBlock, 0, c->stream>>>(nd_args(c), d, n2);
                 check_launch(*c);
-                g->digits = true;
-            } else {
-                auto k = dev::k_to_mont<4 * cs, C::TH>;
-                constexpr int NI = dev::kBlock / C::TH;
-                int grid2 = occupancy_grid(*c, k, n2, NI);
-                k<<<grid2, dev::kBlock, 0, c->stream>>>(arg(c->mod_n2), g->d, n2);
-                check_launch(*c);
-                g->digits = false;
-                g->digits_n = false;
-                if (nd_histogram(c)) {
-                    auto ks = dev::k_gh_split_n<2 * cs, C::TND>;
-                    constexpr int NIs = dev::kBlock / C::TND;
-                    ks<<<occupancy_grid(*c, ks, n2, NIs), dev::kBlock, 0, c->stream>>>(nd_args(c), g->d, n2);
-                    check_launch(*c);
-                    g->digits_n = true;
-                }
             }
         }
     });
-    (void)S4;
+}
+
+void gh_choose_form(sfxb_ctx *c, sfxb_gh *g) {
+    g->digits = crt_histogram(c);
+    g->digits_n = !g->digits && nd_histogram(c);
+}
+
+void gh_prepare(sfxb_ctx *c, sfxb_gh *g) {
+    gh_choose_form(c, g);
+    gh_prepare_range(c, g, 0, g->n_samples);
+}
+
+// Host gh rows -> device, pipelined: chunk k's copy (copy stream) overlaps
+// the conversion of chunk k−1 (context stream).
+void gh_upload_pipelined(sfxb_ctx *c, sfxb_gh *g, const uint32_t *gh_cts) {
+    const size_t S4 = 4 * (size_t)c->s, cw = 2 * (size_t)c->nw, n = g->n_samples;
+    gh_choose_form(c, g);
+    if (cw != S4 || n < 65536) { // padded layout or small: one shot
+        if (n) h2d_padded(c, g->d, gh_cts, 2 * n, cw, S4);
+        gh_prepare_range(c, g, 0, n);
+        return;
+    }
+    if (!c->copy_stream) CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    constexpr int kChunks = 8;
+    if (!c->ev_chunk[0])
+        for (int k = 0; k < kChunks; ++k) CK(cudaEventCreateWithFlags(&c->ev_chunk[k], cudaEventDisableTiming));
+    // the copy stream must not overwrite rows still read by earlier work
+    CK(cudaEventRecord(c->ev_chunk[0], c->stream));
+    CK(cudaStreamWaitEvent(c->copy_stream, c->ev_chunk[0], 0));
+    for (int k = 0; k < kChunks; ++k) {
+        const size_t lo = n * k / kChunks, hi = n * (k + 1) / kChunks;
+        CK(cudaMemcpyAsync(g->d + 2 * lo * S4, gh_cts + 2 * lo * cw, 2 * (hi - lo) * S4 * 4, cudaMemcpyHostToDevice,
+                           c->copy_stream));
+        CK(cudaEventRecord(c->ev_chunk[k], c->copy_stream));
+        CK(cudaStreamWaitEvent(c->stream, c->ev_chunk[k], 0));
+        gh_prepare_range(c, g, lo, hi);
+    }
 }
 
 sfxb_gh *gh_alloc(sfxb_ctx *c, uint32_t n_samples) {
@@ -1863,6 +1898,12 @@ void sfxb_ctx_destroy(sfxb_ctx *c) {
     }
     cudaSetDevice(c->device);
     if (c->ev_part) cudaEventDestroy(c->ev_part);
+    for (auto &e : c->ev_chunk)
+        if (e) cudaEventDestroy(e);
+    if (c->copy_stream) {
+        cudaStreamSynchronize(c->copy_stream);
+        cudaStreamDestroy(c->copy_stream);
+    }
     free_hist_bufs(c);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (void *d : c->owned) cudaFree(d);
@@ -2048,9 +2089,7 @@ int sfxb_gh_upload(sfxb_ctx *c, const uint32_t *gh_cts, uint32_t n_samples, sfxb
         }
         CK(cudaSetDevice(c->device));
         std::unique_ptr<sfxb_gh> g(gh_alloc(c, n_samples));
-        const size_t S4 = 4 * (size_t)c->s;
-        if (n_samples) h2d_padded(c, g->d, gh_cts, 2 * (size_t)n_samples, 2 * c->nw, S4);
-        gh_prepare(c, g.get());
+        gh_upload_pipelined(c, g.get(), gh_cts);
         CK(cudaStreamSynchronize(c->stream));
         *out = g.release();
     });
