@@ -63,8 +63,8 @@ struct CtxState {
     uint8_t *d_dig_m1[2] = {nullptr, nullptr}; // p−1, q−1
     int nd_m1[2] = {0, 0};
     // sliding-window programs (host::sliding_ops) for the digit exponentiations
-    uint8_t *d_ops_pq[2] = {nullptr, nullptr}, *d_ops_m1[2] = {nullptr, nullptr};
-    int nops_pq[2] = {0, 0}, nops_m1[2] = {0, 0};
+    uint8_t *d_ops_pq[2] = {nullptr, nullptr}, *d_ops_m1[2] = {nullptr, nullptr}, *d_ops_e1[2] = {nullptr, nullptr};
+    int nops_pq[2] = {0, 0}, nops_m1[2] = {0, 0}, nops_e1[2] = {0, 0};
 
     // optional per-kernel-family CUDA-event timing (bench roofline):
     // family 0 = K2 segmented product, 1 = K1 encrypt exps, 2 = K3 decrypt exp

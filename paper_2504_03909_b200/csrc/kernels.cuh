@@ -116,6 +116,8 @@ struct EncArgs {
     ModArg mod_n2;          // S = 4s
     const uint8_t *dig_e1[2];
     int nd_e1[2];
+    const uint8_t *ops_e1[2]; // sliding-window programs of e1 (preferred when set)
+    int nops_e1[2];
     const uint8_t *dig_pq[2];
     int nd_pq[2];
     const uint8_t *dig_n;
@@ -154,7 +156,8 @@ __global__ void __launch_bounds__(kBlock) k_enc_step1(EncArgs a) {
             atomicOr(a.status, 1u);
             if (a.flags) a.flags[e] = 1;
         }
-        mont_pow<S, TPI>(x, a.dig_e1[which], a.nd_e1[which], W, table, M, st, N);
+        if (a.ops_e1[which]) mont_pow_ops<S, TPI>(x, a.ops_e1[which], a.nops_e1[which], W, table, M, st, N);
+        else mont_pow<S, TPI>(x, a.dig_e1[which], a.nd_e1[which], W, table, M, st, N);
         from_mont<S, TPI>(x, x, st, N, M.np);
         if (active) {
             uint32_t *dst = a.x + (e * 2 + which) * 2 * S;

@@ -264,5 +264,71 @@ __device__ __forceinline__ void mont_pow(uint32_t (&x)[S / TPI], const uint8_t *
     for (int k = 0; k < L; ++k) x[k] = acc[k];
 }
 
+// Sliding-window exponentiation in the Montgomery domain: x <- x^e with e as
+// a host::sliding_ops program (n_ops byte pairs: squarings, odd digit).
+// `table` = this instance's scratch of 2^(w−1) + 1 entries of S words: x^1,
+// x^3, …, x^(2^w − 1), then x².  One Montgomery multiply call site.
+template <int S, int TPI>
+__device__ __forceinline__ void mont_pow_ops(uint32_t (&x)[S / TPI], const uint8_t *ops, int n_ops, int w,
+                                             uint32_t *table, const ModRef &M, const Stage &st,
+                                             const uint32_t (&N)[S / TPI]) {
+    constexpr int L = S / TPI;
+    const int T = 1 << (w - 1);
+    uint32_t *x2 = table + S * T;
+    store_lane<S, TPI>(table, x);
+    uint32_t acc[L];
+#pragma unroll
+    for (int k = 0; k < L; ++k) acc[k] = x[k];
+    int j = -1, oi = 0, sq = 0;
+    bool started = false;
+    for (;;) {
+        bool square;
+        const uint32_t *bsrc = nullptr;
+        if (j < T - 1) {
+            square = j < 0;
+            bsrc = x2;
+        } else {
+            if (!started) {
+                load_lane<S, TPI>(acc, table + S * (ops[1] >> 1));
+                oi = 1;
+                sq = n_ops > 1 ? ops[2] : 0;
+                started = true;
+            }
+            if (sq > 0) {
+                square = true;
+            } else {
+                if (oi >= n_ops) break;
+                const int d = ops[2 * oi + 1];
+                ++oi;
+                sq = oi < n_ops ? ops[2 * oi] : 0;
+                if (d == 0) continue;
+                square = false;
+                bsrc = table + S * (d >> 1);
+            }
+        }
+        uint32_t b[L];
+        if (square) {
+#pragma unroll
+            for (int k = 0; k < L; ++k) b[k] = acc[k];
+        } else {
+            load_lane<S, TPI>(b, bsrc);
+        }
+        mmul<S, TPI>(acc, acc, b, st, N, M.np);
+        if (j < T - 1) {
+            if (j < 0) {
+                store_lane<S, TPI>(x2, acc);
+                load_lane<S, TPI>(acc, table);
+            } else {
+                store_lane<S, TPI>(table + S * (j + 1), acc);
+            }
+            ++j;
+        } else if (square) {
+            --sq;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < L; ++k) x[k] = acc[k];
+}
+
 } // namespace dev
 } // namespace sfxb

@@ -312,6 +312,8 @@ void encrypt_dev(sfxb_ctx *c, const int64_t *d_q, const uint32_t *d_r, size_t co
             a.mod_pq2[i] = arg(c->mod_pq2[i]);
             a.dig_e1[i] = c->d_dig_e1[i];
             a.nd_e1[i] = c->nd_e1[i];
+            a.ops_e1[i] = c->d_ops_e1[i];
+            a.nops_e1[i] = c->nops_e1[i];
             a.dig_pq[i] = c->d_dig_pq[i];
             a.nd_pq[i] = c->nd_pq[i];
         }
@@ -1767,6 +1769,15 @@ int sfxb_ctx_create(sfxb_ctx **out, int device, const uint32_t *n, uint32_t n_wo
                 c->nops_pq[i] = (int)host_window[i].dig_pr.size() / 2;
                 c->d_ops_m1[i] = dev_upload(*c, host_window[i].dig_pm1.data(), host_window[i].dig_pm1.size());
                 c->nops_m1[i] = (int)host_window[i].dig_pm1.size() / 2;
+                {
+                    const std::vector<uint8_t> e1ops = host::sliding_ops(host::mod(ot, pm1), kWindow);
+                    c->d_ops_e1[i] = dev_upload(*c, e1ops.data(), e1ops.size());
+                    c->nops_e1[i] = (int)e1ops.size() / 2;
+                    // step 1 (mod p, s limbs) runs the sliding program
+                    uint64_t m1 = 1 + ((1ull << (kWindow - 1)) - 1);
+                    for (size_t k = 1; k < e1ops.size() / 2; ++k) m1 += e1ops[2 * k] + (e1ops[2 * k + 1] ? 1 : 0);
+                    host_window[i].e1 = m1;
+                }
                 c->d_pinv[i] = dev_big(*c, host::inv_pow2(pr, s), s);
                 // h = (−other mod prime)^-1 mod prime, in Montgomery form
                 Big negot = host::sub(pr, host::mod(ot, pr));
