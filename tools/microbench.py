@@ -7,7 +7,7 @@ decrypt throughput over batch sizes and key sizes on one B200.
 One JSON line per (op, bits, size): throughput from CUDA events on the
 context stream (inputs resident in HBM, warm-up call at the same size
 first), and the fraction of the IMAD.WIDE peak from the multiplications the
-kernels executed.  "add" folds k ciphertexts (k/2 rows × (G, H)) into 256
+kernels executed.  "add" / "add_pub" (key holder / passive party) fold k ciphertexts (k/2 rows × (G, H)) into 256
 bins with uniform-random bin ids (seed 1) and counts k − occupied additions,
 as the reference's counter does.  Sizes whose estimated time exceeds
 --max-seconds (from the previous size's rate) are skipped and reported so.
@@ -44,7 +44,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--bits", type=int, nargs="+", default=[1024, 2048, 3072])
     ap.add_argument("--sizes", type=int, nargs="+", default=[1024, 16384, 262144, 4194304])
-    ap.add_argument("--ops", nargs="+", default=["enc", "enc_pub", "add", "dec"])
+    ap.add_argument("--ops", nargs="+", default=["enc", "enc_pub", "add", "add_pub", "dec"])
     ap.add_argument("--max-seconds", type=float, default=20.0)
     a = ap.parse_args()
     dev = torch.device("cuda:0")
@@ -58,7 +58,8 @@ def main():
         prod_p2 = 2 * s2 * s2 + s2
         prod_n2 = 2 * cw * cw + cw
         for op in a.ops:
-            c = ctx if op != "enc_pub" else pub
+            # key holder (CRT digits) vs passive party (public key: base-n digits)
+            c = pub if op in ("enc_pub", "add_pub") else ctx
             ops = _lib.DeviceOps(c)
             stream = torch.cuda.ExternalStream(c.lib.sfxb_ctx_stream(c.h), device=dev)
             rate = None
