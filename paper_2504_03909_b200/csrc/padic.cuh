@@ -458,6 +458,9 @@ __global__ void __launch_bounds__(kBlock) k_gh_digits(CrtArgs a, uint32_t *gh, s
 #ifndef SFXB_ND_MINB
 #define SFXB_ND_MINB 1
 #endif
+#ifndef SFXB_ND_PREFETCH
+#define SFXB_ND_PREFETCH 0
+#endif
 #ifndef SFXB_K_MINB
 #define SFXB_K_MINB 1
 #endif
@@ -665,6 +668,13 @@ __global__ void __launch_bounds__(kBlock, SFXB_ND_MINB) k_seg_prod_nd(NdArgs a, 
         for (int k = 1; k < C; ++k) {
             const bool more = active && (uint32_t)k < pc.len;
             if (!__any_sync(0xffffffffu, more)) break; // warp-uniform exit
+#if SFXB_ND_PREFETCH
+            if (more && (uint32_t)k + 1 < pc.len && inst_lane<TPI>() == 0) {
+                const uint32_t *nx = item_ptr((uint32_t)k + 1);
+#pragma unroll
+                for (int o = 0; o < 2 * S; o += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(nx + o));
+            }
+#endif
             p2_mul<S, TPI>(A, B, more ? item_ptr((uint32_t)k) : a.one, false, st, sD, N, M.np, M.w + kOne * S,
                            a.negR);
         }
