@@ -436,6 +436,18 @@ __global__ void __launch_bounds__(kBlock) k_reduce_peer(ModArg M, PeerSet parts,
     }
 }
 
+// Columns past the slots of a node in rank-sliced blocks (2·J·K not a
+// multiple of world) hold the Montgomery one, so that the cross-rank product
+// and the batch inversion of sibling subtraction see units there.
+__global__ void k_fill_pad(uint32_t *send, uint32_t world, size_t n_nodes, size_t jl, size_t spn, int S,
+                           const uint32_t *one) {
+    const size_t total = (size_t)world * n_nodes * jl * S;
+    for (size_t w = (size_t)blockIdx.x * blockDim.x + threadIdx.x; w < total; w += (size_t)gridDim.x * blockDim.x) {
+        const size_t slot = w / S, k = slot / (n_nodes * jl), j = slot % jl;
+        if (k * jl + j >= spn) send[w] = one[w % S];
+    }
+}
+
 // per (key, gh): real (non-trivial-zero) ciphertexts folded into the slot
 __global__ void k_hist_real(const uint32_t *count, const uint32_t *ones, size_t nkeys, uint32_t *real) {
     for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < nkeys; k += (size_t)gridDim.x * blockDim.x) {

@@ -1455,7 +1455,12 @@ void accumulate_part(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint
     uint32_t *part = bget<uint32_t>(B.g_part, (size_t)N * spn * S4);
     accumulate_dev(c, g, d_bins, J, d_offs, N, d_rows, R, K, part, 1, nullptr, nullptr, h_offs, skip.data(), d_real);
     cudaStream_t st = c->stream;
-    if (jl * world != spn) CK(cudaMemsetAsync(d_send, 0, (size_t)world * N * jl * S4 * 4, st));
+    if (jl * world != spn && N) {
+        const size_t words = (size_t)world * N * jl * S4;
+        const int grid = (int)std::min<size_t>((words + 255) / 256, (size_t)c->sms * 16);
+        dev::k_fill_pad<<<grid, 256, 0, st>>>(d_send, world, N, jl, spn, (int)S4, c->mod_n2.w + S4); // R mod n²
+        check_launch(*c);
+    }
     for (uint32_t k = 0; k < world && N; ++k) {
         const size_t lo = (size_t)k * jl, w = lo < spn ? std::min<size_t>(jl, spn - lo) : 0;
         if (w)

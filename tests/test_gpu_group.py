@@ -157,3 +157,67 @@ def test_group_decrypt_tree_equals_single():
         got, gd = grp.decrypt_tree(5, h, len(nodes), par)
         assert np.array_equal(got.view(np.int64), want.view(np.int64)) and gd == wd
     assert grp.dec_derived == one.dec_derived > 0
+
+
+@pytest.mark.parametrize("private", [False, True])
+@pytest.mark.parametrize("world,J,K", [(3, 1, 5), (4, 2, 3), (2, 3, 8)])
+def test_rank_sliced_histograms_equal_single(world, J, K, private):
+    """The one-process-per-GPU entry points (sfxb_accumulate_part_dev, the
+    caller's all_to_all + count all_reduce, sfxb_combine_slices_dev) with
+    `world` contexts on this GPU standing in for the ranks and the exchange
+    done by hand: tree-mode histograms and the reference counter equal one
+    context's, level by level, incl. padded column blocks (2·J·K not a
+    multiple of world)."""
+    import torch
+
+    from paper_2504_03909_b200 import dist as pdist
+
+    kname = "k512_c0ffee"
+    n, p, q = key(kname)
+    mk = (lambda: _lib.Context(n, p, q)) if private else (lambda: _lib.Context(n))
+    one, ranks = mk(), [mk() for _ in range(world)]
+    o1, ops = _lib.DeviceOps(one), [_lib.DeviceOps(c) for c in ranks]
+    rng = random.Random(f"{world}{J}{K}{private}")
+    n_samples, depth = 400, 4
+    cts = [rng.randrange(2, n * n) for _ in range(2 * n_samples)]
+    cts[3] = 1
+    cw = ints_to_words(cts, one.ct_words)
+    bins = np.array([[rng.randrange(K) for _ in range(n_samples)] for _ in range(J)], np.uint16)
+    dev = torch.device("cuda:0")
+    g1 = o1.gh_upload(cw)
+    spans = [pdist.row_shard(n_samples, world, r) for r in range(world)]
+    ghs = [ops[r].gh_upload(cw[2 * lo:2 * hi]) for r, (lo, hi) in enumerate(spans)]
+    d_bins = [torch.from_numpy(bins[:, lo:hi].astype(np.int16).copy()).to(dev) for lo, hi in spans]
+    spn = 2 * J * K
+    jl = ops[0].slice_width(J, K, world)
+    assert jl == (spn + world - 1) // world
+    for lvl, (nodes, parents) in enumerate(_random_tree(rng, n_samples, depth)):
+        N = len(nodes)
+        offs, rows = frontier(nodes)
+        par = np.array(parents, np.int32)
+        sizes = np.diff(offs).astype(np.uint32)
+        want, want_adds = o1.accumulate_tree_host(g1, bins, offs, rows, K, par)
+        sends, reals = [], []
+        for r, (lo, hi) in enumerate(spans):
+            sub = [[x - lo for x in nd if lo <= x < hi] for nd in nodes]
+            so, sr = frontier(sub)
+            d_off = torch.from_numpy(so.astype(np.int32)).to(dev)
+            d_rows = torch.from_numpy(sr.astype(np.int32) if len(sr) else np.zeros(1, np.int32)).to(dev)
+            send = torch.zeros((world * N * jl, one.ct_words), dtype=torch.int32, device=dev)
+            real = torch.zeros(2 * N * J * K, dtype=torch.int32, device=dev)
+            ops[r].accumulate_part(ghs[r], d_bins[r], J, d_off, so, N, d_rows, len(sr), K, par, sizes, world,
+                                   send, real)
+            sends.append(send.view(world, N * jl, one.ct_words))
+            reals.append(real)
+        total = sum(reals)
+        adds = ops[0].count_additions(total, 2 * N * J * K)
+        assert adds == want_adds, lvl
+        blocks = []
+        for r in range(world):
+            recv = torch.stack([sends[k][r] for k in range(world)]).contiguous()  # the all_to_all
+            out = torch.zeros((N * jl, one.ct_words), dtype=torch.int32, device=dev)
+            ops[r].combine_slices(ghs[r], recv, world, r, N, J, K, par, sizes, out)
+            blocks.append(out.cpu().numpy().view(np.uint32).reshape(N, jl, -1))
+        got = np.concatenate(blocks, 1)[:, :spn].reshape(N * spn, -1)
+        assert np.array_equal(got, want), lvl
+    assert sum(c.lib.sfxb_ctx_tree_derived(c.h) for c in ranks) > 0
