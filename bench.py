@@ -392,7 +392,9 @@ def run_ours(a):
         recv = pdist.exchange(sends[d][pi], world)
         pdist.all_reduce_counts(reals[d][pi])
         adds = ops[pi].count_additions(reals[d][pi], 2 * N * J * K) if rank == 0 else 0
-        ops[pi].combine_slices(g, recv, world, rank, N, J, K, parents[d], sizes[d], slices[d][pi], sync=False)
+        # sync=True: torch's stream (the collectives) drains before the context
+        # stream reads the received blocks
+        ops[pi].combine_slices(g, recv, world, rank, N, J, K, parents[d], sizes[d], slices[d][pi])
         return adds
     stream = torch.cuda.ExternalStream(ctxs[0].lib.sfxb_ctx_stream(ctxs[0].h), device=dev)
 

@@ -321,3 +321,31 @@ def test_histogram_mod_n2_path_for_keys_short_of_their_class(private):
                         if bins[f][r] == b:
                             want = want * cts[2 * r + g] % (n * n)
                     assert got[((ni * J + f) * K + b) * 2 + g] == want
+
+
+@pytest.mark.parametrize("private", [False, True])
+def test_pipelined_gh_upload_equals_device_copy(private):
+    """sfxb_gh_upload of >= 65536 rows runs chunked copies on a copy stream
+    overlapped with the per-chunk conversion (digits / Montgomery form): the
+    histogram equals the one of a handle built from a device copy."""
+    import torch
+
+    n, p, q = key("k512_c0ffee")
+    ctx = _lib.Context(n, p, q) if private else _lib.Context(n)
+    ops = _lib.DeviceOps(ctx)
+    rng = np.random.default_rng(11)
+    n_samples, J, K = 70001, 2, 16
+    cw = rng.integers(0, 2**32, (2 * n_samples, ctx.ct_words), dtype=np.uint64).astype(np.uint32)
+    cw[:, -1] &= 0x3FFFFFFF  # < 2^(32·cw − 2) < n²
+    cw[7] = 0
+    cw[7, 0] = 1  # a trivial zero
+    bins = rng.integers(0, K, (J, n_samples), dtype=np.uint16)
+    offs = np.array([0, 30000, 65000], np.uint32)
+    rows = rng.permutation(n_samples)[:65000].astype(np.uint32)
+    rows[:30000].sort()
+    rows[30000:].sort()
+    g_host = ops.gh_upload(cw)
+    g_dev = ops.gh_from_dev(torch.from_numpy(cw.view(np.int32)).cuda(), n_samples)
+    a, adds_a = ops.accumulate_host(g_host, bins, offs, rows, K)
+    b, adds_b = ops.accumulate_host(g_dev, bins, offs, rows, K)
+    assert np.array_equal(a, b) and adds_a == adds_b > 0
