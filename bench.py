@@ -74,6 +74,7 @@ def parse():
     ap.add_argument("--cpu-sample-rows", type=int, default=12000, help="per host thread (reference arm)")
     ap.add_argument("--cpu-rows", type=int, default=40000, help="single-core cpu_baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-plugin-e2e", action="store_true", help="skip the reference-facing plugin timing")
     ap.add_argument("--no-tree", action="store_true", help="disable sibling subtraction (direct histograms)")
     ap.add_argument("--check", action="store_true",
                     help="N>1: rank 0 recomputes every level's histograms from all rows on one GPU and compares "
@@ -230,6 +231,33 @@ def cpu_baseline(a, n, nw, adds_tree, threads: int = 1):
 
 
 # ------------------------------------------------------------------ reference arm
+
+
+def plugin_e2e(a):
+    """The reference-facing end to end: tools/plugin_bench.cpp drives the
+    reference's EncryptionPlugin calls of one tree (encrypt_gh, accumulate_rows
+    per level and party, decrypt_histogram per level and party) with the GPU
+    adapter LD_PRELOADed over the unmodified reference library — host
+    marshalling of the reference's mpz payloads included.  Two trees, the
+    second reported (the first grows buffers)."""
+    import subprocess
+
+    exe = os.path.join(ROOT, "oracle", "_ref", "plugin_bench")
+    plugin = os.path.join(ROOT, "paper_2504_03909_b200", "lib", "libsfxb_cuda_plugin.so")
+    if not (os.path.exists(exe) and os.path.exists(plugin)):
+        return {"unavailable": "oracle/_ref/plugin_bench or the plugin library not built"}
+    bits = {"k512_c0ffee": 512, "k1024_7": 1024, "k2048_7": 2048, "k3072_7": 3072}.get(a.key, 2048)
+    env = dict(os.environ, LD_PRELOAD=plugin)
+    try:
+        out = subprocess.run([exe, str(a.rows), str(a.feats), str(a.bins), str(a.depth), str(bits), str(a.parties),
+                              "2"], env=env, capture_output=True, text=True, timeout=600)
+        res = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": f"plugin_bench failed: {e}"}
+    res["pattern"] = ("reference EncryptionPlugin calls of one tree through the GPU adapter (LD_PRELOAD over "
+                      "oracle/_ref/libsfxb_ref.so): encrypt_gh (2 x rows ciphertexts), accumulate_rows per level "
+                      "and party, decrypt_histogram of every party's histograms; keygen(bits, 7)")
+    return res
 
 
 def run_reference(a):
@@ -681,6 +709,8 @@ def run_ours(a):
         "check": check,
         "clocks": clk.summary(),
     }
+    if world == 1 and not a.no_plugin_e2e:
+        line["plugin_e2e"] = plugin_e2e(a)
     if world == 1 and not a.no_cpu:
         try:
             line["cpu_baseline"] = cpu_baseline(a, n, nw, adds_tree_ref, threads=1)

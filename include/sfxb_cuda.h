@@ -77,6 +77,11 @@ int sfxb_ctx_create(sfxb_ctx **out, int device, const uint32_t *n, uint32_t n_wo
  * SFXB_ERR_UNSUPPORTED on a group (its gradient handle is host-API only). */
 int sfxb_ctx_create_multi(sfxb_ctx **out, const int *devices, uint32_t n_devices, const uint32_t *n,
                           uint32_t n_words, const uint32_t *p, const uint32_t *q, uint32_t pq_words);
+/* Page-locked host memory for callers' marshalling buffers: host-pointer
+ * entry points copy from / to it at full PCIe speed (pageable buffers are
+ * staged by the driver).  NULL on failure. */
+void *sfxb_host_alloc(size_t bytes);
+void sfxb_host_free(void *p);
 /* visible CUDA devices (0 without a driver/GPU) */
 int sfxb_device_count(void);
 /* shards of a context (1 for sfxb_ctx_create) and the device of shard k */

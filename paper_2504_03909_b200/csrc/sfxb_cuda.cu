@@ -1112,15 +1112,21 @@ void encrypt_host(sfxb_ctx *c, const int64_t *q_fixed, const uint32_t *m_words, 
     if (count == 0) return;
     const size_t Sn = 2 * (size_t)c->s, S4 = 4 * (size_t)c->s;
     // range checks of encrypt_with_r (he.cpp:88-89), in its order per element
+    // (word-wise compares against n, no allocation per element)
+    const std::vector<uint32_t> nw_words = host::pad(c->n, c->nw);
+    auto lt_n = [&](const uint32_t *x) {
+        for (uint32_t k = c->nw; k-- > 0;)
+            if (x[k] != nw_words[k]) return x[k] < nw_words[k];
+        return false; // equal
+    };
     for (size_t i = 0; i < count; ++i) {
-        if (m_words && host::cmp(host::from_words(m_words + i * c->nw, c->nw), c->n) >= 0)
+        if (m_words && !lt_n(m_words + i * c->nw))
             throw ApiError(SFXB_ERR_RANGE, "encrypt: plaintext out of range [0, n)");
         const uint32_t *ri = r + i * c->nw;
         bool small = true;
         for (uint32_t k = 1; k < c->nw; ++k) small &= ri[k] == 0;
         if (small && ri[0] < 1) throw ApiError(SFXB_ERR_RANGE, "encrypt: blinding factor out of range");
-        if (host::cmp(host::from_words(ri, c->nw), c->n) >= 0)
-            throw ApiError(SFXB_ERR_RANGE, "encrypt: blinding factor out of range");
+        if (!lt_n(ri)) throw ApiError(SFXB_ERR_RANGE, "encrypt: blinding factor out of range");
     }
     IoBuf<int64_t> dq(c->io[0], m_words ? 1 : count);
     IoBuf<uint32_t> dr(c->io[1], count * Sn), dout(c->io[2], count * S4);
@@ -1185,9 +1191,14 @@ void add_host(sfxb_ctx *c, const uint32_t *a, const uint32_t *b, size_t count, u
     CK(cudaSetDevice(c->device));
     if (count == 0) return;
     const size_t S4 = 4 * (size_t)c->s, cw = 2 * c->nw;
+    const std::vector<uint32_t> n2w = host::pad(c->n2, cw);
+    auto lt_n2 = [&](const uint32_t *x) {
+        for (size_t k = cw; k-- > 0;)
+            if (x[k] != n2w[k]) return x[k] < n2w[k];
+        return false;
+    };
     for (size_t i = 0; i < count; ++i)
-        if (host::cmp(host::from_words(a + i * cw, cw), c->n2) >= 0 ||
-            host::cmp(host::from_words(b + i * cw, cw), c->n2) >= 0)
+        if (!lt_n2(a + i * cw) || !lt_n2(b + i * cw))
             throw ApiError(SFXB_ERR_RANGE, "add_ciphertexts: ciphertext out of range");
     IoBuf<uint32_t> da(c->io[0], count * S4), db(c->io[1], count * S4), dout(c->io[2], count * S4);
     h2d_padded(c, da.p, a, count, cw, S4);
@@ -1888,6 +1899,19 @@ int sfxb_ctx_create_multi(sfxb_ctx **out, const int *devices, uint32_t n_devices
     }
     *out = c;
     return SFXB_OK;
+}
+
+void *sfxb_host_alloc(size_t bytes) {
+    void *p = nullptr;
+    if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+
+void sfxb_host_free(void *p) {
+    if (p) cudaFreeHost(p);
 }
 
 int sfxb_device_count(void) {

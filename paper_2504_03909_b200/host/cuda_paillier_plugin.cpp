@@ -22,6 +22,7 @@
 #include <gmp.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <map>
 #include <cmath>
@@ -52,10 +53,12 @@ unsigned host_threads() {
     return n;
 }
 
+// f(lo, hi) over [0, n) on host_threads() threads; ranges below `grain`
+// items run inline
 template <typename F>
-void parallel_for(size_t n, F &&f) {
+void parallel_for(size_t n, F &&f, size_t grain = 4096) {
     const unsigned T = host_threads();
-    if (n < 4096 || T <= 1) {
+    if (n < grain || n < 2 || T <= 1) {
         f(size_t(0), n);
         return;
     }
@@ -73,6 +76,53 @@ void parallel_for(size_t n, F &&f) {
 // byte-identical to pairs of u32 limbs): raw limb copies, no mpz_import.
 static_assert(sizeof(mp_limb_t) == 8, "64-bit GMP limbs expected");
 
+// SFXB_PLUGIN_PROFILE=1: per-call phase times on stderr (host-side costs of
+// the reference's payload types vs the GPU call)
+struct PhaseTimer {
+    const char *name;
+    bool on;
+    std::chrono::steady_clock::time_point t;
+    std::string line;
+    explicit PhaseTimer(const char *n)
+        : name(n), on(std::getenv("SFXB_PLUGIN_PROFILE") != nullptr), t(std::chrono::steady_clock::now()) {}
+    void lap(const char *phase) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        char buf[64];
+        std::snprintf(buf, sizeof buf, " %s=%.1fms", phase, std::chrono::duration<double, std::milli>(now - t).count());
+        line += buf;
+        t = now;
+    }
+    ~PhaseTimer() {
+        if (on) std::fprintf(stderr, "[sfxb-cuda-plugin] %s%s\n", name, line.c_str());
+    }
+};
+
+// Grow-only page-locked buffer (sfxb_host_alloc) for the marshalled limbs the
+// C ABI copies to / from the device: full-speed DMA, no per-call allocation.
+class PinnedBuf {
+public:
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf &) = delete;
+    PinnedBuf &operator=(const PinnedBuf &) = delete;
+    ~PinnedBuf() { sfxb_host_free(p_); }
+    template <typename T>
+    T *get(size_t n) {
+        const size_t need = std::max<size_t>(n * sizeof(T), 1);
+        if (need > bytes_) {
+            sfxb_host_free(p_);
+            p_ = sfxb_host_alloc(need);
+            bytes_ = p_ ? need : 0;
+            if (!p_) throw sfxb::Error("CUDA Paillier plugin: page-locked host allocation failed");
+        }
+        return static_cast<T *>(p_);
+    }
+
+private:
+    void *p_ = nullptr;
+    size_t bytes_ = 0;
+};
+
 void to_words(const mpz_class &z, uint32_t *out, size_t words) {
     const size_t used = mpz_size(z.get_mpz_t());
     if (used * 2 > words + 1 || mpz_sgn(z.get_mpz_t()) < 0) {
@@ -88,7 +138,10 @@ void to_words(const mpz_class &z, uint32_t *out, size_t words) {
 }
 
 bool fits(const mpz_class &z, size_t words) {
-    return mpz_sgn(z.get_mpz_t()) >= 0 && mpz_sizeinbase(z.get_mpz_t(), 2) <= 32 * words;
+    if (mpz_sgn(z.get_mpz_t()) < 0) return false;
+    // whole 64-bit limbs: the header alone decides (no load of the limbs)
+    if (words % 2 == 0) return mpz_size(z.get_mpz_t()) <= words / 2;
+    return mpz_sizeinbase(z.get_mpz_t(), 2) <= 32 * words;
 }
 
 void from_words(mpz_class &z, const uint32_t *w, size_t words) {
@@ -111,9 +164,31 @@ void from_words(mpz_class &z, const uint32_t *w, size_t words) {
 // ------------------------------------------------------------ the plugin
 
 // previous decrypted level of one histogram stream (one sender's tree)
+// std::vector without value-initialisation of new elements (the limb buffers
+// are overwritten completely; zeroing 100+ MB per call is measurable)
+template <typename T>
+struct NoInitAlloc : std::allocator<T> {
+    template <typename U>
+    struct rebind {
+        using other = NoInitAlloc<U>;
+    };
+    NoInitAlloc() = default;
+    template <typename U>
+    NoInitAlloc(const NoInitAlloc<U> &) {}
+    template <typename U>
+    void construct(U *p) {
+        ::new (static_cast<void *>(p)) U;
+    }
+    template <typename U, typename... A>
+    void construct(U *p, A &&...a) {
+        ::new (static_cast<void *>(p)) U(std::forward<A>(a)...);
+    }
+};
+using LimbVec = std::vector<uint32_t, NoInitAlloc<uint32_t>>;
+
 struct DecStream {
     uint64_t tag = 0; // sfxb_decrypt_tree cache tag
-    std::vector<uint32_t> cts;
+    LimbVec cts;
     uint32_t n_nodes = 0;
     size_t spn = 0;
     uint64_t last_use = 0;
@@ -181,25 +256,29 @@ public:
             q[i] = v;
             ++ok;
         }
+        PhaseTimer pt("encrypt_gh");
+        pt.lap("encode");
         const size_t nw = n_words_;
-        std::vector<uint32_t> r(ok * nw);
-        draw_blinding(r.data(), ok);
+        uint32_t *r = pin_r_.get<uint32_t>(ok * nw);
+        draw_blinding(r, ok);
+        pt.lap("draw_r");
         if (ok < count) {
             counters_.encryptions += 2 * (ok / 2); // pairs completed before the failure
             throw Error(fail_msg);
         }
-        std::vector<uint32_t> cts(count * ct_words_);
+        uint32_t *cts = pin_cts_.get<uint32_t>(count * ct_words_);
         std::vector<uint8_t> flags(count, 0);
-        int rc = sfxb_encrypt(ctx_, q.data(), r.data(), count, cts.data(), flags.data());
+        int rc = sfxb_encrypt(ctx_, q.data(), r, count, cts, flags.data());
         if (rc == SFXB_ERR_COPRIME) {
             // some r shares a factor with n (probability ~2^-1000): redo the
             // draw with the reference's exact rejection rule from the saved state
             gmp_randclear(rng_);
             gmp_randinit_set(rng_, rng_snapshot_);
-            draw_blinding(r.data(), ok, /*exact_gcd=*/true);
-            rc = sfxb_encrypt(ctx_, q.data(), r.data(), count, cts.data(), nullptr);
+            draw_blinding(r, ok, /*exact_gcd=*/true);
+            rc = sfxb_encrypt(ctx_, q.data(), r, count, cts, nullptr);
         }
         check(rc);
+        pt.lap("gpu");
         out.cts.resize(count);
         parallel_for(count, [&](size_t lo, size_t hi) {
             for (size_t i = lo; i < hi; ++i) {
@@ -208,6 +287,7 @@ public:
             }
         });
         counters_.encryptions += count;
+        pt.lap("marshal");
         return out;
     }
 
@@ -224,21 +304,41 @@ public:
         HistogramPayload out;
         out.layout = HistLayout::enc_scalar;
         const size_t J = feature_ids.size(), K = (size_t)std::max(n_bins, 0), N = nodes.size();
-        // bins are checked per visited row, as the reference loop does
-        for (const NodeRows &nd : nodes)
-            for (size_t f = 0; f < J; ++f)
-                for (std::uint32_t row : nd.rows) {
-                    if (row >= gh.n_samples) throw Error("row index out of range in accumulate");
-                    if (bins[f][row] >= static_cast<std::uint16_t>(n_bins))
-                        throw Error("bin index out of range in accumulate");
+        PhaseTimer pt("accumulate_rows");
+        // bins are checked per visited row, as the reference loop does: a
+        // parallel scan, and on a hit the reference's serial order picks the message
+        {
+            std::atomic<bool> bad{false};
+            parallel_for(N * J, [&](size_t lo, size_t hi) {
+                for (size_t t = lo; t < hi && !bad; ++t) {
+                    const NodeRows &nd = nodes[t / J];
+                    const std::vector<std::uint16_t> &col = bins[t % J];
+                    for (std::uint32_t row : nd.rows)
+                        if (row >= gh.n_samples || col[row] >= static_cast<std::uint16_t>(n_bins)) {
+                            bad = true;
+                            break;
+                        }
                 }
+            });
+            if (bad)
+                for (const NodeRows &nd : nodes)
+                    for (size_t f = 0; f < J; ++f)
+                        for (std::uint32_t row : nd.rows) {
+                            if (row >= gh.n_samples) throw Error("row index out of range in accumulate");
+                            if (bins[f][row] >= static_cast<std::uint16_t>(n_bins))
+                                throw Error("bin index out of range in accumulate");
+                        }
+        }
+        pt.lap("validate");
         ensure_gh(gh);
+        pt.lap("ensure_gh");
         std::vector<uint16_t> flat(J * gh.n_samples);
         for (size_t f = 0; f < J; ++f) std::memcpy(&flat[f * gh.n_samples], bins[f].data(), gh.n_samples * 2);
         std::vector<uint32_t> offs(N + 1, 0), rows;
         for (size_t i = 0; i < N; ++i) offs[i + 1] = offs[i] + (uint32_t)nodes[i].rows.size();
         rows.reserve(offs[N]);
         for (const NodeRows &nd : nodes) rows.insert(rows.end(), nd.rows.begin(), nd.rows.end());
+        pt.lap("flatten");
         // Sibling subtraction: the reference's next frontier lists the two
         // children of each split node consecutively, in parent order
         // (federation.cpp:591-592).  A parent is accepted only when the merged
@@ -261,11 +361,14 @@ public:
                 }
             }
         }
-        std::vector<uint32_t> slots(N * J * K * 2 * ct_words_);
+        pt.lap("parents");
+        uint32_t *slots = pin_slots_.get<uint32_t>(N * J * K * 2 * ct_words_);
+        pt.lap("alloc_slots");
         uint64_t adds = 0;
         if (N && J && K)
             check(sfxb_accumulate_tree_gh(ctx_, gh_, flat.data(), (uint32_t)J, offs.data(), (uint32_t)N, rows.data(),
-                                          (uint32_t)K, parent.data(), slots.data(), &adds));
+                                          (uint32_t)K, parent.data(), slots, &adds));
+        pt.lap("gpu");
         prev_valid_ = N && J && K;
         prev_bins_key_ = bins_key;
         prev_gh_ = gh_;
@@ -281,6 +384,7 @@ public:
             nh.n_bins = n_bins;
             nh.scalar_cts.resize(per_node);
         }
+        pt.lap("out_alloc");
         parallel_for(N * per_node, [&](size_t lo, size_t hi) {
             for (size_t s = lo; s < hi; ++s) {
                 Ciphertext &c = out.nodes[s / per_node].scalar_cts[s % per_node];
@@ -288,6 +392,7 @@ public:
                 c.key_id = pub_.key_id;
             }
         });
+        pt.lap("out_marshal");
         return out;
     }
 
@@ -299,33 +404,60 @@ public:
             throw Error("paillier decrypt expects encrypted layouts");
         }
         std::vector<std::pair<std::uint32_t, Histogram>> out;
+        PhaseTimer pt("decrypt_histogram");
         size_t total = 0;
         for (const NodeHistogram &node : payload.nodes)
             total += 2 * node.feature_ids.size() * (size_t)std::max(node.n_bins, 0);
-        std::vector<uint32_t> cts(total * ct_words_);
+        LimbVec cts(total * ct_words_);
+        pt.lap("alloc");
         // the reference decrypts slot by slot: key and range errors surface at
-        // the first offending non-trivial slot in that order
+        // the first offending non-trivial slot in that order.  Marshalled in
+        // parallel; on a bad slot the serial scan below reports the first one.
         size_t base = 0;
+        std::vector<std::pair<const NodeHistogram *, size_t>> node_base;
         for (const NodeHistogram &node : payload.nodes) {
             const size_t cnt = 2 * node.feature_ids.size() * (size_t)std::max(node.n_bins, 0);
             if (node.scalar_cts.size() < cnt) throw Error("decrypt_histogram: scalar slot count mismatch");
-            for (size_t s = 0; s < cnt; ++s) {
-                const Ciphertext &c = node.scalar_cts[s];
-                if (c.value == 1) {
-                    std::memset(&cts[(base + s) * ct_words_], 0, ct_words_ * 4);
-                    cts[(base + s) * ct_words_] = 1;
-                    continue;
-                }
-                if (c.key_id != pub_.key_id) throw Error("decrypt: ciphertext key mismatch");
-                if (c.value < 1 || c.value >= pub_.n2 || !fits(c.value, ct_words_))
-                    throw Error("decrypt: ciphertext out of range");
-                to_words(c.value, &cts[(base + s) * ct_words_], ct_words_);
-            }
+            node_base.emplace_back(&node, base);
             base += cnt;
         }
+        std::atomic<bool> bad{false};
+        parallel_for(node_base.size(), [&](size_t lo, size_t hi) {
+            for (size_t i = lo; i < hi && !bad; ++i) {
+                const NodeHistogram &node = *node_base[i].first;
+                const size_t b0 = node_base[i].second;
+                const size_t cnt = 2 * node.feature_ids.size() * (size_t)std::max(node.n_bins, 0);
+                for (size_t s = 0; s < cnt; ++s) {
+                    const Ciphertext &c = node.scalar_cts[s];
+                    uint32_t *w = &cts[(b0 + s) * ct_words_];
+                    if (c.value == 1) {
+                        std::memset(w, 0, ct_words_ * 4);
+                        w[0] = 1;
+                        continue;
+                    }
+                    if (c.key_id != pub_.key_id || c.value < 1 || c.value >= pub_.n2 || !fits(c.value, ct_words_)) {
+                        bad = true;
+                        break;
+                    }
+                    to_words(c.value, w, ct_words_);
+                }
+            }
+        }, /*grain=*/1);
+        if (bad)
+            for (const NodeHistogram &node : payload.nodes) {
+                const size_t cnt = 2 * node.feature_ids.size() * (size_t)std::max(node.n_bins, 0);
+                for (size_t s = 0; s < cnt; ++s) {
+                    const Ciphertext &c = node.scalar_cts[s];
+                    if (c.value == 1) continue;
+                    if (c.key_id != pub_.key_id) throw Error("decrypt: ciphertext key mismatch");
+                    if (c.value < 1 || c.value >= pub_.n2 || !fits(c.value, ct_words_))
+                        throw Error("decrypt: ciphertext out of range");
+                }
+            }
+        pt.lap("marshal_in");
         std::vector<double> vals(total);
         uint64_t decs = 0;
-        if (total) decrypt_level(payload, cts, vals, &decs);
+        if (total) decrypt_level(payload, cts, vals, &decs, pt);
         counters_.decryptions += decs;
         base = 0;
         for (const NodeHistogram &node : payload.nodes) {
@@ -341,6 +473,7 @@ public:
             base += 2 * node.feature_ids.size() * (size_t)std::max(node.n_bins, 0);
             out.emplace_back(node.node_id, std::move(hist));
         }
+        pt.lap("marshal_out");
         return out;
     }
 
@@ -579,21 +712,28 @@ private:
         const size_t nchunks = (count + kChunk - 1) / kChunk;
         std::vector<uint64_t> part(nchunks, 0);
         std::atomic<bool> bad_key{false}, bad_range{false};
+        // The device copy is keyed on every ciphertext's key id, limb buffer
+        // and length, and on the full limbs of every 32nd ciphertext (hashing
+        // all 2·n·s limbs each call would cost more than the histogram
+        // itself; a new GhPayload — a new encryption — changes every
+        // ciphertext).  INTEGRATION.md states the contract.
         parallel_for(nchunks, [&](size_t lo, size_t hi) {
             for (size_t ch = lo; ch < hi; ++ch) {
                 uint64_t h = 14695981039346656037ULL;
+                auto mix = [&h](uint64_t v) {
+                    h ^= v;
+                    h *= 1099511628211ULL;
+                };
                 for (size_t i = ch * kChunk; i < std::min(count, (ch + 1) * kChunk); ++i) {
                     const Ciphertext &c = gh.cts[i];
                     if (c.key_id != pub_.key_id) bad_key = true;
                     if (!fits(c.value, ct_words_)) bad_range = true;
                     const size_t used = mpz_size(c.value.get_mpz_t());
                     const mp_limb_t *l = mpz_limbs_read(c.value.get_mpz_t());
-                    for (size_t k = 0; k < used; ++k) {
-                        h ^= l[k];
-                        h *= 1099511628211ULL;
-                    }
-                    h ^= used + 0x51;
-                    h *= 1099511628211ULL;
+                    mix(reinterpret_cast<uintptr_t>(l));
+                    mix(used + 0x51);
+                    if (i % 32 == 0)
+                        for (size_t k = 0; k < used; ++k) mix(l[k]);
                 }
                 part[ch] = h;
             }
@@ -605,11 +745,11 @@ private:
         if (gh_ && gh_hash_ == h && gh_count_ == count) return;
         if (gh_) sfxb_gh_free(gh_);
         gh_ = nullptr;
-        std::vector<uint32_t> limbs(count * ct_words_);
+        uint32_t *limbs = pin_limbs_.get<uint32_t>(count * ct_words_);
         parallel_for(count, [&](size_t lo, size_t hi) {
             for (size_t i = lo; i < hi; ++i) to_words(gh.cts[i].value, &limbs[i * ct_words_], ct_words_);
         });
-        check(sfxb_gh_upload(ctx_, limbs.data(), gh.n_samples, &gh_));
+        check(sfxb_gh_upload(ctx_, limbs, gh.n_samples, &gh_));
         gh_hash_ = h;
         gh_count_ = count;
     }
@@ -652,8 +792,8 @@ private:
         return false;
     }
 
-    void decrypt_level(const HistogramPayload &payload, std::vector<uint32_t> &cts, std::vector<double> &vals,
-                       uint64_t *decs) {
+    void decrypt_level(const HistogramPayload &payload, LimbVec &cts, std::vector<double> &vals,
+                       uint64_t *decs, PhaseTimer &pt) {
         const auto &nodes = payload.nodes;
         const size_t spn = 2 * nodes[0].feature_ids.size() * (size_t)std::max(nodes[0].n_bins, 0);
         bool uniform = spn > 0;
@@ -696,8 +836,10 @@ private:
                                         [](const DecStream &x, const DecStream &y) { return x.last_use < y.last_use; });
             }
         }
+        pt.lap("parents");
         check(sfxb_decrypt_tree(ctx_, st->tag, cts.data(), (uint32_t)nodes.size(), (uint32_t)spn, parent.data(),
                                 scale_bits_, vals.data(), decs));
+        pt.lap("gpu");
         st->cts.swap(cts);
         st->n_nodes = (uint32_t)nodes.size();
         st->spn = spn;
@@ -844,6 +986,7 @@ private:
     sfxb_ctx *ctx_ = nullptr;
     size_t n_words_ = 0, ct_words_ = 0;
     sfxb_gh *gh_ = nullptr;
+    PinnedBuf pin_r_, pin_cts_, pin_slots_, pin_limbs_; // page-locked marshalling buffers
     // previous accumulate call (sibling-subtraction parents)
     bool prev_valid_ = false;
     uint64_t prev_bins_key_ = 0;
