@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
 #include <atomic>
 #include <map>
 #include <cmath>
@@ -259,6 +260,10 @@ public:
         PhaseTimer pt("encrypt_gh");
         pt.lap("encode");
         const size_t nw = n_words_;
+        if (ok == count && has_priv_ && count >= 2 * enc_chunk()) {
+            encrypt_gh_pipelined(q, out, pt);
+            return out;
+        }
         uint32_t *r = pin_r_.get<uint32_t>(ok * nw);
         draw_blinding(r, ok);
         pt.lap("draw_r");
@@ -319,7 +324,7 @@ public:
                             break;
                         }
                 }
-            });
+            }, /*grain=*/1);
             if (bad)
                 for (const NodeRows &nd : nodes)
                     for (size_t f = 0; f < J; ++f)
@@ -658,6 +663,101 @@ private:
         gmp_randinit_mt(rng_snapshot_);
     }
 
+    // encrypt_gh for large batches with the host's sequential work off the
+    // GPU's critical path: a helper thread draws the blinding factors of chunk
+    // k+1 (the reference's MT stream, in order) while the GPU encrypts chunk k,
+    // and the ciphertexts of chunk k are marshalled into the payload while the
+    // GPU encrypts chunk k+1.  If chunk k holds an r sharing a factor with n
+    // (probability ≈ 2^-1000), the stream is rewound to the state before chunk
+    // k and the rest is redrawn with the reference's exact rejection rule.
+    // chunk size (SFXB_ENC_CHUNK overrides; the tests shrink it to exercise
+    // the pipeline on small runs)
+    static size_t enc_chunk() {
+        static const size_t c = std::getenv("SFXB_ENC_CHUNK") ? (size_t)std::max(1L, std::atol(std::getenv("SFXB_ENC_CHUNK")))
+                                                             : (size_t)262144;
+        return c;
+    }
+    void encrypt_gh_pipelined(const std::vector<int64_t> &q, GhPayload &out, PhaseTimer &pt) {
+        const size_t kEncChunk = enc_chunk();
+        const size_t count = q.size(), nw = n_words_, nch = (count + kEncChunk - 1) / kEncChunk;
+        uint32_t *r = pin_r_.get<uint32_t>(count * nw);
+        uint32_t *cts = pin_cts_.get<uint32_t>(count * ct_words_);
+        std::vector<uint8_t> flags(count, 0);
+        out.cts.resize(count);
+        struct Snap {
+            gmp_randstate_t s;
+            Snap() { gmp_randinit_mt(s); }
+            ~Snap() { gmp_randclear(s); }
+        };
+        std::vector<std::unique_ptr<Snap>> snap(nch);
+        for (auto &x : snap) x = std::make_unique<Snap>();
+        std::mutex mu;
+        std::condition_variable cv;
+        size_t drawn = 0;
+        std::atomic<bool> stop{false};
+        std::thread drawer([&] {
+            mpz_class rv;
+            for (size_t k = 0; k < nch && !stop; ++k) {
+                gmp_randclear(snap[k]->s);
+                gmp_randinit_set(snap[k]->s, rng_);
+                const size_t lo = k * kEncChunk, hi = std::min(count, lo + kEncChunk);
+                for (size_t i = lo; i < hi; ++i) {
+                    do mpz_urandomm(rv.get_mpz_t(), rng_, pub_.n.get_mpz_t());
+                    while (rv <= 1); // gcd(r, n) is tested on the device
+                    to_words(rv, r + i * nw, nw);
+                }
+                std::lock_guard<std::mutex> lk(mu);
+                drawn = k + 1;
+                cv.notify_one();
+            }
+        });
+        auto marshal = [&](size_t lo, size_t hi) {
+            parallel_for(hi - lo, [&](size_t a, size_t b) {
+                for (size_t i = lo + a; i < lo + b; ++i) {
+                    from_words(out.cts[i].value, &cts[i * ct_words_], ct_words_);
+                    out.cts[i].key_id = pub_.key_id;
+                }
+            });
+        };
+        std::thread marshaller;
+        auto join_marshal = [&] {
+            if (marshaller.joinable()) marshaller.join();
+        };
+        try {
+            for (size_t k = 0; k < nch; ++k) {
+                {
+                    std::unique_lock<std::mutex> lk(mu);
+                    cv.wait(lk, [&] { return drawn > k; });
+                }
+                const size_t lo = k * kEncChunk, n = std::min(count, lo + kEncChunk) - lo;
+                int rc = sfxb_encrypt(ctx_, &q[lo], r + lo * nw, n, cts + lo * ct_words_, flags.data() + lo);
+                if (rc == SFXB_ERR_COPRIME) {
+                    stop = true;
+                    drawer.join();
+                    gmp_randclear(rng_);
+                    gmp_randinit_set(rng_, snap[k]->s);
+                    draw_blinding(r + lo * nw, count - lo, /*exact_gcd=*/true);
+                    check(sfxb_encrypt(ctx_, &q[lo], r + lo * nw, count - lo, cts + lo * ct_words_, nullptr));
+                    join_marshal();
+                    marshal(lo, count);
+                    break;
+                }
+                check(rc);
+                join_marshal();
+                marshaller = std::thread(marshal, lo, lo + n);
+            }
+        } catch (...) {
+            stop = true;
+            if (drawer.joinable()) drawer.join();
+            join_marshal();
+            throw;
+        }
+        if (drawer.joinable()) drawer.join();
+        join_marshal();
+        pt.lap("pipelined");
+        counters_.encryptions += count;
+    }
+
     // `count` draws of HeRng::unit_below(n) (he.cpp:19-28).  With p, q the
     // gcd test is done on the device (p | r or q | r, SFXB_ERR_COPRIME) and the
     // state before the batch is kept for an exact replay; without them the
@@ -737,7 +837,7 @@ private:
                 }
                 part[ch] = h;
             }
-        });
+        }, /*grain=*/1);
         if (bad_range) throw Error("add_ciphertexts: ciphertext out of range");
         if (bad_key) throw Error("add_ciphertexts: key mismatch");
         uint64_t h = (uint64_t)count * 0x9E3779B97F4A7C15ull;

@@ -25,13 +25,14 @@ def _need(path):
         pytest.skip(f"{path} not built (built in the dev container, travels with the repo)")
 
 
-def _train_with_plugin(name, devices=None):
+def _train_with_plugin(name, devices=None, extra_env=None):
     from make_golden import TRAIN_CONFIGS
 
     ini, bits, seed = TRAIN_CONFIGS[name]
     env = dict(os.environ, LD_PRELOAD=PLUGIN, SFXB_PLUGIN_VERBOSE="1")
     if devices:
         env["SFXB_CUDA_DEVICES"] = devices
+    env.update(extra_env or {})
     out = subprocess.run([sys.executable, os.path.join(HERE, "train_driver.py"), os.path.join(HERE, "configs", ini),
                           str(bits), str(seed)], env=env, capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stderr[-2000:]
@@ -79,6 +80,22 @@ def test_training_loop_with_device_group_plugin(name):
     got, stats = _train_with_plugin(name, devices="0,0,0")
     assert stats and all("shards=3" in s for s in stats)
     assert sum(int(s.split("derived_nodes=")[1].split()[0]) for s in stats) > 0
+    for k in ("forest", "partials", "counters", "transcript_bytes", "transcript_fnv"):
+        assert got[k] == want[k], k
+
+
+@pytest.mark.parametrize("name", ["vertical_c1_1024", "vertical_threaded_3p"])
+def test_training_loop_with_pipelined_encrypt_gh(name):
+    """encrypt_gh's pipelined path (blinding factors of chunk k+1 drawn while
+    the GPU encrypts chunk k, output marshalled one chunk behind) with the
+    chunk shrunk to 997 so the small golden runs go through it: the same r
+    stream, ciphertexts and transcript bytes."""
+    _need(PLUGIN)
+    _need(os.path.join(REF, "libsfxb_refcapi.so"))
+    gpath = os.path.join(HERE, "golden", f"train_{name}.json")
+    _need(gpath)
+    want = json.load(open(gpath))
+    got, _ = _train_with_plugin(name, extra_env={"SFXB_ENC_CHUNK": "997"})
     for k in ("forest", "partials", "counters", "transcript_bytes", "transcript_fnv"):
         assert got[k] == want[k], k
 
