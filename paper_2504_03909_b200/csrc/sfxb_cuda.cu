@@ -10,6 +10,9 @@
 #include <thread>
 #include <vector>
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <exception>
 
 #include <dlfcn.h>
@@ -1222,6 +1225,27 @@ void decrypt_host(sfxb_ctx *c, const uint32_t *cts, size_t count, uint32_t scale
     if (out_plain) d2h_padded(c, out_plain, dplain.p, count, c->nw, Sn);
 }
 
+// SFXB_TRACE=1: per-phase wall times of one call (stream synchronized at each lap)
+struct TraceT {
+    cudaStream_t st;
+    bool on;
+    std::chrono::steady_clock::time_point t;
+    std::string line;
+    TraceT(cudaStream_t s_) : st(s_), on(std::getenv("SFXB_TRACE") != nullptr), t(std::chrono::steady_clock::now()) {}
+    void lap(const char *ph) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        const auto now = std::chrono::steady_clock::now();
+        char b[64];
+        std::snprintf(b, sizeof b, " %s=%.1fms", ph, std::chrono::duration<double, std::milli>(now - t).count());
+        line += b;
+        t = now;
+    }
+    ~TraceT() {
+        if (on) std::fprintf(stderr, "[sfxb-trace]%s\n", line.c_str());
+    }
+};
+
 // sfxb_decrypt_tree on slot slice [j0, j0 + jl) of every node (the whole node
 // for a single-device context).  The slice's cache entry is this level's
 // ciphertexts and plaintexts; sibling checks compare slot j of a, b and P, so
@@ -1234,6 +1258,7 @@ void decrypt_tree_impl(sfxb_ctx *c, uint64_t tag, const uint32_t *cts, uint32_t 
     const uint32_t spn = jl;
     const size_t count = (size_t)n_nodes * spn;
     const size_t Sn = 2 * (size_t)c->s, S4 = 4 * (size_t)c->s;
+    TraceT tr(c->stream);
     CtxState::DecCache &prev = c->dec_cache[tag];
     // sibling pairs (two children of one cached parent): b = second child
     std::vector<uint32_t> pairs;
@@ -1252,7 +1277,9 @@ void decrypt_tree_impl(sfxb_ctx *c, uint64_t tag, const uint32_t *cts, uint32_t 
     uint32_t *dc = (uint32_t *)grow(prev.cts[nx], count * S4 * 4 + 64);
     uint32_t *dplain = (uint32_t *)grow(prev.plain[nx], count * Sn * 4 + 64);
     IoBuf<double> dv(c->io[2], count ? count : 1);
+    tr.lap("alloc");
     if (count) h2d_cols(c, dc, cts, n_nodes, spn_total, j0, jl, 2 * c->nw, S4);
+    tr.lap("h2d");
     uint8_t *skip = nullptr;
     const size_t np = pairs.size() / 3;
     uint32_t *dpairs = nullptr;
@@ -1272,7 +1299,9 @@ void decrypt_tree_impl(sfxb_ctx *c, uint64_t tag, const uint32_t *cts, uint32_t 
             check_launch(*c);
         });
     }
+    tr.lap("verify");
     if (count) decrypt_dev(c, dc, count, scale, dv.p, dplain, decryptions, skip);
+    tr.lap("decrypt");
     if (skip) {
         dispatch_class(c->s, [&](auto sc) {
             constexpr int cs = decltype(sc)::value;
@@ -1286,6 +1315,12 @@ void decrypt_tree_impl(sfxb_ctx *c, uint64_t tag, const uint32_t *cts, uint32_t 
         CK(cudaMemcpy2DAsync(out_values + j0, (size_t)spn_total * 8, dv.p, (size_t)jl * 8, (size_t)jl * 8, n_nodes,
                              cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    tr.lap("derive_d2h");
+    if (tr.on) {
+        char b[96];
+        std::snprintf(b, sizeof b, " tag=%llu nodes=%u spn=%u pairs=%zu", (unsigned long long)tag, n_nodes, spn, np);
+        tr.line += b;
+    }
     // this level becomes the parent level of the tag
     prev.cur = nx;
     prev.n_nodes = n_nodes;

@@ -193,6 +193,7 @@ struct DecStream {
     uint32_t n_nodes = 0;
     size_t spn = 0;
     uint64_t last_use = 0;
+    uint32_t continued = 0; // levels appended after this stream's root level
 };
 constexpr size_t kStreams = 8;
 
@@ -917,6 +918,7 @@ private:
                     break;
                 }
         std::vector<int32_t> parent(nodes.size(), -1);
+        const bool continues = st != nullptr;
         if (st) {
             uint32_t cand = first;
             for (size_t i : pairs) {
@@ -927,7 +929,19 @@ private:
                 }
             }
         } else {
-            if (dec_streams_.size() < kStreams) {
+            // a level without sibling pairs is a sender's root level: the
+            // trees of every sender advance level by level together
+            // (federation.cpp:456-534), so a stream that already continued
+            // past its root belongs to a finished tree.  Recycling the least
+            // recently used of those keeps one cache tag (and its device
+            // buffers, grown to the deepest level) per sender across trees.
+            DecStream *done = nullptr;
+            if (pairs.empty())
+                for (DecStream &c : dec_streams_)
+                    if (c.continued && (!done || c.last_use < done->last_use)) done = &c;
+            if (done) {
+                st = done;
+            } else if (dec_streams_.size() < kStreams) {
                 dec_streams_.emplace_back();
                 dec_streams_.back().tag = dec_streams_.size();
                 st = &dec_streams_.back();
@@ -941,6 +955,7 @@ private:
                                 scale_bits_, vals.data(), decs));
         pt.lap("gpu");
         st->cts.swap(cts);
+        st->continued = continues ? st->continued + 1 : 0;
         st->n_nodes = (uint32_t)nodes.size();
         st->spn = spn;
         st->last_use = ++dec_clock_;
