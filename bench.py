@@ -233,6 +233,32 @@ def cpu_baseline(a, n, nw, adds_tree, threads: int = 1):
 # ------------------------------------------------------------------ reference arm
 
 
+def wire_codec(a):
+    """The processor buffers one tree puts on the reference's Bus (SURVEY
+    §8f rank 1; Bus::send = serialize_buffer + parse_buffer,
+    federation.cpp:96-102): the gh_pairs_enc buffer (2 x rows ciphertexts)
+    and the deepest level's scalar histogram (2^(depth-1) nodes), serialized
+    and parsed by the reference's implementation and by the parallel codec
+    LD_PRELOADed with the GPU adapter (host/wire_parallel.cpp); bytes and
+    payloads compared (tools/wire_bench.cpp)."""
+    import subprocess
+
+    exe = os.path.join(ROOT, "oracle", "_ref", "wire_bench")
+    plugin = os.path.join(ROOT, "paper_2504_03909_b200", "lib", "libsfxb_cuda_plugin.so")
+    if not (os.path.exists(exe) and os.path.exists(plugin)):
+        return {"unavailable": "oracle/_ref/wire_bench or the plugin library not built"}
+    bits = {"k512_c0ffee": 512, "k1024_7": 1024, "k2048_7": 2048, "k3072_7": 3072}.get(a.key, 2048)
+    env = dict(os.environ, LD_PRELOAD=plugin)
+    try:
+        out = subprocess.run([exe, str(a.rows), str(1 << (a.depth - 1)), str(a.feats), str(a.bins), str(bits), "1",
+                              "0"], env=env, capture_output=True, text=True, timeout=600)
+        res = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": f"wire_bench failed: {e}"}
+    res["host_threads"] = os.cpu_count()
+    return res
+
+
 def plugin_e2e(a):
     """The reference-facing end to end: tools/plugin_bench.cpp drives the
     reference's EncryptionPlugin calls of one tree (encrypt_gh, accumulate_rows
@@ -711,6 +737,7 @@ def run_ours(a):
     }
     if world == 1 and not a.no_plugin_e2e:
         line["plugin_e2e"] = plugin_e2e(a)
+        line["wire"] = wire_codec(a)
     if world == 1 and not a.no_cpu:
         try:
             line["cpu_baseline"] = cpu_baseline(a, n, nw, adds_tree_ref, threads=1)
