@@ -478,12 +478,42 @@ void decrypt_dev(sfxb_ctx *c, const uint32_t *d_cts, size_t count, uint32_t scal
             pa.idx = a.idx;
             pa.count = n_items;
             pa.status = a.status;
-            auto k = dev::k_p2_pow<cs, C::TP, kWindow, 1>;
-            constexpr int NI = dev::kBlock / C::TP;
-            int grid = occupancy_grid(*c, k, 2 * (size_t)n_items, NI, 2);
-            pa.scratch = (uint32_t *)grow(c->scratch_table, 2 * (size_t)grid * NI * ((size_t)(2 * cs) << kWindow) * 4);
-            k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(pa);
-            check_launch(*c);
+            auto launch = [&](auto tp) {
+                constexpr int TPv = decltype(tp)::value;
+                auto k = dev::k_p2_pow<cs, TPv, kWindow, 1>;
+                constexpr int NI = dev::kBlock / TPv;
+                int grid = occupancy_grid(*c, k, 2 * (size_t)n_items, NI, 2);
+                pa.scratch =
+                    (uint32_t *)grow(c->scratch_table, 2 * (size_t)grid * NI * ((size_t)(2 * cs) << kWindow) * 4);
+                k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(pa);
+                check_launch(*c);
+            };
+            // Small batches (a tree's first levels: a few thousand slots)
+            // leave most SMs idle at one lane per instance, and the call
+            // takes one exponentiation's latency.  Spread each instance
+            // over 4 (or 2) lanes when that still fits in one wave: ~3x
+            // lower latency, same results (SFXB_DEC_SMALL_TPI=0 disables).
+            int tpi = C::TP;
+            if constexpr (C::TP == 1 && (cs == 16 || cs == 32)) {
+                const char *e = std::getenv("SFXB_DEC_SMALL_TPI");
+                if (!e || std::atoi(e) != 0) {
+                    const size_t inst = 2 * (size_t)n_items;
+                    auto lanes_cap = [&](auto k) {
+                        int per_sm = 0;
+                        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, dev::kBlock, 0));
+                        return (size_t)std::max(per_sm, 1) * c->sms * dev::kBlock;
+                    };
+                    if (4 * inst <= lanes_cap(dev::k_p2_pow<cs, 4, kWindow, 1>)) tpi = 4;
+                    else if (2 * inst <= lanes_cap(dev::k_p2_pow<cs, 2, kWindow, 1>)) tpi = 2;
+                }
+            }
+            if constexpr (C::TP == 1 && (cs == 16 || cs == 32)) {
+                if (tpi == 4) launch(std::integral_constant<int, 4>{});
+                else if (tpi == 2) launch(std::integral_constant<int, 2>{});
+                else launch(std::integral_constant<int, C::TP>{});
+            } else {
+                launch(std::integral_constant<int, C::TP>{});
+            }
         } else {
             auto k = dev::k_dec_step<cs, C::TD, kWindow>;
             constexpr int NI = dev::kBlock / C::TD;

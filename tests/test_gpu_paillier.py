@@ -255,3 +255,33 @@ def test_primes_short_of_their_size_class_use_the_mod_p2_kernels(pbits):
     _, decs, plain = ctx.decrypt(ints_to_words(cts, ctx.ct_words), want_plain=True)
     assert decs == count
     assert words_to_ints(plain) == [((pow(c, lam, n2) - 1) // n) * mu % n for c in cts]
+
+
+@pytest.mark.parametrize("kname", ["k1024_7", "k2048_7"])
+def test_small_batch_decrypt_lanes_equal_one_lane(oracle, kname, monkeypatch):
+    """Small decrypt batches spread each exponentiation over 4 or 2 lanes
+    (one wave, lower latency); the one-lane kernel (SFXB_DEC_SMALL_TPI=0)
+    gives the same plaintexts and values, and both match the oracle."""
+    n, p, q = key(kname)
+    ok = OracleKey(oracle, n, p, q)
+    ctx = _lib.Context(n, p, q)
+    rng = random.Random(kname + "lanes")
+    n2 = n * n
+    base_m = [rng.randrange(n) for _ in range(48)]
+    base_c = [(1 + m * n) * pow(rng.randrange(2, n), n, n2) % n2 for m in base_m]
+    for count in (3, 700, 5000, 14000, 30000):
+        # homomorphic sums of random pairs: valid ciphertexts of known plaintexts
+        pairs = [(rng.randrange(48), rng.randrange(48)) for _ in range(count)]
+        ms = [(base_m[a] + base_m[b]) % n for a, b in pairs]
+        cts = [base_c[a] * base_c[b] % n2 for a, b in pairs]
+        words = ints_to_words(cts, ctx.ct_words)
+        monkeypatch.delenv("SFXB_DEC_SMALL_TPI", raising=False)
+        v1, d1, p1 = ctx.decrypt(words, want_plain=True)
+        monkeypatch.setenv("SFXB_DEC_SMALL_TPI", "0")
+        v0, d0, p0 = ctx.decrypt(words, want_plain=True)
+        assert d1 == d0 == count
+        assert np.array_equal(p1, p0)
+        assert np.array_equal(v1.view(np.uint64), v0.view(np.uint64))
+        assert words_to_ints(p1) == ms
+        for i in (0, count // 2, count - 1):
+            assert ok.decrypt(cts[i]) == ms[i]
