@@ -261,6 +261,7 @@ public:
         }
         check(rc);
         pt.lap("gpu");
+        const hostpar::TopPadScope pad(count * ct_words_ * 4);
         out.cts.resize(count);
         parallel_for(count, [&](size_t lo, size_t hi) {
             for (size_t i = lo; i < hi; ++i) {
@@ -367,6 +368,7 @@ public:
             nh.scalar_cts.resize(per_node);
         }
         pt.lap("out_alloc");
+        const hostpar::TopPadScope pad(N * per_node * ct_words_ * 4);
         parallel_for(N * per_node, [&](size_t lo, size_t hi) {
             for (size_t s = lo; s < hi; ++s) {
                 Ciphertext &c = out.nodes[s / per_node].scalar_cts[s % per_node];
@@ -660,6 +662,7 @@ private:
         uint32_t *r = pin_r_.get<uint32_t>(count * nw);
         uint32_t *cts = pin_cts_.get<uint32_t>(count * ct_words_);
         std::vector<uint8_t> flags(count, 0);
+        const hostpar::TopPadScope pad(count * ct_words_ * 4);
         out.cts.resize(count);
         struct Snap {
             gmp_randstate_t s;

@@ -243,6 +243,7 @@ ProcessorBuffer parse_buffer(const std::string &bytes) {
     const bool gh = kind == static_cast<uint8_t>(BufferKind::gh_pairs_enc);
     const bool hist = enc_hist_kind(static_cast<BufferKind>(kind));
     if (!gh && !hist) return ref_parse(bytes);
+    const hostpar::TopPadScope pad(size); // the limb arrays total ≈ the wire bytes
     ProcessorBuffer buf;
     buf.version = 1;
     buf.kind = static_cast<BufferKind>(kind);
