@@ -29,6 +29,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "parallel.hpp"
@@ -270,12 +271,17 @@ ProcessorBuffer parse_buffer(const std::string &bytes) {
     if (gh) {
         const uint64_t n = 2ull * buf.header[0];
         if (n < min_cts()) return ref_parse(bytes);
-        off.reserve(n);
-        if (!walk(n) || pos != size) return ref_parse(bytes);
+        if (n > (size - pos) / 4) return ref_parse(bytes); // cannot hold n length prefixes
+        // the payload's n empty ciphertexts are constructed on a second thread
+        // while this one walks the length chain (both serial, ≈ equal cost)
         GhPayload p;
         p.encrypted = true;
         p.n_samples = buf.header[0];
-        p.cts.resize(n);
+        std::thread alloc([&] { p.cts.resize(n); });
+        off.reserve(n);
+        const bool ok = walk(n) && pos == size;
+        alloc.join();
+        if (!ok) return ref_parse(bytes);
         hostpar::parallel_for(n, [&](size_t lo, size_t hi) {
             for (size_t k = lo; k < hi; ++k) get_ct_at(p.cts[k].value, d + off[k] + 4, rd32(d + off[k]));
         }, 1024);
