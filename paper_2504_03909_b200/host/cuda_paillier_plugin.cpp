@@ -315,8 +315,8 @@ public:
         pt.lap("validate");
         ensure_gh(gh);
         pt.lap("ensure_gh");
-        std::vector<uint16_t> flat(J * gh.n_samples);
-        for (size_t f = 0; f < J; ++f) std::memcpy(&flat[f * gh.n_samples], bins[f].data(), gh.n_samples * 2);
+        uint16_t *flat = pin_bins_.get<uint16_t>(J * gh.n_samples);
+        const uint64_t bins_key = stage_bins(bins, J, gh.n_samples, feature_ids, n_bins, flat);
         std::vector<uint32_t> offs(N + 1, 0), rows;
         for (size_t i = 0; i < N; ++i) offs[i + 1] = offs[i] + (uint32_t)nodes[i].rows.size();
         rows.reserve(offs[N]);
@@ -327,7 +327,6 @@ public:
         // (federation.cpp:591-592).  A parent is accepted only when the merged
         // rows of the pair equal its rows exactly and the features, bins and
         // gradients are those of the previous call.
-        const uint64_t bins_key = bins_fingerprint(flat, feature_ids, n_bins);
         std::vector<int32_t> parent(N, -1);
         if (prev_valid_ && prev_bins_key_ == bins_key && prev_gh_ == gh_) {
             size_t p = 0;
@@ -349,7 +348,7 @@ public:
         pt.lap("alloc_slots");
         uint64_t adds = 0;
         if (N && J && K)
-            check(sfxb_accumulate_tree_gh(ctx_, gh_, flat.data(), (uint32_t)J, offs.data(), (uint32_t)N, rows.data(),
+            check(sfxb_accumulate_tree_gh(ctx_, gh_, flat, (uint32_t)J, offs.data(), (uint32_t)N, rows.data(),
                                           (uint32_t)K, parent.data(), slots, &adds));
         pt.lap("gpu");
         prev_valid_ = N && J && K;
@@ -773,13 +772,36 @@ private:
         return i == a.size() && j == b.size();
     }
 
-    static uint64_t bins_fingerprint(const std::vector<uint16_t> &flat, const std::vector<int> &fids, int n_bins) {
-        uint64_t h = 14695981039346656037ULL ^ (uint64_t)n_bins;
-        for (int f : fids) h = (h ^ (uint32_t)f) * 1099511628211ULL;
-        const uint64_t *w = reinterpret_cast<const uint64_t *>(flat.data());
-        const size_t n64 = flat.size() / 4;
-        for (size_t i = 0; i < n64; ++i) h = (h ^ w[i]) * 1099511628211ULL;
-        for (size_t i = n64 * 4; i < flat.size(); ++i) h = (h ^ flat[i]) * 1099511628211ULL;
+    // The call's bin columns (J × n u16, column-major) copied into the
+    // page-locked staging buffer on all host threads, and their content key:
+    // FNV-1a over the per-block FNV-1a digests (blocks of kBinsBlock rows of
+    // one feature, in order), each computed on its block's copy.
+    static constexpr size_t kBinsBlock = size_t(1) << 18;
+    static uint64_t stage_bins(const std::vector<std::vector<uint16_t>> &bins, size_t J, size_t n,
+                               const std::vector<int> &fids, int n_bins, uint16_t *flat) {
+        constexpr uint64_t kBasis = 14695981039346656037ULL, kPrime = 1099511628211ULL;
+        const size_t per_f = (n + kBinsBlock - 1) / kBinsBlock, nb = J * per_f;
+        std::vector<uint64_t> dig(nb);
+        parallel_for(nb, [&](size_t lo, size_t hi) {
+            for (size_t b = lo; b < hi; ++b) {
+                const size_t f = b / per_f, i0 = (b % per_f) * kBinsBlock, cnt = std::min(kBinsBlock, n - i0);
+                const uint16_t *src = bins[f].data() + i0;
+                std::memcpy(flat + f * n + i0, src, cnt * 2);
+                uint64_t h = kBasis;
+                size_t k = 0;
+                for (; k + 4 <= cnt; k += 4) {
+                    uint64_t w;
+                    std::memcpy(&w, src + k, 8);
+                    h = (h ^ w) * kPrime;
+                }
+                for (; k < cnt; ++k) h = (h ^ src[k]) * kPrime;
+                dig[b] = h;
+            }
+        }, /*grain=*/2);
+        uint64_t h = kBasis ^ (uint64_t)n_bins;
+        for (int f : fids) h = (h ^ (uint32_t)f) * kPrime;
+        h = (h ^ (uint64_t)n) * kPrime;
+        for (uint64_t d : dig) h = (h ^ d) * kPrime;
         return h;
     }
 
@@ -1080,7 +1102,7 @@ private:
     sfxb_ctx *ctx_ = nullptr;
     size_t n_words_ = 0, ct_words_ = 0;
     sfxb_gh *gh_ = nullptr;
-    PinnedBuf pin_r_, pin_cts_, pin_slots_, pin_limbs_; // page-locked marshalling buffers
+    PinnedBuf pin_r_, pin_cts_, pin_slots_, pin_limbs_, pin_bins_; // page-locked marshalling buffers
     // previous accumulate call (sibling-subtraction parents)
     bool prev_valid_ = false;
     uint64_t prev_bins_key_ = 0;
