@@ -84,18 +84,20 @@ def test_training_loop_with_device_group_plugin(name):
         assert got[k] == want[k], k
 
 
+@pytest.mark.parametrize("chunk", ["997", "61"])
 @pytest.mark.parametrize("name", ["vertical_c1_1024", "vertical_threaded_3p"])
-def test_training_loop_with_pipelined_encrypt_gh(name):
+def test_training_loop_with_pipelined_encrypt_gh(name, chunk):
     """encrypt_gh's pipelined path (blinding factors of chunk k+1 drawn while
     the GPU encrypts chunk k, output marshalled one chunk behind) with the
-    chunk shrunk to 997 so the small golden runs go through it: the same r
-    stream, ciphertexts and transcript bytes."""
+    chunk shrunk to 997 or 61 so the small golden runs go through it (61: many
+    chunks, a ragged last one): the same r stream, ciphertexts and transcript
+    bytes."""
     _need(PLUGIN)
     _need(os.path.join(REF, "libsfxb_refcapi.so"))
     gpath = os.path.join(HERE, "golden", f"train_{name}.json")
     _need(gpath)
     want = json.load(open(gpath))
-    got, _ = _train_with_plugin(name, extra_env={"SFXB_ENC_CHUNK": "997"})
+    got, _ = _train_with_plugin(name, extra_env={"SFXB_ENC_CHUNK": chunk})
     for k in ("forest", "partials", "counters", "transcript_bytes", "transcript_fnv"):
         assert got[k] == want[k], k
 
