@@ -26,8 +26,8 @@ def _need(path):
         pytest.skip(f"{path} not built (__graft_entry__.build() in the dev container)")
 
 
-def _bench(lib, args, min_cts):
-    env = dict(os.environ, LD_PRELOAD=lib, SFXB_WIRE_MIN_CTS=str(min_cts), SFXB_WIRE_VERBOSE="1")
+def _bench(lib, args, min_cts, extra_env=None):
+    env = dict(os.environ, LD_PRELOAD=lib, SFXB_WIRE_MIN_CTS=str(min_cts), SFXB_WIRE_VERBOSE="1", **(extra_env or {}))
     out = subprocess.run([BENCH, *map(str, args)], env=env, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, (out.stdout[-2000:], out.stderr[-2000:])
     return json.loads(out.stdout.strip().splitlines()[-1]), out.stderr
@@ -46,6 +46,21 @@ def test_codec_matches_reference(bits, seed):
         a, b = r["malformed_same_error"].split("/")
         assert a == b
     assert "serialize fast=2 " in err and "parse fast=2 " in err
+
+
+@pytest.mark.parametrize("top_pad", ["1", "0"])
+def test_codec_large_buffer_heap_step(top_pad):
+    """a gh buffer above 64 MB (140,000 ciphertexts at 2048-bit n) parses with
+    glibc's heap-growth step raised (host/parallel.hpp TopPadScope) and without
+    it (SFXB_HOST_TOP_PAD=0): bytes, payloads and errors equal the reference's"""
+    _need(WIRE)
+    _need(BENCH)
+    res, err = _bench(WIRE, [70000, 1, 2, 16, 2048, 5], 0, {"SFXB_HOST_TOP_PAD": top_pad})
+    r = res["gh_pairs_enc"]
+    assert res["ok"] and r["bytes"] >= 64 << 20
+    assert r["bytes_identical"] and r["parse_identical"]
+    a, b = r["malformed_same_error"].split("/")
+    assert a == b
 
 
 def test_codec_in_the_plugin_library_and_threshold():
