@@ -14,14 +14,16 @@
 //     |value| big-endian without leading zero bytes (count 0 for value 0);
 //     here: count from the limb header, bytes by byte-swapped limb stores;
 //   * WireReader::ct (:71-79) imports count bytes big-endian, key_id 0;
-//     here: a sequential walk over the length prefixes finds every entry's
-//     offset (and every truncation, which the reference then reports), then
-//     the imports run on all host threads into limbs directly.
+//     here: a walk over the length prefixes finds every entry's offset (and
+//     every truncation, which the reference then reports) — for gh buffers on
+//     all host threads (walk_entries) — then the imports run on all host
+//     threads into limbs directly.
 // SFXB_WIRE_MIN_CTS (default 4096): buffers with fewer ciphertexts use the
 // reference path unchanged.  SFXB_WIRE_VERBOSE=1: call counts at exit.
 #include <gmp.h>
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
@@ -200,6 +202,87 @@ std::string head_bytes(const ProcessorBuffer &b) {
 
 bool enc_hist_kind(BufferKind k) { return k == BufferKind::histogram_enc || k == BufferKind::agg_result_enc; }
 
+// Offsets of the length-prefixed entries of d[start, size) in wire order, as
+// the serial walk from `start` finds them; true iff that walk reads exactly n
+// valid entries ending at `size` (the serial condition).  The buffer is cut
+// into one byte range per host thread; each thread past the first finds a
+// plausible entry start in its range (kSync consecutive lengths ≤ kSyncLen
+// that stay inside the buffer) and walks from there to the end of its range.
+// The true chain is then followed range by range: where it lands on a
+// position a thread recorded, that thread's list is the true continuation
+// (the walk from a position is deterministic); otherwise the range is walked
+// serially.  A wrong sync therefore costs time, never a different result.
+bool walk_entries(const char *d, size_t size, size_t start, uint64_t n, std::vector<size_t> &off) {
+    // SFXB_WIRE_WALK_TEST=1 (tests): accept the first in-buffer length as an
+    // entry start, so most ranges sync wrongly and take the serial fallback
+    static const bool loose = std::getenv("SFXB_WIRE_WALK_TEST") != nullptr;
+    const size_t kSync = loose ? 1 : 16, kSyncLen = loose ? SIZE_MAX : 4096;
+    constexpr size_t kMinRange = size_t(1) << 20;
+    const unsigned T = std::min<size_t>(hostpar::host_threads(), (size - start) / kMinRange);
+    // one entry at p: its end, or 0 when the length runs past the buffer
+    auto next = [&](size_t p) -> size_t {
+        if (size - p < 4) return 0;
+        const uint32_t len = rd32(d + p);
+        return len > size - p - 4 ? 0 : p + 4 + (size_t)len;
+    };
+    auto serial = [&](size_t p, size_t stop, std::vector<size_t> &out) -> size_t { // 0 = invalid entry
+        while (p < stop) {
+            const size_t q = next(p);
+            if (!q) return 0;
+            __builtin_prefetch(d + q + 16 * (q - p));
+            out.push_back(p);
+            p = q;
+        }
+        return p;
+    };
+    off.clear();
+    if (T < 2) {
+        off.reserve(n);
+        return serial(start, size, off) == size && off.size() == n;
+    }
+    std::vector<size_t> lo(T + 1);
+    for (unsigned t = 0; t <= T; ++t) lo[t] = start + (size - start) / T * t;
+    lo[T] = size;
+    std::vector<std::vector<size_t>> lists(T);
+    std::vector<size_t> ends(T, 0);
+    hostpar::parallel_for(T, [&](size_t a, size_t b) {
+        for (size_t t = a; t < b; ++t) {
+            size_t s = lo[t];
+            if (t > 0) {
+                for (; s < lo[t + 1]; ++s) {
+                    size_t p = s, k = 0;
+                    for (; k < kSync && p < size; ++k) {
+                        if (size - p < 4 || rd32(d + p) > kSyncLen) break;
+                        const size_t q = next(p);
+                        if (!q) break;
+                        p = q;
+                    }
+                    if (k == kSync || (p == size && k > 0)) break;
+                }
+                if (s >= lo[t + 1]) continue; // no plausible start: walked serially below
+            }
+            lists[t].reserve((lo[t + 1] - s) / 256 + 16);
+            ends[t] = serial(s, lo[t + 1], lists[t]);
+        }
+    }, 1);
+    off.reserve(n);
+    size_t p = start;
+    for (unsigned t = 0; t < T && p < size; ++t) {
+        if (p >= lo[t + 1]) continue;
+        const auto &L = lists[t];
+        auto it = std::lower_bound(L.begin(), L.end(), p);
+        if (it != L.end() && *it == p) {
+            if (!ends[t]) return false;
+            off.insert(off.end(), it, L.end());
+            p = ends[t];
+        } else if (!(p = serial(p, lo[t + 1], off))) {
+            return false;
+        }
+        if (off.size() > n) return false;
+    }
+    return p == size && off.size() == n;
+}
+
 } // namespace
 
 // secure_processor.cpp:119-215 (fast path: gh_pairs_enc, scalar encrypted histograms)
@@ -273,13 +356,12 @@ ProcessorBuffer parse_buffer(const std::string &bytes) {
         if (n < min_cts()) return ref_parse(bytes);
         if (n > (size - pos) / 4) return ref_parse(bytes); // cannot hold n length prefixes
         // the payload's n empty ciphertexts are constructed on a second thread
-        // while this one walks the length chain (both serial, ≈ equal cost)
+        // while the length chain is walked (walk_entries, all host threads)
         GhPayload p;
         p.encrypted = true;
         p.n_samples = buf.header[0];
         std::thread alloc([&] { p.cts.resize(n); });
-        off.reserve(n);
-        const bool ok = walk(n) && pos == size;
+        const bool ok = walk_entries(d, size, pos, n, off);
         alloc.join();
         if (!ok) return ref_parse(bytes);
         hostpar::parallel_for(n, [&](size_t lo, size_t hi) {

@@ -48,14 +48,17 @@ def test_codec_matches_reference(bits, seed):
     assert "serialize fast=2 " in err and "parse fast=2 " in err
 
 
-@pytest.mark.parametrize("top_pad", ["1", "0"])
-def test_codec_large_buffer_heap_step(top_pad):
+@pytest.mark.parametrize("top_pad,walk_test", [("1", None), ("0", None), ("1", "1")])
+def test_codec_large_buffer_heap_step(top_pad, walk_test):
     """a gh buffer above 64 MB (140,000 ciphertexts at 2048-bit n) parses with
     glibc's heap-growth step raised (host/parallel.hpp TopPadScope) and without
-    it (SFXB_HOST_TOP_PAD=0): bytes, payloads and errors equal the reference's"""
+    it (SFXB_HOST_TOP_PAD=0), its length chain walked on all threads (and with
+    SFXB_WIRE_WALK_TEST: wrong range syncs, serial fallback): bytes, payloads
+    and errors equal the reference's"""
     _need(WIRE)
     _need(BENCH)
-    res, err = _bench(WIRE, [70000, 1, 2, 16, 2048, 5], 0, {"SFXB_HOST_TOP_PAD": top_pad})
+    env = {"SFXB_HOST_TOP_PAD": top_pad, **({"SFXB_WIRE_WALK_TEST": walk_test} if walk_test else {})}
+    res, err = _bench(WIRE, [70000, 1, 2, 16, 2048, 5], 0, env)
     r = res["gh_pairs_enc"]
     assert res["ok"] and r["bytes"] >= 64 << 20
     assert r["bytes_identical"] and r["parse_identical"]
