@@ -56,7 +56,7 @@ class TopPadScope {
             const char *e = std::getenv("SFXB_HOST_TOP_PAD");
             return !(e && std::atoi(e) == 0);
         }();
-        on_ = allowed && bytes_to_allocate >= (size_t(64) << 20);
+        on_ = allowed && bytes_to_allocate >= (size_t(16) << 20);
         if (on_) mallopt(M_TOP_PAD, 128 << 20);
     }
     ~TopPadScope() {
