@@ -175,11 +175,24 @@ uint64_t pow_mmuls(const Big &e, int w) {
     for (size_t i = 1; i < d.size(); ++i) m += d[i] != 0;
     return m;
 }
+// Grow-only device buffer.  The old allocation is released first (the new
+// one is usually larger than what is left); the size is recorded only once
+// the new allocation exists, so a failed cudaMalloc (OOM) leaves an empty
+// buffer that the next call allocates again, never a null pointer that
+// claims capacity.
 void *grow(Buf &b, size_t bytes) {
     if (b.bytes < bytes) {
-        if (b.p) CK(cudaFree(b.p));
+        void *old = b.p;
         b.p = nullptr;
-        CK(cudaMalloc(&b.p, bytes));
+        b.bytes = 0;
+        if (old) CK(cudaFree(old));
+        void *p = nullptr;
+        const cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) {
+            (void)cudaGetLastError(); // an allocation failure is not sticky: clear it
+            throw CudaError(std::string("cudaMalloc of ") + std::to_string(bytes) + " bytes: " + cudaGetErrorString(e));
+        }
+        b.p = p;
         b.bytes = bytes;
     }
     return b.p;

@@ -94,6 +94,10 @@ public:
         }
         return static_cast<T *>(p_);
     }
+    template <typename T>
+    const T *peek() const {
+        return static_cast<const T *>(p_);
+    }
 
 private:
     void *p_ = nullptr;
@@ -275,6 +279,26 @@ public:
     }
 
     // ---- accumulate_rows (secure_processor.cpp:587-620)
+    //
+    // The histogram products run on the GPU over the device copy of gh.  Inputs
+    // the reference treats specially keep its semantics exactly:
+    //   * ciphertexts equal to 1 are skipped (fold_into, :724-732) whatever
+    //     their key id;
+    //   * "irregular" ciphertexts — a foreign key id, or a value outside
+    //     [0, n²) (negative, ≥ n², wider than the ciphertext) — are not
+    //     ciphertexts of this key.  They go to the device as the identity and
+    //     every slot they land in is folded again on the host with the
+    //     reference's rules (assign into an empty slot keeping the value and
+    //     key id as they are; a·b tdiv n² otherwise; add_ciphertexts' key
+    //     check, he.cpp:117-121).  A foreign key therefore fails only where
+    //     the reference's loop multiplies it, with the reference's counter at
+    //     that point (replay_folds);
+    //   * a bad bin index fails at the reference's loop position, with the
+    //     additions it counted before it.
+    // Known deviation (not replayed): if a running slot product other than the
+    // last becomes exactly 1 (c·c⁻¹ inside one slot — never the case for
+    // honest encryptions), the reference's next fold is an uncounted assign;
+    // the GPU counts Σ max(k − 1, 0).  Residues are identical either way.
     HistogramPayload accumulate_rows(const GhPayload &gh, const std::vector<std::vector<std::uint16_t>> &bins,
                                      const std::vector<int> &feature_ids, const std::vector<NodeRows> &nodes,
                                      int n_bins) override {
@@ -288,8 +312,12 @@ public:
         out.layout = HistLayout::enc_scalar;
         const size_t J = feature_ids.size(), K = (size_t)std::max(n_bins, 0), N = nodes.size();
         PhaseTimer pt("accumulate_rows");
+        // header-only pass over gh: key ids, signs, sizes, the value 1
+        const GhScan scan = scan_gh(gh);
+        pt.lap("scan");
         // bins are checked per visited row, as the reference loop does: a
-        // parallel scan, and on a hit the reference's serial order picks the message
+        // parallel scan, and on a hit the reference's loop is replayed for its
+        // exception and counter
         {
             std::atomic<bool> bad{false};
             parallel_for(N * J, [&](size_t lo, size_t hi) {
@@ -303,17 +331,11 @@ public:
                         }
                 }
             }, /*grain=*/1);
-            if (bad)
-                for (const NodeRows &nd : nodes)
-                    for (size_t f = 0; f < J; ++f)
-                        for (std::uint32_t row : nd.rows) {
-                            if (row >= gh.n_samples) throw Error("row index out of range in accumulate");
-                            if (bins[f][row] >= static_cast<std::uint16_t>(n_bins))
-                                throw Error("bin index out of range in accumulate");
-                        }
+            if (bad) fail_with_replay(gh, scan, bins, J, nodes, n_bins);
         }
         pt.lap("validate");
-        ensure_gh(gh);
+        const bool candidate = gh_ && gh_scan_key_ == scan.key && gh_count_ == gh.cts.size();
+        if (!candidate) upload_gh(gh, scan.key);
         pt.lap("ensure_gh");
         uint16_t *flat = pin_bins_.get<uint16_t>(J * gh.n_samples);
         const uint64_t bins_key = stage_bins(bins, J, gh.n_samples, feature_ids, n_bins, flat);
@@ -322,41 +344,61 @@ public:
         rows.reserve(offs[N]);
         for (const NodeRows &nd : nodes) rows.insert(rows.end(), nd.rows.begin(), nd.rows.end());
         pt.lap("flatten");
-        // Sibling subtraction: the reference's next frontier lists the two
-        // children of each split node consecutively, in parent order
-        // (federation.cpp:591-592).  A parent is accepted only when the merged
-        // rows of the pair equal its rows exactly and the features, bins and
-        // gradients are those of the previous call.
-        std::vector<int32_t> parent(N, -1);
-        if (prev_valid_ && prev_bins_key_ == bins_key && prev_gh_ == gh_) {
-            size_t p = 0;
-            for (size_t i = 0; i + 1 < N && p < prev_rows_.size(); ) {
-                const auto &a = nodes[i].rows, &b = nodes[i + 1].rows;
-                size_t q = p;
-                while (q < prev_rows_.size() && prev_rows_[q].size() != a.size() + b.size()) ++q;
-                if (q < prev_rows_.size() && merged_equals(a, b, prev_rows_[q])) {
-                    parent[i] = parent[i + 1] = (int32_t)q;
-                    p = q + 1;
-                    i += 2;
-                } else {
-                    ++i;
+        uint32_t *slots = pin_slots_.get<uint32_t>(N * J * K * 2 * ct_words_);
+        uint64_t adds = 0;
+        auto run_gpu = [&](bool allow_parents) -> int {
+            // Sibling subtraction: the reference's next frontier lists the two
+            // children of each split node consecutively, in parent order
+            // (federation.cpp:591-592).  A parent is accepted only when the
+            // merged rows of the pair equal its rows exactly and the features,
+            // bins and gradients are those of the previous call.
+            std::vector<int32_t> parent(N, -1);
+            if (allow_parents && prev_valid_ && prev_bins_key_ == bins_key && prev_gh_ == gh_) {
+                size_t p = 0;
+                for (size_t i = 0; i + 1 < N && p < prev_rows_.size();) {
+                    const auto &ra = nodes[i].rows, &rb = nodes[i + 1].rows;
+                    size_t q = p;
+                    while (q < prev_rows_.size() && prev_rows_[q].size() != ra.size() + rb.size()) ++q;
+                    if (q < prev_rows_.size() && merged_equals(ra, rb, prev_rows_[q])) {
+                        parent[i] = parent[i + 1] = (int32_t)q;
+                        p = q + 1;
+                        i += 2;
+                    } else {
+                        ++i;
+                    }
                 }
             }
+            adds = 0;
+            if (!(N && J && K)) return SFXB_OK;
+            return sfxb_accumulate_tree_gh(ctx_, gh_, flat, (uint32_t)J, offs.data(), (uint32_t)N, rows.data(),
+                                           (uint32_t)K, parent.data(), slots, &adds);
+        };
+        int rc;
+        if (candidate) {
+            // Same limb buffers as the resident copy: the GPU starts on it while
+            // the host compares every limb (and every irregular value) with what
+            // was uploaded.  A difference discards the result and reruns on a
+            // fresh upload — the device copy is never trusted on a sampled key.
+            bool same = false;
+            std::thread verify([&] { same = verify_gh(gh); });
+            rc = run_gpu(true);
+            verify.join();
+            pt.lap("gpu+verify");
+            if (!same) {
+                upload_gh(gh, scan.key);
+                rc = run_gpu(false);
+                pt.lap("reupload+gpu");
+            }
+        } else {
+            rc = run_gpu(true);
+            pt.lap("gpu");
         }
-        pt.lap("parents");
-        uint32_t *slots = pin_slots_.get<uint32_t>(N * J * K * 2 * ct_words_);
-        pt.lap("alloc_slots");
-        uint64_t adds = 0;
-        if (N && J && K)
-            check(sfxb_accumulate_tree_gh(ctx_, gh_, flat, (uint32_t)J, offs.data(), (uint32_t)N, rows.data(),
-                                          (uint32_t)K, parent.data(), slots, &adds));
-        pt.lap("gpu");
+        check(rc);
         prev_valid_ = N && J && K;
         prev_bins_key_ = bins_key;
         prev_gh_ = gh_;
         prev_rows_.resize(N);
         for (size_t i = 0; i < N; ++i) prev_rows_[i] = nodes[i].rows;
-        counters_.ciphertext_additions += adds;
         const size_t per_node = 2 * J * K;
         out.nodes.resize(N);
         for (size_t i = 0; i < N; ++i) {
@@ -367,15 +409,20 @@ public:
             nh.scalar_cts.resize(per_node);
         }
         pt.lap("out_alloc");
-        const hostpar::TopPadScope pad(N * per_node * ct_words_ * 4);
-        parallel_for(N * per_node, [&](size_t lo, size_t hi) {
-            for (size_t s = lo; s < hi; ++s) {
-                Ciphertext &c = out.nodes[s / per_node].scalar_cts[s % per_node];
-                from_words(c.value, &slots[s * ct_words_], ct_words_);
-                c.key_id = pub_.key_id;
-            }
-        });
+        {
+            const hostpar::TopPadScope pad(N * per_node * ct_words_ * 4);
+            parallel_for(N * per_node, [&](size_t lo, size_t hi) {
+                for (size_t s = lo; s < hi; ++s) {
+                    Ciphertext &c = out.nodes[s / per_node].scalar_cts[s % per_node];
+                    from_words(c.value, &slots[s * ct_words_], ct_words_);
+                    c.key_id = pub_.key_id;
+                }
+            });
+        }
         pt.lap("out_marshal");
+        // slots holding irregular ciphertexts: the reference's folds on the host
+        if (!irr_.empty()) adds = refold_irregular(gh, scan, bins, J, nodes, n_bins, out, adds);
+        counters_.ciphertext_additions += adds;
         return out;
     }
 
@@ -426,21 +473,20 @@ public:
                 }
             }
         }, /*grain=*/1);
-        if (bad)
-            for (const NodeHistogram &node : payload.nodes) {
-                const size_t cnt = 2 * node.feature_ids.size() * (size_t)std::max(node.n_bins, 0);
-                for (size_t s = 0; s < cnt; ++s) {
-                    const Ciphertext &c = node.scalar_cts[s];
-                    if (c.value == 1) continue;
-                    if (c.key_id != pub_.key_id) throw Error("decrypt: ciphertext key mismatch");
-                    if (c.value < 1 || c.value >= pub_.n2 || !fits(c.value, ct_words_))
-                        throw Error("decrypt: ciphertext out of range");
-                }
-            }
+        if (bad) fail_decrypt(payload, /*coprime_error=*/false);
         pt.lap("marshal_in");
         std::vector<double> vals(total);
         uint64_t decs = 0;
-        if (total) decrypt_level(payload, cts, vals, &decs, pt);
+        if (total) {
+            try {
+                decrypt_level(payload, cts, vals, &decs, pt);
+            } catch (const Error &) {
+                // the GPU found a slot sharing a factor with n
+                if (std::string(sfxb_last_error(ctx_)).find("not coprime") != std::string::npos)
+                    fail_decrypt(payload, /*coprime_error=*/true);
+                throw;
+            }
+        }
         counters_.decryptions += decs;
         base = 0;
         for (const NodeHistogram &node : payload.nodes) {
@@ -805,61 +851,279 @@ private:
         return h;
     }
 
-    // Device-resident gh keyed on the ciphertext contents: one parallel
-    // read-only pass hashes the mpz limbs (and applies the checks); only on a
-    // miss are the limbs marshalled and uploaded (sfxb_gh_upload).
-    void ensure_gh(const GhPayload &gh) {
+    // ---------------------------------------------------------------- gh residency
+    //
+    // Per ciphertext of a GhPayload: trivial (value 1: skipped by fold_into),
+    // regular (this key, 0 ≤ value < n²: multiplied on the GPU) or irregular
+    // (anything else: uploaded as the identity, its slots refolded on the host).
+    enum : uint8_t { kRegular = 0, kTrivial = 1, kForeign = 2, kOffRange = 3 };
+
+    struct GhScan {
+        uint64_t key = 0;          // buffer addresses, sizes and key ids: the residency pre-filter
+        std::vector<uint8_t> cls;  // per ciphertext, header-level class (kOffRange needs the limbs)
+    };
+
+    // header-only pass: key id, sign, size, and the value 1
+    GhScan scan_gh(const GhPayload &gh) const {
         const size_t count = gh.cts.size();
-        constexpr size_t kChunk = 4096;
+        constexpr size_t kChunk = 8192;
         const size_t nchunks = (count + kChunk - 1) / kChunk;
+        GhScan sc;
+        sc.cls.resize(count);
         std::vector<uint64_t> part(nchunks, 0);
-        std::atomic<bool> bad_key{false}, bad_range{false};
-        // The device copy is keyed on every ciphertext's key id, limb buffer
-        // and length, and on the full limbs of every 32nd ciphertext (hashing
-        // all 2·n·s limbs each call would cost more than the histogram
-        // itself; a new GhPayload — a new encryption — changes every
-        // ciphertext).  INTEGRATION.md states the contract.
         parallel_for(nchunks, [&](size_t lo, size_t hi) {
             for (size_t ch = lo; ch < hi; ++ch) {
                 uint64_t h = 14695981039346656037ULL;
-                auto mix = [&h](uint64_t v) {
-                    h ^= v;
-                    h *= 1099511628211ULL;
-                };
                 for (size_t i = ch * kChunk; i < std::min(count, (ch + 1) * kChunk); ++i) {
                     const Ciphertext &c = gh.cts[i];
-                    if (c.key_id != pub_.key_id) bad_key = true;
-                    if (!fits(c.value, ct_words_)) bad_range = true;
-                    const size_t used = mpz_size(c.value.get_mpz_t());
-                    const mp_limb_t *l = mpz_limbs_read(c.value.get_mpz_t());
-                    mix(reinterpret_cast<uintptr_t>(l));
-                    mix(used + 0x51);
-                    if (i % 32 == 0)
-                        for (size_t k = 0; k < used; ++k) mix(l[k]);
+                    const mpz_srcptr z = c.value.get_mpz_t();
+                    uint8_t k = kRegular;
+                    if (z->_mp_size == 1 && mpz_limbs_read(z)[0] == 1) k = kTrivial;
+                    else if (c.key_id != pub_.key_id) k = kForeign;
+                    else if (z->_mp_size < 0 || (size_t)z->_mp_size * 2 > ct_words_) k = kOffRange;
+                    sc.cls[i] = k;
+                    h = (h ^ reinterpret_cast<uintptr_t>(mpz_limbs_read(z))) * 1099511628211ULL;
+                    h = (h ^ ((uint64_t)(uint32_t)z->_mp_size << 8 ^ k)) * 1099511628211ULL;
+                    h = (h ^ c.key_id) * 1099511628211ULL;
                 }
                 part[ch] = h;
             }
         }, /*grain=*/1);
-        if (bad_range) throw Error("add_ciphertexts: ciphertext out of range");
-        if (bad_key) throw Error("add_ciphertexts: key mismatch");
-        uint64_t h = (uint64_t)count * 0x9E3779B97F4A7C15ull;
-        for (uint64_t x : part) h = (h ^ x) * 1099511628211ULL;
-        if (gh_ && gh_hash_ == h && gh_count_ == count) return;
+        sc.key = (uint64_t)count * 0x9E3779B97F4A7C15ull;
+        for (uint64_t x : part) sc.key = (sc.key ^ x) * 1099511628211ULL;
+        return sc;
+    }
+
+    // full class of ciphertext c (reads the top limbs for the n² bound)
+    uint8_t classify(const Ciphertext &c) const {
+        const mpz_srcptr z = c.value.get_mpz_t();
+        if (z->_mp_size == 1 && mpz_limbs_read(z)[0] == 1) return kTrivial;
+        if (c.key_id != pub_.key_id) return kForeign;
+        if (z->_mp_size < 0 || (size_t)z->_mp_size * 2 > ct_words_) return kOffRange;
+        if (mpz_cmp(z, pub_.n2.get_mpz_t()) >= 0) return kOffRange;
+        return kRegular;
+    }
+
+    // marshal every ciphertext into the page-locked staging buffer (regular:
+    // its limbs; trivial and irregular: the identity), record the irregular
+    // ones, upload (sfxb_gh_upload)
+    void upload_gh(const GhPayload &gh, uint64_t scan_key) {
         if (gh_) sfxb_gh_free(gh_);
         gh_ = nullptr;
-        uint32_t *limbs = pin_limbs_.get<uint32_t>(count * ct_words_);
-        parallel_for(count, [&](size_t lo, size_t hi) {
-            for (size_t i = lo; i < hi; ++i) to_words(gh.cts[i].value, &limbs[i * ct_words_], ct_words_);
-        });
+        prev_valid_ = false; // a new resident copy: no cached parents (the handle address may repeat)
+        const size_t count = gh.cts.size(), cw = ct_words_;
+        uint32_t *limbs = pin_limbs_.get<uint32_t>(count * cw);
+        constexpr size_t kChunk = 8192;
+        const size_t nchunks = (count + kChunk - 1) / kChunk;
+        std::vector<std::vector<uint32_t>> irr(nchunks);
+        parallel_for(nchunks, [&](size_t lo, size_t hi) {
+            for (size_t ch = lo; ch < hi; ++ch)
+                for (size_t i = ch * kChunk; i < std::min(count, (ch + 1) * kChunk); ++i) {
+                    uint32_t *w = &limbs[i * cw];
+                    const uint8_t k = classify(gh.cts[i]);
+                    if (k == kRegular) {
+                        to_words(gh.cts[i].value, w, cw);
+                    } else {
+                        std::memset(w, 0, cw * 4);
+                        w[0] = 1;
+                        if (k != kTrivial) irr[ch].push_back((uint32_t)i);
+                    }
+                }
+        }, /*grain=*/1);
+        irr_.clear();
+        for (const auto &v : irr)
+            for (uint32_t i : v) irr_.push_back(IrrCt{i, gh.cts[i]});
         check(sfxb_gh_upload(ctx_, limbs, gh.n_samples, &gh_));
-        gh_hash_ = h;
+        gh_scan_key_ = scan_key;
         gh_count_ = count;
+    }
+
+    // every limb of gh equals the resident copy (staging buffer) and the
+    // irregular ciphertexts are the recorded ones
+    bool verify_gh(const GhPayload &gh) const {
+        const size_t count = gh.cts.size(), cw = ct_words_;
+        const uint32_t *limbs = pin_limbs_.peek<uint32_t>();
+        constexpr size_t kChunk = 8192;
+        const size_t nchunks = (count + kChunk - 1) / kChunk;
+        std::atomic<bool> same{true};
+        std::vector<std::vector<uint32_t>> irr(nchunks);
+        parallel_for(nchunks, [&](size_t lo, size_t hi) {
+            for (size_t ch = lo; ch < hi && same; ++ch)
+                for (size_t i = ch * kChunk; i < std::min(count, (ch + 1) * kChunk); ++i) {
+                    const uint32_t *w = &limbs[i * cw];
+                    const uint8_t k = classify(gh.cts[i]);
+                    bool ok;
+                    if (k == kRegular) {
+                        const mpz_srcptr z = gh.cts[i].value.get_mpz_t();
+                        const size_t used = (size_t)z->_mp_size, bytes = used * 8;
+                        ok = std::memcmp(w, mpz_limbs_read(z), bytes) == 0;
+                        for (size_t j = bytes / 4; ok && j < cw; ++j) ok = w[j] == 0;
+                    } else {
+                        ok = w[0] == 1;
+                        for (size_t j = 1; ok && j < cw; ++j) ok = w[j] == 0;
+                        if (k != kTrivial) irr[ch].push_back((uint32_t)i);
+                    }
+                    if (!ok) {
+                        same = false;
+                        break;
+                    }
+                }
+        }, /*grain=*/1);
+        if (!same) return false;
+        size_t j = 0;
+        for (const auto &v : irr)
+            for (uint32_t i : v) {
+                if (j >= irr_.size() || irr_[j].index != i || irr_[j].ct.key_id != gh.cts[i].key_id ||
+                    mpz_cmp(irr_[j].ct.value.get_mpz_t(), gh.cts[i].value.get_mpz_t()) != 0)
+                    return false;
+                ++j;
+            }
+        return j == irr_.size();
+    }
+
+    // The reference's loop (secure_processor.cpp:603-618 with fold_into
+    // :724-732 and add_ciphertexts' key check, he.cpp:117-121) replayed on
+    // ciphertext classes only: the first exception it raises and the
+    // additions it counted before.  Used on the error paths (bad bin, key
+    // mismatch), where the call fails exactly where the reference's would.
+    [[noreturn]] void fail_with_replay(const GhPayload &gh, const GhScan &scan,
+                                       const std::vector<std::vector<std::uint16_t>> &bins, size_t J,
+                                       const std::vector<NodeRows> &nodes, int n_bins) {
+        const size_t K = (size_t)std::max(n_bins, 0);
+        std::vector<uint8_t> st; // per slot: 0 empty (trivial), 1 this key, 2 foreign
+        uint64_t adds = 0;
+        auto fail = [&](const char *msg) {
+            counters_.ciphertext_additions += adds;
+            throw Error(msg);
+        };
+        for (const NodeRows &nd : nodes) {
+            st.assign(2 * J * K, 0);
+            for (size_t f = 0; f < J; ++f)
+                for (std::uint32_t row : nd.rows) {
+                    if (row >= gh.n_samples) fail("row index out of range in accumulate");
+                    const std::uint16_t b = bins[f][row];
+                    if (b >= static_cast<std::uint16_t>(n_bins)) fail("bin index out of range in accumulate");
+                    for (size_t w = 0; w < 2; ++w) {
+                        const uint8_t k = scan.cls[2 * (size_t)row + w];
+                        if (k == kTrivial) continue;
+                        uint8_t &s = st[2 * (f * K + b) + w];
+                        if (s == 0) {
+                            s = k == kForeign ? 2 : 1;
+                            continue;
+                        }
+                        if (s == 2 || k == kForeign) fail("add_ciphertexts: key mismatch");
+                        ++adds;
+                        s = 1;
+                    }
+                }
+        }
+        // not reached on the paths that call this (they saw a failure)
+        counters_.ciphertext_additions += adds;
+        throw Error("accumulate: internal replay found no failure");
+    }
+
+    // Slots holding irregular ciphertexts, folded again on the host with the
+    // reference's rules over all of their entries in row order; returns the
+    // call's reference addition count (the GPU counted those slots without
+    // their irregular entries).
+    uint64_t refold_irregular(const GhPayload &gh, const GhScan &scan,
+                              const std::vector<std::vector<std::uint16_t>> &bins, size_t J,
+                              const std::vector<NodeRows> &nodes, int n_bins, HistogramPayload &out, uint64_t adds) {
+        const size_t K = (size_t)std::max(n_bins, 0);
+        std::vector<uint8_t> is_irr_row(gh.n_samples, 0);
+        for (const IrrCt &x : irr_) is_irr_row[x.index / 2] = 1;
+        for (size_t i = 0; i < nodes.size(); ++i) {
+            const NodeRows &nd = nodes[i];
+            // (feature, slot) pairs of this node touched by an irregular entry
+            std::vector<std::pair<size_t, size_t>> hit;
+            for (std::uint32_t row : nd.rows)
+                if (is_irr_row[row])
+                    for (size_t f = 0; f < J; ++f)
+                        for (size_t w = 0; w < 2; ++w) {
+                            const size_t ci = 2 * (size_t)row + w;
+                            const uint8_t k = scan.cls[ci] == kRegular ? classify(gh.cts[ci]) : scan.cls[ci];
+                            if (k == kForeign || k == kOffRange) hit.emplace_back(f, 2 * (f * K + bins[f][row]) + w);
+                        }
+            std::sort(hit.begin(), hit.end());
+            hit.erase(std::unique(hit.begin(), hit.end()), hit.end());
+            for (const auto &[f, slot] : hit) {
+                const size_t b = (slot / 2) % K, w = slot & 1;
+                Ciphertext acc{mpz_class(1), pub_.key_id}; // trivial_zero (he.cpp:123)
+                uint64_t ref_adds = 0, gpu_entries = 0;
+                for (std::uint32_t row : nd.rows) {
+                    if (bins[f][row] != b) continue;
+                    const Ciphertext &c = gh.cts[2 * (size_t)row + w];
+                    if (c.value == 1) continue;                      // fold_into: rhs trivial
+                    if (classify(c) == kRegular) ++gpu_entries;
+                    if (acc.value == 1) {                            // lhs trivial: assign
+                        acc = c;
+                        continue;
+                    }
+                    if (acc.key_id != c.key_id || acc.key_id != pub_.key_id)
+                        fail_with_replay(gh, scan, bins, J, nodes, n_bins);
+                    mpz_mul(acc.value.get_mpz_t(), acc.value.get_mpz_t(), c.value.get_mpz_t());
+                    mpz_tdiv_r(acc.value.get_mpz_t(), acc.value.get_mpz_t(), pub_.n2.get_mpz_t());
+                    acc.key_id = pub_.key_id;
+                    ++ref_adds;
+                }
+                adds = adds - (gpu_entries ? gpu_entries - 1 : 0) + ref_adds;
+                out.nodes[i].scalar_cts[slot] = std::move(acc);
+            }
+        }
+        return adds;
     }
 
     void check(int rc) {
         if (rc == SFXB_OK) return;
         std::string msg = sfxb_last_error(ctx_);
         if (rc == SFXB_ERR_AUTH) throw AuthorizationError(msg);
+        throw Error(msg);
+    }
+
+    // Error path of decrypt_histogram: the reference decrypts slot by slot
+    // (secure_processor.cpp:687-696, decrypt_slot :734-738, decrypt he.cpp:
+    // 105-115) and stops at the first non-trivial slot with a foreign key,
+    // a value outside [1, n²) or a common factor with n — in that order per
+    // slot — having counted every non-trivial slot up to and including it.
+    // Locate that slot (gcd on all host threads, only here) and fail there.
+    [[noreturn]] void fail_decrypt(const HistogramPayload &payload, bool coprime_error) {
+        std::vector<const Ciphertext *> nt; // non-trivial slots in the reference's order
+        for (const NodeHistogram &node : payload.nodes) {
+            const size_t cnt = 2 * node.feature_ids.size() * (size_t)std::max(node.n_bins, 0);
+            for (size_t s = 0; s < cnt && s < node.scalar_cts.size(); ++s)
+                if (!(node.scalar_cts[s].value == 1)) nt.push_back(&node.scalar_cts[s]);
+        }
+        auto header_err = [&](const Ciphertext &c) -> const char * {
+            if (c.key_id != pub_.key_id) return "decrypt: ciphertext key mismatch";
+            if (c.value < 1 || c.value >= pub_.n2) return "decrypt: ciphertext out of range";
+            return nullptr;
+        };
+        size_t first = nt.size();
+        const char *msg = nullptr;
+        if (!coprime_error)
+            for (size_t k = 0; k < nt.size(); ++k)
+                if ((msg = header_err(*nt[k]))) {
+                    first = k;
+                    break;
+                }
+        // an earlier slot not coprime to n fails first
+        std::vector<uint8_t> nc(first, 0);
+        parallel_for(first, [&](size_t lo, size_t hi) {
+            mpz_class g;
+            for (size_t k = lo; k < hi; ++k) {
+                if (header_err(*nt[k])) continue;
+                mpz_gcd(g.get_mpz_t(), nt[k]->value.get_mpz_t(), pub_.n.get_mpz_t());
+                nc[k] = g != 1;
+            }
+        }, /*grain=*/256);
+        for (size_t k = 0; k < first; ++k)
+            if (nc[k]) {
+                first = k;
+                msg = "decrypt: ciphertext not coprime to modulus";
+                break;
+            }
+        if (!msg) throw Error("decrypt_histogram: GPU reported an error no slot reproduces");
+        counters_.decryptions += first + 1;
         throw Error(msg);
     }
 
@@ -1108,8 +1372,14 @@ private:
     uint64_t prev_bins_key_ = 0;
     const sfxb_gh *prev_gh_ = nullptr;
     std::vector<std::vector<std::uint32_t>> prev_rows_;
-    uint64_t gh_hash_ = 0;
+    // resident gh: pre-filter key, count, and its irregular ciphertexts
+    struct IrrCt {
+        uint32_t index;
+        Ciphertext ct;
+    };
+    uint64_t gh_scan_key_ = 0;
     size_t gh_count_ = 0;
+    std::vector<IrrCt> irr_;
     std::vector<DecStream> dec_streams_;
     uint64_t dec_clock_ = 0;
 };

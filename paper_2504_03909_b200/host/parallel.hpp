@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -46,7 +47,16 @@ void parallel_for(size_t n, F &&f, size_t grain = 4096) {
 // all host threads otherwise serialises on the heap-growth mprotect calls
 // (parse of 2M ciphertexts: import 0.69 -> 0.28 s on 8 threads).  Left alone
 // when the user tuned M_TOP_PAD (MALLOC_TOP_PAD_ or GLIBC_TUNABLES) or sets
-// SFXB_HOST_TOP_PAD=0; restores glibc's default on exit.
+// SFXB_HOST_TOP_PAD=0.
+//
+// Scopes nest and overlap across threads (parties call their plugins
+// concurrently in the reference's threaded mode, federation.cpp:509-516): a
+// process-wide count under a mutex raises the step on the first entry and
+// restores glibc's default (128 KiB) on the last exit only, so one party's
+// exit never shrinks the step under another party still writing.  Side
+// effect (glibc): any mallopt(M_TOP_PAD) call also disables the dynamic mmap
+// threshold for the rest of the process; an application
+// that cannot accept that sets SFXB_HOST_TOP_PAD=0.
 class TopPadScope {
   public:
     explicit TopPadScope(size_t bytes_to_allocate) {
@@ -57,15 +67,27 @@ class TopPadScope {
             return !(e && std::atoi(e) == 0);
         }();
         on_ = allowed && bytes_to_allocate >= (size_t(16) << 20);
-        if (on_) mallopt(M_TOP_PAD, 128 << 20);
+        if (!on_) return;
+        std::lock_guard<std::mutex> lk(state().mu);
+        if (state().depth++ == 0) mallopt(M_TOP_PAD, 128 << 20);
     }
     ~TopPadScope() {
-        if (on_) mallopt(M_TOP_PAD, 128 * 1024);
+        if (!on_) return;
+        std::lock_guard<std::mutex> lk(state().mu);
+        if (--state().depth == 0) mallopt(M_TOP_PAD, 128 * 1024);
     }
     TopPadScope(const TopPadScope &) = delete;
     TopPadScope &operator=(const TopPadScope &) = delete;
 
   private:
+    struct Shared {
+        std::mutex mu;
+        int depth = 0;
+    };
+    static Shared &state() {
+        static Shared s;
+        return s;
+    }
     bool on_ = false;
 };
 
