@@ -15,8 +15,9 @@
 //   * accumulate_rows / decrypt_histogram keep the reference's validation
 //     order, messages, slot layout, trivial-zero handling and counter laws;
 //   * the packed (horizontal) vector path (encrypt_histogram, add_histograms,
-//     packed decrypt) uses the reference's packing layer (pack_plain /
-//     unpack_plain, he.hpp) on the host and the GPU for every encryption,
+//     packed decrypt) packs and unpacks on the host exactly as the reference's
+//     packing layer does (PackedLayout::validate / pack_plain / unpack_plain,
+//     he.cpp:145-213, restated below) and uses the GPU for every encryption,
 //     ciphertext product and decryption, with the reference's r order, checks,
 //     error order and vector-granularity counters.
 #include <gmp.h>
@@ -141,6 +142,87 @@ void from_words(mpz_class &z, const uint32_t *w, size_t words) {
 }
 
 // the reference implementation, for the out-of-scope packed path
+
+// ------------------------------------------------------------ packed vectors
+//
+// The horizontal path's plaintext packing (he.cpp:145-213), restated so the
+// adapter needs nothing from the reference library but its headers: k =
+// ⌊(modulus_bits − 1) / slot_bits⌋ slots per plaintext, slot s of a plaintext
+// holds q + bias at bit s·slot_bits with q = llround(x·2^scale) and bias =
+// 2^(slot_bits − guard_bits − 1); unpacking subtracts bias·addend_count per
+// slot and decodes with mpz_get_d truncation.  Checks, messages and their
+// order are the reference's.
+namespace packing {
+
+unsigned slots(const PackedLayout &l) { // PackedLayout::slots_per_ciphertext, he.cpp:145-148
+    if (l.slot_bits == 0) throw ConfigError("slot_bits", "must be positive");
+    return (l.modulus_bits - 1) / l.slot_bits;
+}
+
+mpz_class bias(const PackedLayout &l) { // PackedLayout::slot_bias, he.cpp:150-154
+    mpz_class b;
+    mpz_setbit(b.get_mpz_t(), l.slot_bits - l.guard_bits - 1);
+    return b;
+}
+
+void validate(const PackedLayout &l) { // PackedLayout::validate, he.cpp:156-164
+    if (l.slot_bits < 8) throw ConfigError("slot_bits", "must be >= 8");
+    if (l.guard_bits + 2 > l.slot_bits) throw ConfigError("guard_bits", "must leave at least one magnitude bit per slot");
+    if (l.scale_bits == 0 || l.scale_bits > 52) throw ConfigError("scale_bits", "must be in [1, 52]");
+    if (slots(l) < 1) throw ConfigError("slot_bits", "too large for the modulus (zero slots per ciphertext)");
+}
+
+// pack_plain, he.cpp:166-193
+std::vector<mpz_class> pack(const PackedLayout &l, const std::vector<double> &values) {
+    validate(l);
+    const size_t k = slots(l);
+    const mpz_class b = bias(l);
+    const double limit = std::ldexp(1.0, static_cast<int>(62 - l.scale_bits));
+    std::vector<mpz_class> out;
+    out.reserve((values.size() + k - 1) / k);
+    mpz_class q, t;
+    for (size_t i = 0; i < values.size(); i += k) {
+        mpz_class m = 0;
+        for (size_t s = 0; s < std::min(k, values.size() - i); ++s) {
+            const double x = values[i + s];
+            if (!std::isfinite(x)) throw Error("pack_vector: value must be finite");
+            if (std::abs(x) >= limit) throw Error("pack_vector: value too large for the fixed-point grid");
+            mpz_set_si(q.get_mpz_t(), static_cast<long>(std::llround(std::ldexp(x, static_cast<int>(l.scale_bits)))));
+            if (mpz_cmpabs(q.get_mpz_t(), b.get_mpz_t()) >= 0)
+                throw Error("pack_vector: slot overflow at index " + std::to_string(i + s));
+            mpz_add(t.get_mpz_t(), q.get_mpz_t(), b.get_mpz_t());
+            mpz_mul_2exp(t.get_mpz_t(), t.get_mpz_t(), static_cast<unsigned long>(s) * l.slot_bits);
+            mpz_add(m.get_mpz_t(), m.get_mpz_t(), t.get_mpz_t());
+        }
+        out.push_back(std::move(m));
+    }
+    return out;
+}
+
+// unpack_plain, he.cpp:195-213
+std::vector<double> unpack(const PackedLayout &l, const std::vector<mpz_class> &packed, size_t logical_length,
+                           std::uint32_t addend_count) {
+    validate(l);
+    if (addend_count < 1) throw Error("unpack_vector: addend count must be >= 1");
+    const size_t k = slots(l);
+    if (packed.size() != (logical_length + k - 1) / k)
+        throw Error("unpack_vector: ciphertext count does not match logical length");
+    mpz_class offset = bias(l);
+    mpz_mul_ui(offset.get_mpz_t(), offset.get_mpz_t(), addend_count);
+    std::vector<double> out;
+    out.reserve(logical_length);
+    mpz_class slot;
+    for (size_t i = 0; i < logical_length; ++i) {
+        // (m >> s·slot_bits) & (2^slot_bits − 1), floor shift as mpz_class's >>
+        mpz_fdiv_q_2exp(slot.get_mpz_t(), packed[i / k].get_mpz_t(), static_cast<unsigned long>(i % k) * l.slot_bits);
+        mpz_fdiv_r_2exp(slot.get_mpz_t(), slot.get_mpz_t(), l.slot_bits);
+        mpz_sub(slot.get_mpz_t(), slot.get_mpz_t(), offset.get_mpz_t());
+        out.push_back(std::ldexp(mpz_get_d(slot.get_mpz_t()), -static_cast<int>(l.scale_bits)));
+    }
+    return out;
+}
+
+} // namespace packing
 
 // ------------------------------------------------------------ the plugin
 
@@ -507,11 +589,11 @@ public:
     }
 
     // ---- packed (horizontal) path: encrypt_histogram (secure_processor.cpp:622-645)
-    // = pack_plain (the reference's packing layer, he.cpp:166-193) + one GPU
+    // = pack_plain (packing layer below, he.cpp:166-193) + one GPU
     // batch of encrypt_with_r over every packed plaintext, r drawn in the
     // reference's order (node: G vector, then H vector).
     HistogramPayload encrypt_histogram(const std::vector<std::pair<std::uint32_t, Histogram>> &node_hists) override {
-        layout_.validate();
+        packing::validate(layout_);
         HistogramPayload out;
         out.layout = HistLayout::enc_packed;
         std::vector<mpz_class> plains;
@@ -529,7 +611,7 @@ public:
                         hs.push_back(b.h);
                     }
                 for (const std::vector<double> *v : {&gs, &hs}) {
-                    std::vector<mpz_class> p = pack_plain(layout_, *v);
+                    std::vector<mpz_class> p = packing::pack(layout_, *v);
                     for (mpz_class &m : p) plains.push_back(std::move(m));
                     first.push_back(plains.size());
                     lengths.push_back(static_cast<std::uint32_t>(v->size()));
@@ -1334,7 +1416,7 @@ private:
                 std::vector<mpz_class> m(v.cts.size());
                 for (size_t k = 0; k < m.size(); ++k) from_words(m[k], &plain[(idx + k) * n_words_], n_words_);
                 const PackedLayout layout{pub_.modulus_bits, v.slot_bits, v.guard_bits, v.scale_bits};
-                gh[w] = unpack_plain(layout, m, v.logical_length, v.addend_count);
+                gh[w] = packing::unpack(layout, m, v.logical_length, v.addend_count);
                 idx += v.cts.size();
             }
             counters_.decryptions += 2; // vector granularity

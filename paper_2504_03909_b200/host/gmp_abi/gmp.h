@@ -1,14 +1,12 @@
-/* TEST INFRASTRUCTURE ONLY (oracle/).
- *
- * Minimal C declarations for the subset of GMP 6.3.0 that the reference
- * (the .cpp files under /root/reference/proj/src, SURVEY.md §8c "Shim surface") and
- * our oracle restatement call.  The image ships the GMP *runtime*
+/* Minimal C declarations for the subset of GMP 6.3.0 that the host code
+ * calls: the C++ adapter and wire codec (paper_2504_03909_b200/host), the
+ * device library's root inversion (dlopen of the same runtime), and — as test
+ * infrastructure — the reference sources compiled into oracle/_ref and the
+ * oracle restatement (SURVEY.md §8c "Shim surface").  The image ships the GMP *runtime*
  * (`/usr/lib/x86_64-linux-gnu/libgmp.so.10`, GMP 6.3.0) but not its headers,
  * so this file restates the public ABI: struct layouts (`__mpz_struct`,
  * `__gmp_randstate_struct`) and the exported `__gmpz_*` / `__gmp_*` entry
  * points, with the usual `mpz_*` -> `__gmpz_*` name macros.
- *
- * Nothing on the product path includes this header.
  */
 #ifndef SFXB_ORACLE_GMP_SHIM_H
 #define SFXB_ORACLE_GMP_SHIM_H
@@ -80,6 +78,8 @@ typedef __gmp_randstate_struct gmp_randstate_t[1];
 #define mpz_cmp __gmpz_cmp
 #define mpz_cmp_si __gmpz_cmp_si
 #define mpz_cmp_ui __gmpz_cmp_ui
+#define mpz_cmpabs __gmpz_cmpabs
+#define mpz_fdiv_r_2exp __gmpz_fdiv_r_2exp
 #define mpz_abs __gmpz_abs
 #define mpz_neg __gmpz_neg
 #define mpz_get_d __gmpz_get_d
@@ -138,6 +138,8 @@ void mpz_and(mpz_ptr, mpz_srcptr, mpz_srcptr);
 int mpz_cmp(mpz_srcptr, mpz_srcptr);
 int mpz_cmp_si(mpz_srcptr, long);
 int mpz_cmp_ui(mpz_srcptr, unsigned long);
+int mpz_cmpabs(mpz_srcptr, mpz_srcptr);
+void mpz_fdiv_r_2exp(mpz_ptr, mpz_srcptr, mp_bitcnt_t);
 void mpz_abs(mpz_ptr, mpz_srcptr);
 void mpz_neg(mpz_ptr, mpz_srcptr);
 double mpz_get_d(mpz_srcptr);

@@ -1,5 +1,3 @@
-// TEST INFRASTRUCTURE ONLY (oracle/).
-//
 // Minimal `mpz_class` / `gmp_randclass` restatement of the gmpxx C++ wrapper
 // (GMP 6.3.0 semantics) covering exactly what the reference uses (SURVEY.md
 // §8c "Shim surface"): construction from builtin integers, + - * / % (the
@@ -9,8 +7,9 @@
 // get_z_range (mpz_urandomb / mpz_urandomm).  No expression templates: each
 // operator materialises its result, which is value-identical.
 //
-// Used to compile the read-only reference sources into oracle/_ref/ and the
-// C++ adapter; nothing on the device path includes it.
+// Used to compile the C++ adapter against the reference's headers (which
+// include <gmpxx.h>) and, as test infrastructure, the read-only reference
+// sources into oracle/_ref/.
 #pragma once
 #include <gmp.h>
 

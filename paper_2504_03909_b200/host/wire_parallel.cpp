@@ -1,25 +1,33 @@
-// Parallel wire codec for the ciphertext-carrying processor buffers (SURVEY
-// §8f rank 1): sfxb::serialize_buffer / sfxb::parse_buffer
-// (secure_processor.hpp:171-172, secure_processor.cpp:119-375) for the
-// gh_pairs_enc and scalar histogram_enc / agg_result_enc kinds, the ≈1 GB
-// per tree that Bus::send (federation.cpp:96-102) serializes and re-parses.
+// Wire codec for the ciphertext-carrying processor buffers (SURVEY §8f rank
+// 1): sfxb::serialize_buffer / sfxb::parse_buffer (secure_processor.hpp:
+// 171-172, secure_processor.cpp:119-375) for the gh_pairs_enc,
+// histogram_enc and agg_result_enc kinds (scalar and packed layouts) — the
+// ≈1 GB per tree that Bus::send (federation.cpp:96-102) serializes and
+// re-parses — written here, for every buffer size and every malformed input.
 //
 // Interposed the same way as make_paillier_plugin: this library is loaded
 // ahead of the reference library, whose call sites reach both functions
-// through the PLT.  Every other kind, the packed layout, small buffers and
-// every malformed input go to the reference's own implementation
-// (dlsym(RTLD_NEXT)), so error types, messages and offsets are the
-// reference's.  Output bytes and parsed payloads are identical:
-//   * put_ct (secure_processor.cpp:39-45) writes u32 LE byte count, then
-//     |value| big-endian without leading zero bytes (count 0 for value 0);
-//     here: count from the limb header, bytes by byte-swapped limb stores;
-//   * WireReader::ct (:71-79) imports count bytes big-endian, key_id 0;
-//     here: a walk over the length prefixes finds every entry's offset (and
-//     every truncation, which the reference then reports) — for gh buffers on
-//     all host threads (walk_entries) — then the imports run on all host
-//     threads into limbs directly.
-// SFXB_WIRE_MIN_CTS (default 4096): buffers with fewer ciphertexts use the
-// reference path unchanged.  SFXB_WIRE_VERBOSE=1: call counts at exit.
+// through the PLT.  The other kinds (plain gradients / histograms, cut_sync,
+// tree_sync: no ciphertexts, outside the hot path) are handed to the
+// reference's definitions (dlsym(RTLD_NEXT)) after the common header checks.
+//
+// Format (the reference's, reproduced byte for byte):
+//   header  "SFXB", u8 version 1, u8 kind, 3 × u32 LE
+//   put_ct  (:39-45) u32 LE byte count, then |value| big-endian without
+//           leading zero bytes (count 0 for value 0); here the count comes
+//           from the limb header and the bytes from byte-swapped limb stores,
+//           ciphertexts written on all host threads into one pre-sized buffer;
+//   reading (:52-90, :221-375) WireReader: a missing byte is
+//           ParseError("truncated buffer", size); a length running past the
+//           end is ParseError("truncated ciphertext entry", offset after the
+//           length); a surplus is ParseError("trailing bytes in buffer", pos);
+//           parsed ciphertexts carry key id 0.  Here the length chain is
+//           walked first (for gh buffers on all host threads, walk_entries),
+//           the payload's vectors are reserved exactly where the reference
+//           reserves them, and the limb imports run on all host threads.
+//           Errors come from the same walk, so type, message and offset are
+//           the reference's.
+// SFXB_WIRE_VERBOSE=1: how many buffers each path handled, at exit.
 #include <gmp.h>
 #include <dlfcn.h>
 
@@ -42,11 +50,11 @@ namespace sfxb {
 namespace {
 
 struct Stats {
-    std::atomic<unsigned long long> ser_fast{0}, ser_ref{0}, parse_fast{0}, parse_ref{0};
+    std::atomic<unsigned long long> ser_native{0}, ser_ref{0}, parse_native{0}, parse_ref{0};
     ~Stats() {
         if (std::getenv("SFXB_WIRE_VERBOSE"))
-            std::fprintf(stderr, "[sfxb-wire] serialize fast=%llu ref=%llu parse fast=%llu ref=%llu\n",
-                         ser_fast.load(), ser_ref.load(), parse_fast.load(), parse_ref.load());
+            std::fprintf(stderr, "[sfxb-wire] serialize native=%llu ref=%llu parse native=%llu ref=%llu\n",
+                         ser_native.load(), ser_ref.load(), parse_native.load(), parse_ref.load());
     }
 } stats;
 
@@ -60,6 +68,7 @@ Fn next_symbol(const char *mangled) {
     return reinterpret_cast<Fn>(p);
 }
 
+// kinds without ciphertexts (outside the hot path): the reference's codec
 std::string ref_serialize(const ProcessorBuffer &b) {
     ++stats.ser_ref;
     static SerializeFn f = next_symbol<SerializeFn>("_ZN4sfxb16serialize_bufferB5cxx11ERKNS_15ProcessorBufferE");
@@ -72,15 +81,6 @@ ProcessorBuffer ref_parse(const std::string &s) {
         next_symbol<ParseFn>("_ZN4sfxb12parse_bufferERKNSt7__cxx1112basic_stringIcSt11char_traitsIcESaIcEEE");
     return f(s);
 }
-
-size_t min_cts() {
-    static size_t n = [] {
-        const char *e = std::getenv("SFXB_WIRE_MIN_CTS");
-        return e ? (size_t)std::strtoull(e, nullptr, 10) : (size_t)4096;
-    }();
-    return n;
-}
-
 
 constexpr char kMagic[4] = {'S', 'F', 'X', 'B'};
 
@@ -141,6 +141,8 @@ void get_ct_at(mpz_class &v, const char *src, size_t len) {
     mpz_limbs_finish(v.get_mpz_t(), (mp_size_t)nl);
 }
 
+// ---------------------------------------------------------------- serialize
+
 // Ciphertext runs of one buffer in wire order: (first ciphertext, count)
 using Runs = std::vector<std::pair<const Ciphertext *, size_t>>;
 
@@ -150,10 +152,17 @@ using Runs = std::vector<std::pair<const Ciphertext *, size_t>>;
 struct Layout {
     std::string prefix;
     std::vector<std::string> between; // bytes after run r
+    Runs runs;
+    std::string *gap() { return between.empty() ? &prefix : &between.back(); }
+    void run(const std::vector<Ciphertext> &v) {
+        runs.emplace_back(v.data(), v.size());
+        between.emplace_back();
+    }
 };
 
-std::string emit(const Layout &lay, const Runs &runs) {
-    ++stats.ser_fast;
+std::string emit(const Layout &lay) {
+    ++stats.ser_native;
+    const Runs &runs = lay.runs;
     size_t total = 0;
     for (const auto &r : runs) total += r.second;
     std::vector<const Ciphertext *> ct(total);
@@ -186,6 +195,8 @@ std::string emit(const Layout &lay, const Runs &runs) {
     return out;
 }
 
+void put_u8(std::string &s, uint8_t v) { s.push_back(static_cast<char>(v)); }
+
 void put_u32(std::string &s, uint32_t v) {
     char b[4];
     le32(b, v);
@@ -194,13 +205,55 @@ void put_u32(std::string &s, uint32_t v) {
 
 std::string head_bytes(const ProcessorBuffer &b) {
     std::string s(kMagic, 4);
-    s.push_back(static_cast<char>(b.version));
-    s.push_back(static_cast<char>(static_cast<uint8_t>(b.kind)));
+    put_u8(s, b.version);
+    put_u8(s, static_cast<uint8_t>(b.kind));
     for (uint32_t h : b.header) put_u32(s, h);
     return s;
 }
 
 bool enc_hist_kind(BufferKind k) { return k == BufferKind::histogram_enc || k == BufferKind::agg_result_enc; }
+
+// put_packed (secure_processor.cpp:92-100): six u32 descriptors, then the run
+void packed_into(Layout &lay, const PackedVector &v) {
+    std::string *g = lay.gap();
+    put_u32(*g, v.logical_length);
+    put_u32(*g, v.addend_count);
+    put_u32(*g, v.slot_bits);
+    put_u32(*g, v.guard_bits);
+    put_u32(*g, v.scale_bits);
+    put_u32(*g, static_cast<uint32_t>(v.cts.size()));
+    lay.run(v.cts);
+}
+
+// ---------------------------------------------------------------- parse
+
+// WireReader (secure_processor.cpp:52-90) positions and errors
+struct Cursor {
+    const char *d;
+    size_t size, pos;
+    [[noreturn]] void truncated() const { throw ParseError("truncated buffer", size); }
+    uint8_t u8() {
+        if (pos >= size) truncated();
+        return static_cast<uint8_t>(d[pos++]);
+    }
+    uint32_t u32() {
+        if (size - pos < 4) truncated(); // the reference reads byte by byte up to the end
+        const uint32_t v = rd32(d + pos);
+        pos += 4;
+        return v;
+    }
+    // one ciphertext entry: its offset (of the length prefix)
+    size_t ct() {
+        const size_t at = pos;
+        const uint32_t len = u32();
+        if (pos + len > size) throw ParseError("truncated ciphertext entry", pos);
+        pos += len;
+        return at;
+    }
+    void done() const {
+        if (pos != size) throw ParseError("trailing bytes in buffer", pos);
+    }
+};
 
 // Offsets of the length-prefixed entries of d[start, size) in wire order, as
 // the serial walk from `start` finds them; true iff that walk reads exactly n
@@ -283,126 +336,160 @@ bool walk_entries(const char *d, size_t size, size_t start, uint64_t n, std::vec
     return p == size && off.size() == n;
 }
 
+// imports of every recorded entry into its destination, on all host threads
+void import_entries(const char *d, const std::vector<size_t> &off, const std::vector<Ciphertext *> &dst) {
+    hostpar::parallel_for(off.size(), [&](size_t lo, size_t hi) {
+        for (size_t k = lo; k < hi; ++k) get_ct_at(dst[k]->value, d + off[k] + 4, rd32(d + off[k]));
+    }, 1024);
+}
+
+// gh_pairs_enc body (secure_processor.cpp:238-246)
+GhPayload parse_gh(Cursor &r, uint32_t n_samples) {
+    GhPayload gh;
+    gh.encrypted = true;
+    gh.n_samples = n_samples;
+    const uint64_t n = 2ull * n_samples;
+    std::vector<size_t> off;
+    bool ok = false;
+    if (n <= (r.size - r.pos) / 4) {
+        // the n empty ciphertexts are constructed on a second thread while the
+        // length chain is walked on all host threads
+        std::thread alloc([&] { gh.cts.resize(n); });
+        ok = walk_entries(r.d, r.size, r.pos, n, off);
+        alloc.join();
+    }
+    if (!ok) {
+        // malformed (or cannot hold n length prefixes): the reference's own
+        // sequence — reserve, read entry by entry, then the trailing check —
+        // raises the error at its offset
+        gh.cts.clear();
+        gh.cts.shrink_to_fit();
+        gh.cts.reserve(n);
+        for (uint64_t i = 0; i < n; ++i) r.ct();
+        r.done();
+        throw Error("wire codec: gh walk disagrees with the serial reader"); // not reached
+    }
+    std::vector<Ciphertext *> dst(n);
+    for (uint64_t i = 0; i < n; ++i) dst[i] = &gh.cts[i];
+    import_entries(r.d, off, dst);
+    r.pos = r.size;
+    return gh;
+}
+
+// read_packed (secure_processor.cpp:102-113): descriptors, then the entries;
+// returns the entry count
+size_t read_packed(Cursor &r, PackedVector &v, std::vector<size_t> &off) {
+    v.logical_length = r.u32();
+    v.addend_count = r.u32();
+    v.slot_bits = r.u32();
+    v.guard_bits = r.u32();
+    v.scale_bits = r.u32();
+    const uint32_t n = r.u32();
+    v.cts.reserve(n);
+    for (uint32_t i = 0; i < n; ++i) off.push_back(r.ct());
+    return n;
+}
+
+// histogram_enc / agg_result_enc body (secure_processor.cpp:272-299)
+HistogramPayload parse_hist(Cursor &r, const uint32_t header[3]) {
+    HistogramPayload hp;
+    const uint8_t layout = r.u8();
+    if (layout > 1) throw ParseError("unknown encrypted histogram layout", r.pos - 1);
+    hp.layout = static_cast<HistLayout>(layout);
+    const uint32_t n_bins = header[1];
+    std::vector<size_t> off; // every entry in wire order
+    struct Run {
+        size_t node;
+        int vec; // 0 scalar_cts, 1 packed_g, 2 packed_h
+        size_t count;
+    };
+    std::vector<Run> runs;
+    for (uint32_t ni = 0; ni < header[2]; ++ni) {
+        NodeHistogram node;
+        node.node_id = r.u32();
+        node.n_bins = static_cast<int>(n_bins);
+        const uint32_t n_feats = r.u32();
+        for (uint32_t f = 0; f < n_feats; ++f) node.feature_ids.push_back(static_cast<int>(r.u32()));
+        if (hp.layout == HistLayout::enc_scalar) {
+            const uint64_t cnt = 2ull * n_feats * n_bins;
+            node.scalar_cts.reserve(cnt);
+            for (uint64_t i = 0; i < cnt; ++i) off.push_back(r.ct());
+            runs.push_back(Run{hp.nodes.size(), 0, (size_t)cnt});
+        } else {
+            runs.push_back(Run{hp.nodes.size(), 1, read_packed(r, node.packed_g, off)});
+            runs.push_back(Run{hp.nodes.size(), 2, read_packed(r, node.packed_h, off)});
+        }
+        hp.nodes.push_back(std::move(node));
+    }
+    r.done();
+    // destinations in wire order, then the imports on all host threads
+    std::vector<Ciphertext *> dst;
+    dst.reserve(off.size());
+    for (const Run &run : runs) {
+        NodeHistogram &nd = hp.nodes[run.node];
+        std::vector<Ciphertext> &v = run.vec == 0 ? nd.scalar_cts : run.vec == 1 ? nd.packed_g.cts : nd.packed_h.cts;
+        v.resize(run.count);
+        for (Ciphertext &c : v) dst.push_back(&c);
+    }
+    const hostpar::TopPadScope pad(r.size); // the limb arrays total ≈ the wire bytes
+    import_entries(r.d, off, dst);
+    return hp;
+}
+
 } // namespace
 
-// secure_processor.cpp:119-215 (fast path: gh_pairs_enc, scalar encrypted histograms)
+// secure_processor.cpp:119-215 for the ciphertext kinds
 std::string serialize_buffer(const ProcessorBuffer &buffer) {
     if (buffer.kind == BufferKind::gh_pairs_enc) {
-        const auto *gh = std::get_if<GhPayload>(&buffer.payload);
-        if (!gh || gh->cts.size() < min_cts()) return ref_serialize(buffer);
-        Layout lay{head_bytes(buffer), {std::string()}};
-        return emit(lay, Runs{{gh->cts.data(), gh->cts.size()}});
-    }
-    if (enc_hist_kind(buffer.kind)) {
-        const auto *hp = std::get_if<HistogramPayload>(&buffer.payload);
-        if (!hp || hp->layout != HistLayout::enc_scalar) return ref_serialize(buffer);
-        size_t n = 0;
-        for (const NodeHistogram &nd : hp->nodes) n += nd.scalar_cts.size();
-        if (n < min_cts()) return ref_serialize(buffer);
+        const auto &gh = std::get<GhPayload>(buffer.payload);
         Layout lay;
         lay.prefix = head_bytes(buffer);
-        lay.prefix.push_back(static_cast<char>(static_cast<uint8_t>(hp->layout)));
-        Runs runs;
-        std::string *gap = &lay.prefix;
-        for (const NodeHistogram &nd : hp->nodes) {
-            put_u32(*gap, nd.node_id);
-            put_u32(*gap, static_cast<uint32_t>(nd.feature_ids.size()));
-            for (int fid : nd.feature_ids) put_u32(*gap, static_cast<uint32_t>(fid));
-            runs.emplace_back(nd.scalar_cts.data(), nd.scalar_cts.size());
-            lay.between.emplace_back();
-            gap = &lay.between.back();
+        lay.run(gh.cts);
+        return emit(lay);
+    }
+    if (enc_hist_kind(buffer.kind)) {
+        const auto &hp = std::get<HistogramPayload>(buffer.payload);
+        Layout lay;
+        lay.prefix = head_bytes(buffer);
+        put_u8(lay.prefix, static_cast<uint8_t>(hp.layout));
+        for (const NodeHistogram &nd : hp.nodes) {
+            std::string *g = lay.gap();
+            put_u32(*g, nd.node_id);
+            put_u32(*g, static_cast<uint32_t>(nd.feature_ids.size()));
+            for (int fid : nd.feature_ids) put_u32(*g, static_cast<uint32_t>(fid));
+            if (hp.layout == HistLayout::enc_scalar) {
+                lay.run(nd.scalar_cts);
+            } else {
+                packed_into(lay, nd.packed_g);
+                packed_into(lay, nd.packed_h);
+            }
         }
-        if (runs.empty()) return ref_serialize(buffer);
-        return emit(lay, runs);
+        return emit(lay);
     }
     return ref_serialize(buffer);
 }
 
-// secure_processor.cpp:221-375 (fast path: gh_pairs_enc, scalar encrypted histograms)
+// secure_processor.cpp:221-375 for the ciphertext kinds
 ProcessorBuffer parse_buffer(const std::string &bytes) {
-    const size_t size = bytes.size();
-    const char *d = bytes.data();
-    if (size < 18 || std::memcmp(d, kMagic, 4) != 0 || static_cast<uint8_t>(d[4]) != 1) return ref_parse(bytes);
-    const uint8_t kind = static_cast<uint8_t>(d[5]);
-    const bool gh = kind == static_cast<uint8_t>(BufferKind::gh_pairs_enc);
-    const bool hist = enc_hist_kind(static_cast<BufferKind>(kind));
-    if (!gh && !hist) return ref_parse(bytes);
-    const hostpar::TopPadScope pad(size); // the limb arrays total ≈ the wire bytes
+    Cursor r{bytes.data(), bytes.size(), 0};
+    if (r.size < 4 || std::memcmp(r.d, kMagic, 4) != 0) throw ParseError("bad buffer magic", 0);
+    r.pos = 4;
     ProcessorBuffer buf;
-    buf.version = 1;
+    buf.version = r.u8();
+    if (buf.version != 1) throw ParseError("unsupported buffer version", 4);
+    const uint8_t kind = r.u8();
+    if (kind < 1 || kind > 8) throw ParseError("unknown buffer kind", 5);
     buf.kind = static_cast<BufferKind>(kind);
-    for (int i = 0; i < 3; ++i) buf.header[i] = rd32(d + 6 + 4 * i);
-    size_t pos = 18;
-    // entry offsets of every ciphertext, in wire order; any truncation or
-    // trailing byte hands the buffer to the reference (which reports it)
-    std::vector<size_t> off;
-    auto walk = [&](uint64_t count) -> bool {
-        if (count > (size - pos) / 4) return false;
-        for (uint64_t i = 0; i < count; ++i) {
-            if (size - pos < 4) return false;
-            const uint32_t len = rd32(d + pos);
-            if (len > size - pos - 4) return false;
-            // the length chain is serially dependent: prefetch where the
-            // entry 16 ahead lands if the lengths repeat (they almost all
-            // do: full-size residues mod n²)
-            __builtin_prefetch(d + pos + 16 * (4 + (size_t)len));
-            off.push_back(pos);
-            pos += 4 + (size_t)len;
-        }
-        return true;
-    };
+    const bool gh = buf.kind == BufferKind::gh_pairs_enc, hist = enc_hist_kind(buf.kind);
+    if (!gh && !hist) return ref_parse(bytes);
+    for (uint32_t &h : buf.header) h = r.u32();
     if (gh) {
-        const uint64_t n = 2ull * buf.header[0];
-        if (n < min_cts()) return ref_parse(bytes);
-        if (n > (size - pos) / 4) return ref_parse(bytes); // cannot hold n length prefixes
-        // the payload's n empty ciphertexts are constructed on a second thread
-        // while the length chain is walked (walk_entries, all host threads)
-        GhPayload p;
-        p.encrypted = true;
-        p.n_samples = buf.header[0];
-        std::thread alloc([&] { p.cts.resize(n); });
-        const bool ok = walk_entries(d, size, pos, n, off);
-        alloc.join();
-        if (!ok) return ref_parse(bytes);
-        hostpar::parallel_for(n, [&](size_t lo, size_t hi) {
-            for (size_t k = lo; k < hi; ++k) get_ct_at(p.cts[k].value, d + off[k] + 4, rd32(d + off[k]));
-        }, 1024);
-        buf.payload = std::move(p);
-        ++stats.parse_fast;
-        return buf;
+        const hostpar::TopPadScope pad(r.size); // the limb arrays total ≈ the wire bytes
+        buf.payload = parse_gh(r, buf.header[0]);
+    } else {
+        buf.payload = parse_hist(r, buf.header);
     }
-    if (size - pos < 1 || static_cast<uint8_t>(d[pos]) != 0) return ref_parse(bytes); // packed / bad layout
-    ++pos;
-    const uint32_t n_bins = buf.header[1];
-    HistogramPayload hp;
-    hp.layout = HistLayout::enc_scalar;
-    std::vector<std::pair<size_t, size_t>> node_runs; // (first entry, count)
-    for (uint32_t ni = 0; ni < buf.header[2]; ++ni) {
-        if (size - pos < 8) return ref_parse(bytes);
-        NodeHistogram node;
-        node.node_id = rd32(d + pos);
-        node.n_bins = static_cast<int>(n_bins);
-        const uint32_t n_feats = rd32(d + pos + 4);
-        pos += 8;
-        if (n_feats > (size - pos) / 4) return ref_parse(bytes);
-        node.feature_ids.reserve(n_feats);
-        for (uint32_t f = 0; f < n_feats; ++f, pos += 4) node.feature_ids.push_back(static_cast<int>(rd32(d + pos)));
-        const uint64_t cnt = 2ull * n_feats * n_bins;
-        const size_t first = off.size();
-        if (!walk(cnt)) return ref_parse(bytes);
-        node_runs.emplace_back(first, (size_t)cnt);
-        hp.nodes.push_back(std::move(node));
-    }
-    if (pos != size || off.size() < min_cts()) return ref_parse(bytes);
-    for (size_t i = 0; i < hp.nodes.size(); ++i) hp.nodes[i].scalar_cts.resize(node_runs[i].second);
-    std::vector<Ciphertext *> dst(off.size());
-    for (size_t i = 0, k = 0; i < hp.nodes.size(); ++i)
-        for (Ciphertext &c : hp.nodes[i].scalar_cts) dst[k++] = &c;
-    hostpar::parallel_for(off.size(), [&](size_t lo, size_t hi) {
-        for (size_t k = lo; k < hi; ++k) get_ct_at(dst[k]->value, d + off[k] + 4, rd32(d + off[k]));
-    }, 1024);
-    buf.payload = std::move(hp);
-    ++stats.parse_fast;
+    ++stats.parse_native;
     return buf;
 }
 
