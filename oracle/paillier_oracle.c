@@ -443,3 +443,83 @@ double orc_decode_int_sum(const orc_key *k, const int64_t *terms, size_t count, 
     mpz_clear(t);
     return d;
 }
+
+/* ---- integer-sum histograms, the checker at scale ----
+ * accumulate_rows (secure_processor.cpp:587-620) followed by decrypt_histogram
+ * (:679-719), expressed on plaintexts: Dec(∏ c_i) = Σ m_i mod n with m_i ≡ q_i
+ * (mod n), so slot (node i, feature f, bin b, G/H) decrypts to (Σ q) mod n,
+ * decoded by decode_fixed (he.cpp:138-143, orc_decode_fixed).  q: 2·n_samples
+ * signed fixed-point integers (G, H interleaved); bins: n_features columns of
+ * n_samples; the frontier as node offsets + rows.  Empty slots stay the
+ * trivial zero (decrypt_slot → 0.0, uncounted).  out: N·J·K·2 doubles in the
+ * slot layout 2(f·K+b)+{G,H} per node; *adds += Σ max(count − 1, 0) (fold_into
+ * :724-732); *decs += non-empty slots.  Features run in parallel (OpenMP):
+ * they write disjoint slots. */
+int orc_intsum_hist(const orc_key *k, const int64_t *q, uint32_t n_samples, const uint16_t *bins, uint32_t J,
+                    const uint32_t *node_offsets, uint32_t N, const uint32_t *rows, uint32_t K, unsigned scale,
+                    double *out, uint64_t *adds, uint64_t *decs) {
+    const size_t slots = (size_t)N * J * K * 2;
+    __int128 *sum = calloc(slots ? slots : 1, sizeof(__int128));
+    uint32_t *cnt = calloc(slots ? slots : 1, sizeof(uint32_t));
+    if (!sum || !cnt) {
+        free(sum);
+        free(cnt);
+        return fail("intsum_hist: out of memory");
+    }
+    int bad = 0;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (uint32_t f = 0; f < J; ++f) {
+        const uint16_t *col = bins + (size_t)f * n_samples;
+        for (uint32_t i = 0; i < N; ++i) {
+            const size_t base = ((size_t)i * J + f) * K * 2;
+            for (uint32_t t = node_offsets[i]; t < node_offsets[i + 1]; ++t) {
+                const uint32_t row = rows[t];
+                if (row >= n_samples || col[row] >= K) {
+                    bad = 1;
+                    continue;
+                }
+                const size_t s = base + 2 * (size_t)col[row];
+                sum[s] += q[2 * (size_t)row];
+                sum[s + 1] += q[2 * (size_t)row + 1];
+                cnt[s]++;
+                cnt[s + 1]++;
+            }
+        }
+    }
+    if (bad) {
+        free(sum);
+        free(cnt);
+        return fail("bin index out of range in accumulate");
+    }
+    uint64_t a = 0, d = 0;
+#pragma omp parallel reduction(+ : a, d)
+    {
+        mpz_t m;
+        mpz_init(m);
+        uint32_t *buf = malloc(k->nw * 4);
+#pragma omp for schedule(static)
+        for (size_t s = 0; s < slots; ++s) {
+            if (!cnt[s]) {
+                out[s] = 0.0;
+                continue;
+            }
+            a += cnt[s] - 1;
+            d += 1;
+            const __int128 v = sum[s];
+            const unsigned __int128 mag = v < 0 ? (unsigned __int128)(-v) : (unsigned __int128)v;
+            const uint64_t w[2] = {(uint64_t)mag, (uint64_t)(mag >> 64)};
+            mpz_import(m, 2, -1, 8, 0, 0, w);
+            if (v < 0) mpz_neg(m, m);
+            mpz_mod(m, m, k->n); /* the plaintext the decryption produces */
+            exp_words(buf, k->nw, m);
+            out[s] = orc_decode_fixed(k, buf, scale);
+        }
+        free(buf);
+        mpz_clear(m);
+    }
+    *adds += a;
+    *decs += d;
+    free(sum);
+    free(cnt);
+    return 0;
+}

@@ -103,6 +103,9 @@ class Oracle:
                                           C.POINTER(C.c_uint64)]
         lib.orc_decode_int_sum.restype = C.c_double
         lib.orc_decode_int_sum.argtypes = [C.c_void_p, _i64p, C.c_size_t, C.c_uint]
+        lib.orc_intsum_hist.argtypes = [C.c_void_p, _i64p, C.c_uint32, _u16p, C.c_uint32, _u32p, C.c_uint32,
+                                        _u32p, C.c_uint32, C.c_uint, _f64p, C.POINTER(C.c_uint64),
+                                        C.POINTER(C.c_uint64)]
 
     def _check(self, rc):
         if rc != 0:
@@ -199,6 +202,20 @@ class OracleKey:
     def decode_int_sum(self, terms, scale: int = 40) -> float:
         t = np.ascontiguousarray(terms, dtype=np.int64)
         return self.o.lib.orc_decode_int_sum(self.h, t, len(t), scale)
+
+    def intsum_hist(self, q, bins, offs, rows, n_bins: int, scale: int = 40):
+        """Decrypted histograms of one frontier from the plaintexts (orc_intsum_hist):
+        (values N×J×K×2 doubles, reference additions, reference decryptions)."""
+        q = np.ascontiguousarray(q, dtype=np.int64)
+        bins = np.ascontiguousarray(bins, dtype=np.uint16)
+        J = bins.shape[0]
+        N = len(offs) - 1
+        out = np.empty(N * J * n_bins * 2, np.float64)
+        adds, decs = C.c_uint64(0), C.c_uint64(0)
+        self.o._check(self.o.lib.orc_intsum_hist(
+            self.h, q, len(q) // 2, bins.reshape(-1), J, np.ascontiguousarray(offs, dtype=np.uint32), N,
+            np.ascontiguousarray(rows, dtype=np.uint32), n_bins, scale, out, C.byref(adds), C.byref(decs)))
+        return out, adds.value, decs.value
 
 
 # ---------------------------------------------------------------- reference

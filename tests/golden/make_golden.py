@@ -100,7 +100,57 @@ TRAIN_CONFIGS = {
     "vertical_threaded_3p": ("vertical_threaded_3p.ini", 512, 0xC0FFEE),
     "vertical_c1_1024": ("vertical_c1_1024.ini", 1024, 7),
     "horizontal_toy1024": ("horizontal_toy1024.ini", 1024, 7),
+    "vertical_toy2048": ("vertical_toy2048.ini", 2048, 7),
 }
+
+# Runs too large for the CPU Paillier plugin: the reference training loop with
+# the integer-sum oracle plugin (oracle/intsum_plugin.cpp, pinned against the
+# CPU Paillier plugin on vertical_toy512 and vertical_c1_1024 by
+# tests/test_oracle.py) under the recording wrapper (oracle/record_plugin.cpp).
+SCALE_CONFIGS = {
+    "vertical_c2_2048": ("vertical_c2_2048.ini", 2048, 7),
+}
+
+
+def record_lines(stderr):
+    """the recording wrapper's per-plugin JSON lines, in plugin destruction order"""
+    return [json.loads(ln.split("] ", 1)[1]) for ln in stderr.splitlines() if ln.startswith("[sfxb-record]")]
+
+
+def run_recorded(ini, bits, seed, preload_after, env=None, timeout=3600):
+    """run_training through tests/train_driver.py with the recording wrapper
+    ahead of `preload_after` (a plugin library or None = the reference's own)"""
+    import subprocess
+
+    rec = os.path.join(ROOT, "oracle", "_ref", "librecord_plugin.so")
+    pre = rec + (" " + preload_after if preload_after else "")
+    e = dict(os.environ, **(env or {}))
+    e["LD_PRELOAD"] = pre
+    drv = os.path.join(ROOT, "tests", "train_driver.py")
+    out = subprocess.run([sys.executable, drv, os.path.join(ROOT, "tests", "configs", ini), str(bits), str(seed)],
+                         capture_output=True, text=True, env=e, timeout=timeout)
+    if out.returncode != 0:
+        raise RuntimeError(out.stderr[-3000:])
+    res = json.loads(out.stdout)
+    res["records"] = record_lines(out.stderr)
+    return res
+
+
+def scale_goldens(names=None):
+    """integer-sum oracle runs -> tests/golden/train_<name>_intsum.json"""
+    intsum = os.path.join(ROOT, "oracle", "_ref", "libintsum_plugin.so")
+    for name, (ini, bits, seed) in SCALE_CONFIGS.items():
+        if names and name not in names:
+            continue
+        res = run_recorded(ini, bits, seed, intsum)
+        keep = {k: res[k] for k in ("forest", "partials", "counters")}
+        keep["counters"] = keep["counters"][:3]  # bytes differ (shorter values on the wire)
+        keep["records"] = [{k: r[k] for k in ("key", "private", "decrypt_calls", "slots", "fnv", "per_call", "counters")}
+                           for r in res["records"]]
+        path = os.path.join(HERE, f"train_{name}_intsum.json")
+        with open(path, "w") as f:
+            json.dump(keep, f, indent=1)
+        print("wrote", path, flush=True)
 
 
 def train_goldens(names=None):
@@ -122,5 +172,7 @@ def train_goldens(names=None):
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "train":
         train_goldens(sys.argv[2:] or None)
+    elif len(sys.argv) > 1 and sys.argv[1] == "scale":
+        scale_goldens(sys.argv[2:] or None)
     else:
         main()

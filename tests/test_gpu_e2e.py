@@ -41,7 +41,7 @@ def _train_with_plugin(name, devices=None, extra_env=None):
 
 
 @pytest.mark.parametrize("name", ["vertical_toy512", "vertical_threaded_3p", "vertical_c1_1024",
-                                  "horizontal_toy1024"])
+                                  "vertical_toy2048", "horizontal_toy1024"])
 def test_reference_training_loop_with_gpu_plugin(name):
     _need(PLUGIN)
     _need(os.path.join(REF, "libsfxb_refcapi.so"))

@@ -11,6 +11,7 @@ import json
 import math
 import os
 import random
+import sys
 
 import numpy as np
 import pytest
@@ -20,6 +21,7 @@ from py_oracle import (Oracle, OracleError, OracleKey, RefPlugin, Reference, int
                        reference_available, to_words, words_to_ints)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
 
 
 @pytest.fixture(scope="module")
@@ -177,3 +179,53 @@ def test_keys_fixture_sizes():
 def test_to_words_roundtrip():
     x = (1 << 200) + 12345
     assert words_to_ints(to_words(x, 8)[None, :]) == [x]
+
+
+# ---- integer-sum oracle plugin (oracle/intsum_plugin.cpp) -----------------
+
+
+def _scale_libs():
+    ref = os.path.join(ROOT, "oracle", "_ref")
+    libs = [os.path.join(ref, x) for x in ("libintsum_plugin.so", "librecord_plugin.so", "libsfxb_refcapi.so")]
+    for p in libs:
+        if not os.path.exists(p):
+            pytest.skip(f"{p} not built")
+    return libs[0]
+
+
+@pytest.mark.parametrize("name", ["vertical_toy512", "vertical_threaded_3p"])
+def test_intsum_plugin_equals_cpu_paillier(name):
+    """The integer-sum oracle plugin reproduces the reference's CPU Paillier
+    run: forest, partial models, enc/add/dec counters and every decrypted
+    histogram (recording wrapper digests, call by call).  (Also checked on
+    BASELINE config 1, 10k × 8 at 1024-bit, when the golden was made.)"""
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    from make_golden import TRAIN_CONFIGS, run_recorded
+
+    intsum = _scale_libs()
+    ini, bits, seed = TRAIN_CONFIGS[name]
+    a = run_recorded(ini, bits, seed, None)
+    b = run_recorded(ini, bits, seed, intsum)
+    assert a["forest"] == b["forest"] and a["partials"] == b["partials"]
+    assert a["counters"][:3] == b["counters"][:3]
+    assert len(a["records"]) == len(b["records"]) >= 2
+    for x, y in zip(a["records"], b["records"]):
+        for k in ("key", "private", "decrypt_calls", "slots", "per_call", "fnv", "counters"):
+            assert x[k] == y[k], k
+
+
+def test_intsum_golden_at_c2_reproduces():
+    """tests/golden/train_vertical_c2_2048_intsum.json is what the oracle
+    plugin produces now (1M × 28, 2048-bit, depth 6, two trees; ≈30 s)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    from make_golden import SCALE_CONFIGS, run_recorded
+
+    intsum = _scale_libs()
+    want = json.load(open(os.path.join(ROOT, "tests", "golden", "train_vertical_c2_2048_intsum.json")))
+    ini, bits, seed = SCALE_CONFIGS["vertical_c2_2048"]
+    got = run_recorded(ini, bits, seed, intsum)
+    assert got["forest"] == want["forest"] and got["partials"] == want["partials"]
+    assert got["counters"][:3] == want["counters"]
+    for x, y in zip(got["records"], want["records"]):
+        for k in ("key", "private", "decrypt_calls", "slots", "per_call", "fnv", "counters"):
+            assert x[k] == y[k], k
