@@ -260,6 +260,10 @@ class Reference:
         lib.ref_accumulate_threaded.argtypes = [_u32p, C.c_size_t, _u32p, C.c_uint32, _u16p, C.c_uint32,
                                                 _u32p, C.c_uint32, _u32p, C.c_uint32, C.c_int,
                                                 C.POINTER(C.c_uint64)]
+        lib.ref_encrypt_threaded.argtypes = [_u32p, C.c_size_t, C.c_uint32, C.c_int, C.POINTER(C.c_uint64),
+                                             C.POINTER(C.c_double)]
+        lib.ref_decrypt_threaded.argtypes = [_u32p, _u32p, C.c_size_t, _u32p, C.c_uint32, C.c_int,
+                                             C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
         lib.ref_train.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t, C.c_char_p, C.c_size_t,
                                   C.POINTER(C.c_uint64 * 4), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                   C.POINTER(C.c_double * 6)]

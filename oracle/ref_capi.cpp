@@ -15,6 +15,7 @@
 #include <gmp.h>
 
 #include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <fstream>
@@ -257,7 +258,10 @@ int ref_decrypt_slots(void *h, const std::uint32_t *slots, std::uint32_t n_nodes
 
 // CPU baseline with all host threads: `threads` independent plugin instances
 // (the plugin is stateless apart from keys and counters, secure_processor.hpp:111)
-// each accumulate a feature slice of the same node list.  Returns adds performed.
+// claim work items (feature f, row range k) from a shared counter; an item is
+// accumulate_rows over the frontier restricted to the range's rows for one
+// feature (J × threads items, so every thread stays busy whatever J is).
+// Returns the additions performed (each instance's counter) and the wall time.
 int ref_accumulate_threaded(const std::uint32_t *n, std::size_t nw, const std::uint32_t *cts,
                             std::uint32_t n_samples, const std::uint16_t *bins,
                             std::uint32_t n_features, const std::uint32_t *node_offsets,
@@ -272,22 +276,30 @@ int ref_accumulate_threaded(const std::uint32_t *n, std::size_t nw, const std::u
             ps.push_back(std::move(rp));
         }
         GhPayload gh = gh_from_words(ps[0].get(), cts, n_samples);
-        std::vector<NodeRows> nodes(n_nodes);
-        for (std::uint32_t i = 0; i < n_nodes; ++i) {
-            nodes[i].node_id = i;
-            nodes[i].rows.assign(rows + node_offsets[i], rows + node_offsets[i + 1]);
-        }
-        // work items: (feature) slices round-robin over threads
+        // the frontier cut into `threads` contiguous row ranges
+        const std::uint32_t chunks = static_cast<std::uint32_t>(threads);
+        std::vector<std::vector<NodeRows>> part(chunks, std::vector<NodeRows>(n_nodes));
+        for (std::uint32_t i = 0; i < n_nodes; ++i)
+            for (std::uint32_t t = node_offsets[i]; t < node_offsets[i + 1]; ++t) {
+                const std::uint32_t k = static_cast<std::uint32_t>(std::uint64_t(rows[t]) * chunks / n_samples);
+                part[k][i].node_id = i;
+                part[k][i].rows.push_back(rows[t]);
+            }
+        std::vector<std::vector<std::uint16_t>> cols(n_features);
+        for (std::uint32_t f = 0; f < n_features; ++f)
+            cols[f].assign(bins + std::size_t(f) * n_samples, bins + std::size_t(f + 1) * n_samples);
+        std::atomic<std::uint32_t> next{0};
+        const std::uint32_t items = n_features * chunks;
         std::vector<std::thread> pool;
         std::vector<std::string> errs(threads);
         for (int t = 0; t < threads; ++t)
             pool.emplace_back([&, t] {
                 try {
-                    for (std::uint32_t f = t; f < n_features; f += threads) {
-                        std::vector<std::vector<std::uint16_t>> b(1);
-                        b[0].assign(bins + std::size_t(f) * n_samples,
-                                    bins + std::size_t(f + 1) * n_samples);
-                        ps[t]->plugin->accumulate_rows(gh, b, {int(f)}, nodes, int(n_bins));
+                    std::vector<std::vector<std::uint16_t>> b(1);
+                    for (std::uint32_t it; (it = next.fetch_add(1)) < items;) {
+                        const std::uint32_t f = it % n_features, k = it / n_features;
+                        b[0] = cols[f];
+                        ps[t]->plugin->accumulate_rows(gh, b, {int(f)}, part[k], int(n_bins));
                     }
                 } catch (const std::exception &e) {
                     errs[t] = e.what();
@@ -299,6 +311,80 @@ int ref_accumulate_threaded(const std::uint32_t *n, std::size_t nw, const std::u
         std::uint64_t adds = 0;
         for (auto &p : ps) adds += p->plugin->counters().ciphertext_additions;
         *additions = adds;
+    });
+}
+
+// Reference encrypt_gh (secure_processor.cpp:574-585) on all host threads:
+// one plugin per thread (rng seed t + 1), `pairs` (g, h) pairs each.
+// Returns the encryptions performed and the wall seconds.
+int ref_encrypt_threaded(const std::uint32_t *n, std::size_t nw, std::uint32_t pairs, int threads,
+                         std::uint64_t *encryptions, double *seconds) {
+    return guarded([&] {
+        std::vector<std::unique_ptr<RefPlugin>> ps;
+        for (int t = 0; t < threads; ++t) {
+            auto rp = std::unique_ptr<RefPlugin>(
+                static_cast<RefPlugin *>(ref_plugin_new(n, nullptr, nullptr, nw, 1 + t, 40)));
+            if (!rp) throw Error(g_err);
+            ps.push_back(std::move(rp));
+        }
+        std::vector<GHPair> gh(pairs);
+        for (std::uint32_t i = 0; i < pairs; ++i)
+            gh[i] = GHPair{(i % 2 ? -0.37 : 0.41) + 1e-3 * (i % 97), 0.2 - 1e-4 * (i % 89)};
+        std::vector<std::thread> pool;
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int t = 0; t < threads; ++t) pool.emplace_back([&, t] { (void)ps[t]->plugin->encrypt_gh(gh); });
+        for (auto &th : pool) th.join();
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        std::uint64_t e = 0;
+        for (auto &p : ps) e += p->plugin->counters().encryptions;
+        *encryptions = e;
+    });
+}
+
+// Reference decrypt_histogram (secure_processor.cpp:679-719) on all host
+// threads: the `count` ciphertexts (2·nw limbs each) split into one slice per
+// thread, each slice one node × one feature × slice/2 bins of the key
+// holder's plugin.  Returns the decryptions performed and the wall seconds.
+int ref_decrypt_threaded(const std::uint32_t *p, const std::uint32_t *q, std::size_t nw,
+                         const std::uint32_t *cts, std::uint32_t count, int threads,
+                         std::uint64_t *decryptions, double *seconds) {
+    return guarded([&] {
+        std::vector<std::unique_ptr<RefPlugin>> ps;
+        std::vector<HistogramPayload> hp(threads);
+        const std::uint32_t per = (count / threads) & ~1u;
+        for (int t = 0; t < threads; ++t) {
+            auto rp = std::unique_ptr<RefPlugin>(static_cast<RefPlugin *>(ref_plugin_new(nullptr, p, q, nw, 1, 40)));
+            if (!rp) throw Error(g_err);
+            hp[t].layout = HistLayout::enc_scalar;
+            NodeHistogram nh;
+            nh.node_id = 0;
+            nh.n_bins = int(per / 2);
+            nh.feature_ids = {0};
+            for (std::uint32_t i = 0; i < per; ++i) {
+                const std::uint32_t *w = cts + (std::size_t(t) * per + i) * 2 * nw;
+                nh.scalar_cts.push_back(Ciphertext{from_words(w, 2 * nw), rp->pub.key_id});
+            }
+            hp[t].nodes.push_back(std::move(nh));
+            ps.push_back(std::move(rp));
+        }
+        std::vector<std::thread> pool;
+        std::vector<std::string> errs(threads);
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int t = 0; t < threads; ++t)
+            pool.emplace_back([&, t] {
+                try {
+                    (void)ps[t]->plugin->decrypt_histogram(hp[t]);
+                } catch (const std::exception &e) {
+                    errs[t] = e.what();
+                }
+            });
+        for (auto &th : pool) th.join();
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        for (auto &e : errs)
+            if (!e.empty()) throw Error(e);
+        std::uint64_t d = 0;
+        for (auto &pp : ps) d += pp->plugin->counters().decryptions;
+        *decryptions = d;
     });
 }
 
