@@ -295,7 +295,7 @@ def wire_codec(a):
     return res
 
 
-def plugin_e2e(a):
+def plugin_e2e(a, devices=None):
     """The reference-facing end to end: tools/plugin_bench.cpp drives the
     reference's EncryptionPlugin calls of one tree (encrypt_gh, accumulate_rows
     per level and party, decrypt_histogram per level and party) with the GPU
@@ -310,6 +310,10 @@ def plugin_e2e(a):
         return {"unavailable": "oracle/_ref/plugin_bench or the plugin library not built"}
     bits = {"k512_c0ffee": 512, "k1024_7": 1024, "k2048_7": 2048, "k3072_7": 3072}.get(a.key, 2048)
     env = dict(os.environ, LD_PRELOAD=plugin)
+    if devices:
+        # the drop-in plugin spread over a device group (sfxb_ctx_create_multi):
+        # row-sharded histograms reduced over NVLink peer memory in one kernel
+        env["SFXB_CUDA_DEVICES"] = devices
     try:
         out = subprocess.run([exe, str(a.rows), str(a.feats), str(a.bins), str(a.depth), str(bits), str(a.parties),
                               "2"], env=env, capture_output=True, text=True, timeout=600)
@@ -460,6 +464,9 @@ def run_ours(a):
     if world > 1:
         backend = os.environ.get("SFXB_DIST_BACKEND", "nccl")
         if backend == "nccl":
+            # communicator setup lines on stderr (nRanks per communicator)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
@@ -750,7 +757,7 @@ def run_ours(a):
 
     if rank != 0:
         if world > 1:
-            dist.barrier()
+            dist.barrier()  # rank 0 runs the device-group plugin arm meanwhile
             dist.destroy_process_group()
         return
     enc_per_s = E / enc_s * world
@@ -829,6 +836,11 @@ def run_ours(a):
     if world == 1 and not a.no_plugin_e2e:
         line["plugin_e2e"] = plugin_e2e(a)
         line["wire"] = wire_codec(a)
+    elif world > 1 and not a.no_plugin_e2e and os.environ.get("SFXB_DIST_BACKEND", "nccl") == "nccl":
+        # the drop-in plugin's own multi-GPU path: one process, the N GPUs of
+        # this job as a device group (the other ranks wait at the barrier)
+        torch.cuda.synchronize()
+        line["plugin_e2e_group"] = plugin_e2e(a, devices=",".join(str(i) for i in range(world)))
     if world == 1 and not a.no_cpu:
         try:
             line["cpu_baseline"] = cpu_baseline(a, n, nw, adds_tree_ref, threads=1)

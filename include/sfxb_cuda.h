@@ -125,6 +125,12 @@ int sfxb_encrypt_dev(sfxb_ctx *ctx, const int64_t *d_q_fixed, const uint32_t *d_
  * SFXB_OK and q = llround(ldexp(x, scale)), or SFXB_ERR_RANGE with the
  * reference's message. */
 int sfxb_encode_check(sfxb_ctx *ctx, double x, uint32_t scale_bits, int64_t *q_out);
+/* The same for `count` values on all host threads (encrypt_gh's encode of a
+ * whole GhPayload): q_out[i] for every value before the first failing one;
+ * *first_bad = index of the first value that fails (count when none) and the
+ * call returns SFXB_ERR_RANGE with that value's message. */
+int sfxb_encode_batch(sfxb_ctx *ctx, const double *x, size_t count, uint32_t scale_bits, int64_t *q_out,
+                      size_t *first_bad);
 
 /* ---- ciphertext addition (add_ciphertexts, he.cpp:117-121), batched -------- */
 int sfxb_add(sfxb_ctx *ctx, const uint32_t *a, const uint32_t *b, size_t count, uint32_t *out);

@@ -75,6 +75,7 @@ def load() -> C.CDLL:
         "sfxb_encrypt_dev": (C.c_int, [vp, vp, vp, sz, vp, vp]),
         "sfxb_encrypt_plain": (C.c_int, [vp, _u32p, _u32p, sz, _u32p, vp]),
         "sfxb_encode_check": (C.c_int, [vp, C.c_double, C.c_uint32, C.POINTER(C.c_int64)]),
+        "sfxb_encode_batch": (C.c_int, [vp, _f64p, C.c_size_t, C.c_uint32, _i64p, C.POINTER(C.c_size_t)]),
         "sfxb_add": (C.c_int, [vp, _u32p, _u32p, sz, _u32p]),
         "sfxb_accumulate": (C.c_int, [vp, _u32p, C.c_uint32, _u16p, C.c_uint32, _u32p, C.c_uint32, _u32p,
                                       C.c_uint32, _u32p, C.POINTER(C.c_uint64)]),
@@ -226,6 +227,16 @@ class Context:
         q = C.c_int64()
         self._check(self.lib.sfxb_encode_check(self.h, float(x), scale, C.byref(q)))
         return q.value
+
+    def encode_batch(self, x, scale: int = 40):
+        """encode_fixed of every value (sfxb_encode_batch): (q, first failing index or None)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        q = np.zeros(len(x), np.int64)
+        bad = C.c_size_t(0)
+        rc = self.lib.sfxb_encode_batch(self.h, x, len(x), scale, q, C.byref(bad))
+        if rc != SFXB_OK and bad.value >= len(x):
+            self._check(rc)
+        return q, (bad.value if rc != SFXB_OK else None)
 
     def encrypt(self, q_fixed, r):
         """q_fixed: int64[count]; r: uint32[count, n_words] -> uint32[count, ct_words]."""

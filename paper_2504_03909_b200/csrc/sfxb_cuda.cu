@@ -1648,6 +1648,20 @@ void accumulate_group(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *bins, uint3
     }
     const std::vector<size_t> jlo = split_even(spn, G);
     const uint32_t n_samples = g->n_samples;
+    // The reference lists each node's rows ascending (gbdt.cpp:157-180): then
+    // a shard's rows of a node are one contiguous run, found by two binary
+    // searches, and each shard touches only its own rows.  Otherwise every
+    // shard filters the whole frontier.
+    bool ascending = true;
+    for (uint32_t i = 0; i < N && ascending; ++i)
+        for (uint32_t t = offs[i] + 1; t < offs[i + 1]; ++t)
+            if (rows[t] <= rows[t - 1]) {
+                ascending = false;
+                break;
+            }
+    for (uint32_t i = 0; i < N && ascending; ++i)
+        if (offs[i + 1] > offs[i] && rows[offs[i + 1] - 1] >= n_samples)
+            throw ApiError(SFXB_ERR_ARG, "row index out of range in accumulate");
     // ---- phase 1: partial histograms of each shard's rows
     std::vector<const uint32_t *> part_ptr(G), real_ptr(G);
     for_shards(c, G, [&](size_t k, sfxb_ctx *sh) {
@@ -1655,10 +1669,16 @@ void accumulate_group(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *bins, uint3
         std::vector<uint32_t> loffs(N + 1, 0), lrows;
         lrows.reserve((size_t)offs[N] / G + 1024);
         for (uint32_t i = 0; i < N; ++i) {
-            for (uint32_t t = offs[i]; t < offs[i + 1]; ++t) {
-                const uint32_t row = rows[t];
-                if (row >= n_samples) throw ApiError(SFXB_ERR_ARG, "row index out of range in accumulate");
-                if (row >= lo && row < hi) lrows.push_back(row - lo);
+            if (ascending) {
+                const uint32_t *b = rows + offs[i], *e = rows + offs[i + 1];
+                for (const uint32_t *r = std::lower_bound(b, e, lo), *re = std::lower_bound(b, e, hi); r < re; ++r)
+                    lrows.push_back(*r - lo);
+            } else {
+                for (uint32_t t = offs[i]; t < offs[i + 1]; ++t) {
+                    const uint32_t row = rows[t];
+                    if (row >= n_samples) throw ApiError(SFXB_ERR_ARG, "row index out of range in accumulate");
+                    if (row >= lo && row < hi) lrows.push_back(row - lo);
+                }
             }
             loffs[i + 1] = (uint32_t)lrows.size();
         }
@@ -2140,6 +2160,54 @@ int sfxb_encode_check(sfxb_ctx *c, double x, uint32_t scale, int64_t *q_out) {
         if (host::cmp(twice, c->n) >= 0)
             throw ApiError(SFXB_ERR_RANGE, "encode_fixed: |x|·2^scale_bits must stay below n/2");
         *q_out = qv;
+    });
+}
+
+int sfxb_encode_batch(sfxb_ctx *c, const double *x, size_t count, uint32_t scale, int64_t *q_out,
+                      size_t *first_bad) {
+    return guard(c, [&] {
+        // encode_fixed's checks (he.cpp:125-136) per value, on all host
+        // threads; |q| <= 2^62 after the grid check, so 2|q| fits 64 bits and
+        // the n/2 bound is one compare against n's low word (or none when n
+        // is wider than 64 bits).
+        if (scale > 62) throw ApiError(SFXB_ERR_ARG, "encode: scale_bits above 62");
+        const double lim = std::ldexp(1.0, (int)(62 - scale));
+        const bool wide = host::bit_length(c->n) > 64;
+        const uint64_t n64 = wide ? ~0ull
+                                  : (uint64_t)(c->n.size() > 0 ? c->n[0] : 0) |
+                                        ((uint64_t)(c->n.size() > 1 ? c->n[1] : 0) << 32);
+        const unsigned T = (unsigned)std::max<size_t>(1, std::min<size_t>(std::thread::hardware_concurrency(),
+                                                                          count / 65536));
+        std::vector<size_t> bad(T, count);
+        std::vector<int> why(T, 0);
+        auto run = [&](unsigned t) {
+            const size_t lo = count * t / T, hi = count * (t + 1) / T;
+            for (size_t i = lo; i < hi; ++i) {
+                const double v = x[i];
+                if (!std::isfinite(v)) { bad[t] = i; why[t] = 1; return; }
+                if (std::abs(v) >= lim) { bad[t] = i; why[t] = 2; return; }
+                const int64_t qv = std::llround(std::ldexp(v, (int)scale));
+                const uint64_t mag = qv < 0 ? (uint64_t)(-(qv + 1)) + 1u : (uint64_t)qv;
+                if (!wide && 2 * mag >= n64) { bad[t] = i; why[t] = 3; return; }
+                q_out[i] = qv;
+            }
+        };
+        std::vector<std::thread> pool;
+        for (unsigned t = 1; t < T; ++t) pool.emplace_back(run, t);
+        run(0);
+        for (auto &th : pool) th.join();
+        size_t first = count;
+        int w = 0;
+        for (unsigned t = 0; t < T; ++t)
+            if (bad[t] < first) {
+                first = bad[t];
+                w = why[t];
+            }
+        if (first_bad) *first_bad = first;
+        if (first < count)
+            throw ApiError(SFXB_ERR_RANGE, w == 1   ? "encode_fixed: value must be finite"
+                                           : w == 2 ? "encode_fixed: value too large for the fixed-point grid"
+                                                    : "encode_fixed: |x|·2^scale_bits must stay below n/2");
     });
 }
 

@@ -306,20 +306,18 @@ public:
         out.n_samples = static_cast<std::uint32_t>(gh.size());
         const size_t count = 2 * gh.size();
         std::vector<int64_t> q(count);
-        // encode_fixed checks in the reference's order; on the first failure
-        // the reference has drawn one r per successful encryption before it
-        size_t ok = 0;
-        std::string fail_msg;
-        for (size_t i = 0; i < count; ++i) {
-            const double x = (i & 1) ? gh[i / 2].h : gh[i / 2].g;
-            int64_t v = 0;
-            if (sfxb_encode_check(ctx_, x, scale_bits_, &v) != SFXB_OK) {
-                fail_msg = sfxb_last_error(ctx_);
-                break;
-            }
-            q[i] = v;
-            ++ok;
+        // encode_fixed checks in the reference's order (g0, h0, g1, ...): the
+        // index of the first failure; the reference has drawn one r per
+        // successful encryption before it
+        std::vector<double> xs(count);
+        for (size_t i = 0; i < gh.size(); ++i) {
+            xs[2 * i] = gh[i].g;
+            xs[2 * i + 1] = gh[i].h;
         }
+        size_t ok = count;
+        std::string fail_msg;
+        if (count && sfxb_encode_batch(ctx_, xs.data(), count, scale_bits_, q.data(), &ok) != SFXB_OK)
+            fail_msg = sfxb_last_error(ctx_);
         PhaseTimer pt("encrypt_gh");
         pt.lap("encode");
         const size_t nw = n_words_;

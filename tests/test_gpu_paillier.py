@@ -285,3 +285,43 @@ def test_small_batch_decrypt_lanes_equal_one_lane(oracle, kname, monkeypatch):
         assert words_to_ints(p1) == ms
         for i in (0, count // 2, count - 1):
             assert ok.decrypt(cts[i]) == ms[i]
+
+
+@pytest.mark.parametrize("kname", ["toy35", "k512_c0ffee", "k2048_7"])
+def test_encode_batch_equals_encode_check(kname):
+    """sfxb_encode_batch (all host threads; encrypt_gh's encode) returns the
+    per-value sfxb_encode_check results (encode_fixed, he.cpp:125-136) and
+    stops at the first failing value with its message: non-finite, off the
+    fixed-point grid, or |q| >= n/2 (reachable with the toy key only)."""
+    n, p, q = (35, 5, 7) if kname == "toy35" else key(kname)
+    ctx = _lib.Context(n, p, q)
+    rng = np.random.default_rng(7)
+    if kname == "toy35":
+        x = rng.integers(-17, 18, 1000) * 2.0 ** -40
+    else:
+        x = np.concatenate([rng.uniform(-1, 1, 300_000), rng.uniform(0, 0.25, 300_000)])
+    want = np.array([ctx.encode_check(v) for v in x[:2000]], np.int64)
+    got, bad = ctx.encode_batch(x)
+    assert bad is None and np.array_equal(got[:2000], want)
+    cases = [(len(x) // 2 + 3, float("nan"), "finite"), (777 % len(x), 2.0 ** 30, "fixed-point grid"),
+             (len(x) - 1, -math.inf, "finite")]
+    if kname == "toy35":
+        cases.append((500, 18 * 2.0 ** -40, "below n/2"))  # 2·18 >= 35
+    for k, v, msg in cases:
+        y = x.copy()
+        y[k] = v
+        if k + 5 < len(y):
+            y[k + 5] = float("nan")  # a later failure must not win
+        q2, first = _encode_first_bad(ctx, y)
+        assert first == k and msg in ctx.lib.sfxb_last_error(ctx.h).decode()
+        assert np.array_equal(q2[:k], got[:k])
+
+
+def _encode_first_bad(ctx, y):
+    import ctypes as C
+
+    q = np.zeros(len(y), np.int64)
+    bad = C.c_size_t(0)
+    rc = ctx.lib.sfxb_encode_batch(ctx.h, np.ascontiguousarray(y), len(y), 40, q, C.byref(bad))
+    assert rc == _lib.SFXB_ERR_RANGE
+    return q, bad.value

@@ -1,8 +1,8 @@
 """SURVEY §8d config 4 microbenchmark: encrypt / add (fold into 256 bins) /
 decrypt throughput over batch sizes and key sizes on one B200.
 
-    python tools/microbench.py [--bits 1024 2048 3072] [--sizes 1024 16384 262144 4194304]
-                               [--max-seconds 20] > profiles/rNN_micro.jsonl
+    python tools/microbench.py [--bits 1024 2048 3072] [--sizes 1024 4096 ... 16777216]
+                               [--max-seconds 900] > profiles/rNN_micro.jsonl
 
 One JSON line per (op, bits, size): throughput from CUDA events on the
 context stream (inputs resident in HBM, warm-up call at the same size
@@ -43,9 +43,9 @@ def timed(stream, fn):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--bits", type=int, nargs="+", default=[1024, 2048, 3072])
-    ap.add_argument("--sizes", type=int, nargs="+", default=[1024, 16384, 262144, 4194304])
+    ap.add_argument("--sizes", type=int, nargs="+", default=[1 << k for k in range(10, 25, 2)])
     ap.add_argument("--ops", nargs="+", default=["enc", "enc_pub", "add", "add_pub", "dec"])
-    ap.add_argument("--max-seconds", type=float, default=20.0)
+    ap.add_argument("--max-seconds", type=float, default=900.0)
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     peak, mhz = _lib.imad_peak(0)
@@ -84,7 +84,8 @@ def main():
                     else:
                         fn = lambda: ops.encrypt(qf, r, k, cts, sync=False)  # noqa: E731
                         fam, unit_products = (1, prod_p2) if op == "enc" else (None, None)
-                    fn()  # warm-up at this size (scratch growth)
+                    if not rate or k / rate < 5:
+                        fn()  # warm-up at this size (scratch growth; long runs amortise it)
                     c.profile(True)
                     dt, res = timed(stream, fn)
                     stats = c.kernel_stats(fam) if fam is not None else None
@@ -103,7 +104,8 @@ def main():
                     out = torch.empty((256 * 2, cw), dtype=torch.int32, device=dev)
                     fn = lambda: ops.accumulate(gh, d_bins, 1, d_off, 1, d_rows, rows, 256, out,  # noqa: E731
                                                 sync=False)
-                    fn()
+                    if not rate or k / rate < 5:
+                        fn()
                     c.profile(True)
                     dt, res = timed(stream, fn)
                     stats = c.kernel_stats(0)
