@@ -295,7 +295,7 @@ def wire_codec(a):
     return res
 
 
-def plugin_e2e(a, devices=None):
+def plugin_e2e(a, devices=None, env_extra=None):
     """The reference-facing end to end: tools/plugin_bench.cpp drives the
     reference's EncryptionPlugin calls of one tree (encrypt_gh, accumulate_rows
     per level and party, decrypt_histogram per level and party) with the GPU
@@ -309,7 +309,7 @@ def plugin_e2e(a, devices=None):
     if not (os.path.exists(exe) and os.path.exists(plugin)):
         return {"unavailable": "oracle/_ref/plugin_bench or the plugin library not built"}
     bits = {"k512_c0ffee": 512, "k1024_7": 1024, "k2048_7": 2048, "k3072_7": 3072}.get(a.key, 2048)
-    env = dict(os.environ, LD_PRELOAD=plugin)
+    env = dict(os.environ, LD_PRELOAD=plugin, **(env_extra or {}))
     if devices:
         # the drop-in plugin spread over a device group (sfxb_ctx_create_multi):
         # row-sharded histograms reduced over NVLink peer memory in one kernel
@@ -835,6 +835,12 @@ def run_ours(a):
     }
     if world == 1 and not a.no_plugin_e2e:
         line["plugin_e2e"] = plugin_e2e(a)
+        # the same without the offline phase of encryption (blinding powers
+        # of the next encrypt_gh precomputed in the background)
+        off = plugin_e2e(a, env_extra={"SFXB_ENC_PRECOMPUTE": "0"})
+        line["plugin_e2e_no_precompute"] = {k: off.get(k) for k in (
+            "encrypt_gh_s", "accumulate_rows_s", "decrypt_histogram_s", "plugin_s_per_tree", "tree_wall_s",
+            "unavailable")}
         line["wire"] = wire_codec(a)
     elif world > 1 and not a.no_plugin_e2e and os.environ.get("SFXB_DIST_BACKEND", "nccl") == "nccl":
         # the drop-in plugin's own multi-GPU path: one process, the N GPUs of

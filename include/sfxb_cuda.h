@@ -121,6 +121,36 @@ int sfxb_encrypt_plain(sfxb_ctx *ctx, const uint32_t *m_words, const uint32_t *r
 int sfxb_encrypt_dev(sfxb_ctx *ctx, const int64_t *d_q_fixed, const uint32_t *d_r, size_t count,
                      uint32_t *d_out_cts, uint8_t *d_r_flags);
 
+/* ---- offline / online encryption ----------------------------------------
+ * The blinding power r^n mod n² of encrypt_with_r (he.cpp:87-99) does not
+ * depend on the plaintext, so it can be computed ahead of the call that
+ * needs it — e.g. while the host runs the protocol between trees — and the
+ * call then only does c = (1 + m·n)·r^n mod n² (3 multiplications mod n²
+ * instead of the exponentiation).  Ciphertexts are bit-identical as long as
+ * the queued powers are consumed in the order their r were drawn (the
+ * adapter draws them from the reference's HeRng stream, he.cpp:11-28).
+ * A queue lives on one device for one key; appends and encrypts may use
+ * different contexts of that key on that device (e.g. a low-priority
+ * background context).  Single-device contexts only. */
+typedef struct sfxb_blind sfxb_blind;
+int sfxb_blind_create(sfxb_ctx *ctx, size_t capacity, sfxb_blind **out);
+void sfxb_blind_free(sfxb_blind *b);
+size_t sfxb_blind_size(const sfxb_blind *b);
+/* append r_i^n mod n² for `count` host blinding factors (n_words limbs each,
+ * 1 < r < n); synchronous.  r_flags as sfxb_encrypt; on SFXB_ERR_COPRIME
+ * nothing is appended. */
+int sfxb_blind_append(sfxb_ctx *ctx, sfxb_blind *b, const uint32_t *r, size_t count, uint8_t *r_flags);
+/* drop the first `count` queued powers (their r were consumed elsewhere) */
+int sfxb_blind_pop(sfxb_blind *b, size_t count);
+/* c_i = (1 + m_i·n)·Y_i mod n² with Y_i the first `count` queued powers
+ * (consumed); m_i from q_fixed (as sfxb_encrypt) or m_words (as
+ * sfxb_encrypt_plain, with its range check) — exactly one of the two. */
+int sfxb_encrypt_blind(sfxb_ctx *ctx, sfxb_blind *b, const int64_t *q_fixed, const uint32_t *m_words, size_t count,
+                       uint32_t *out_cts);
+/* recreate the context's stream at the lowest priority (background work
+ * that should yield to other contexts' kernels at block boundaries) */
+int sfxb_ctx_set_low_priority(sfxb_ctx *ctx);
+
 /* encode_fixed's checks (he.cpp:125-136) without the mpz work: returns
  * SFXB_OK and q = llround(ldexp(x, scale)), or SFXB_ERR_RANGE with the
  * reference's message. */

@@ -245,14 +245,25 @@ __device__ __forceinline__ void mont_pow(uint32_t (&x)[S / TPI], const uint8_t *
                 bsrc = table + d * S;
             }
         }
-        uint32_t b[L];
-        if (square) {
-#pragma unroll
-            for (int k = 0; k < L; ++k) b[k] = acc[k];
+        if constexpr (TPI == 1) {
+            if (square) {
+                // symmetric products once (mont_sqr: 24% fewer at S = 32)
+                mont_sqr<S>(acc, acc, N, M.np);
+            } else {
+                uint32_t b[L];
+                load_lane<S, TPI>(b, bsrc);
+                mmul<S, TPI>(acc, acc, b, st, N, M.np);
+            }
         } else {
-            load_lane<S, TPI>(b, bsrc);
+            uint32_t b[L];
+            if (square) {
+#pragma unroll
+                for (int k = 0; k < L; ++k) b[k] = acc[k];
+            } else {
+                load_lane<S, TPI>(b, bsrc);
+            }
+            mmul<S, TPI>(acc, acc, b, st, N, M.np);
         }
-        mmul<S, TPI>(acc, acc, b, st, N, M.np);
         if (j < T) {
             store_lane<S, TPI>(table + j * S, acc);
             ++j;
@@ -306,14 +317,25 @@ __device__ __forceinline__ void mont_pow_ops(uint32_t (&x)[S / TPI], const uint8
                 bsrc = table + S * (d >> 1);
             }
         }
-        uint32_t b[L];
-        if (square) {
-#pragma unroll
-            for (int k = 0; k < L; ++k) b[k] = acc[k];
+        if constexpr (TPI == 1) {
+            if (square) {
+                // symmetric products once (mont_sqr: 24% fewer at S = 32)
+                mont_sqr<S>(acc, acc, N, M.np);
+            } else {
+                uint32_t b[L];
+                load_lane<S, TPI>(b, bsrc);
+                mmul<S, TPI>(acc, acc, b, st, N, M.np);
+            }
         } else {
-            load_lane<S, TPI>(b, bsrc);
+            uint32_t b[L];
+            if (square) {
+#pragma unroll
+                for (int k = 0; k < L; ++k) b[k] = acc[k];
+            } else {
+                load_lane<S, TPI>(b, bsrc);
+            }
+            mmul<S, TPI>(acc, acc, b, st, N, M.np);
         }
-        mmul<S, TPI>(acc, acc, b, st, N, M.np);
         if (j < T - 1) {
             if (j < 0) {
                 store_lane<S, TPI>(x2, acc);

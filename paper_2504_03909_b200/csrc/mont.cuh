@@ -510,6 +510,125 @@ __device__ __forceinline__ void mont_mul2(uint32_t (&r)[S / TPI], const uint32_t
     mont_tail<L, TPI, true>(r, X, Y, Z, N);
 }
 
+// ---------------------------------------------------------------- squaring (one lane per instance)
+//
+// r = a²·2^(−32S) mod M, CIOS with the symmetric products taken once: step i
+// adds a_i·(a_i·B^i + 2·Σ_{j>i} a_j·B^j) (relative positions j ≥ i of the
+// shifted accumulator) instead of a·a_i, then q_i·M and the shift as in
+// cios_step.  Requires a < M/2 (sqr_operand flips a to M − a otherwise:
+// (M − a)² ≡ a²), so 2a fits S limbs and each row stays below M·B — the
+// CIOS bound acc < 2M holds and the result is the same canonical residue as
+// mont_mul(a, a).  Products: S(S+1)/2 + S² + S instead of 2S² + S (24% fewer
+// at S = 32).  Positions j < i carry no product; there the shift of the odd
+// array is plain moves with carry (ALU pipe).  Fully unrolled (the row start
+// is a compile-time constant in every step).
+//
+// D[j] = limb j of 2a = (a_j << 1) | (a_{j−1} >> 31); the row's limb at
+// j = i + 1 is a_{i+1} << 1 (a_i's top bit belongs to position i... of 2a but
+// to no term of the row: 2·a_{i+1}·B^{i+1} has only a_{i+1}'s bits).
+template <int S>
+__device__ __forceinline__ uint32_t sqr_step(uint32_t (&E)[S], uint32_t (&Q)[S], uint32_t &Z, const uint32_t (&a)[S],
+                                             const uint32_t (&D)[S], const uint32_t (&N)[S], uint32_t np, const int i) {
+    const uint32_t bi = a[i];
+    auto op = [&](int j) -> uint32_t { return j == i ? a[i] : (j == i + 1 ? (a[j] << 1) : D[j]); };
+    uint32_t Zn;
+    // shift of the previous step fused with the odd products (j odd)
+    E[0] = add_cc(E[0], Q[1]);
+#pragma unroll
+    for (int k = 0; k < S / 2 - 1; ++k) {
+        if (2 * k + 1 < i) {
+            Q[2 * k] = addc_cc(Q[2 * k + 2], 0u);
+            Q[2 * k + 1] = addc_cc(Q[2 * k + 3], 0u);
+        } else {
+            madc_w_cc(Q[2 * k], Q[2 * k + 1], op(2 * k + 1), bi, Q[2 * k + 2], Q[2 * k + 3]);
+        }
+    }
+    madc_w_cc(Q[S - 2], Q[S - 1], op(S - 1), bi, 0u, 0u);
+    Zn = addc(0u, 0u);
+    Q[S - 1] = add_cc(Q[S - 1], Z);
+    Zn = addc(Zn, 0u);
+    // even products (j even, j >= i)
+    const int k0 = (i + 1) / 2;
+    if (k0 < S / 2) {
+        mad_w_cc(E[2 * k0], E[2 * k0 + 1], op(2 * k0), bi, E[2 * k0], E[2 * k0 + 1]);
+#pragma unroll
+        for (int k = k0 + 1; k < S / 2; ++k) madc_w_cc(E[2 * k], E[2 * k + 1], op(2 * k), bi, E[2 * k], E[2 * k + 1]);
+        Q[S - 1] = addc_cc(Q[S - 1], 0u);
+        Zn = addc(Zn, 0u);
+    }
+    const uint32_t q = E[0] * np;
+    mad_w_cc(Q[0], Q[1], N[1], q, Q[0], Q[1]);
+#pragma unroll
+    for (int k = 1; k < S / 2; ++k) madc_w_cc(Q[2 * k], Q[2 * k + 1], N[2 * k + 1], q, Q[2 * k], Q[2 * k + 1]);
+    Zn = addc(Zn, 0u);
+    mad_w_cc(E[0], E[1], N[0], q, E[0], E[1]);
+#pragma unroll
+    for (int k = 1; k < S / 2; ++k) madc_w_cc(E[2 * k], E[2 * k + 1], N[2 * k], q, E[2 * k], E[2 * k + 1]);
+    Q[S - 1] = addc_cc(Q[S - 1], 0u);
+    Z = addc(Zn, 0u);
+    return q;
+}
+
+// a' = min(a, M − a) for a < M (same square mod M, a' < M/2); returns
+// whether a was replaced
+template <int S>
+__device__ __forceinline__ bool sqr_operand(uint32_t (&r)[S], const uint32_t (&a)[S], const uint32_t (&N)[S]) {
+    uint32_t d[S];
+    d[0] = sub_cc(N[0], a[0]);
+#pragma unroll
+    for (int k = 1; k < S; ++k) d[k] = subc_cc(N[k], a[k]);
+    // M − a < a  <=>  a − (M − a) does not borrow and is nonzero; M odd, so
+    // a − (M − a) = 2a − M is never 0
+    uint32_t t = sub_cc(a[0], d[0]);
+#pragma unroll
+    for (int k = 1; k < S; ++k) t = subc_cc(a[k], d[k]);
+    const bool flip = (subc(0u, 0u) & 1u) == 0;
+    (void)t;
+#pragma unroll
+    for (int k = 0; k < S; ++k) r[k] = flip ? d[k] : a[k];
+    return flip;
+}
+
+// r = a²·2^(−32S) mod M (a < M); with `sub`, also V −= m (mod 2^(32S),
+// final borrow in `borrow`), m = Σ q_i·2^(32i) the pass's quotient, as
+// mont_mul_sub — for the operand actually squared (a or M − a, *flipped).
+// Returns ge (M subtracted at the end): a'·a' = (r + ge·M)·2^(32S) − m·M.
+template <int S>
+__device__ __forceinline__ bool mont_sqr_sub(uint32_t (&r)[S], uint32_t (&V)[S], const uint32_t (&a_in)[S],
+                                             const uint32_t (&N)[S], uint32_t np, bool sub, uint32_t &borrow,
+                                             bool &flipped) {
+    uint32_t a[S], D[S];
+    flipped = sqr_operand<S>(a, a_in, N);
+    D[0] = a[0] << 1;
+#pragma unroll
+    for (int k = 1; k < S; ++k) D[k] = (a[k] << 1) | (a[k - 1] >> 31);
+    uint32_t X[S], Y[S], Z = 0, bw = 0;
+#pragma unroll
+    for (int k = 0; k < S; ++k) X[k] = Y[k] = 0;
+#pragma unroll
+    for (int i = 0; i < S; i += 2) {
+        const uint32_t q0 = sqr_step<S>(X, Y, Z, a, D, N, np, i);
+        const uint32_t q1 = sqr_step<S>(Y, X, Z, a, D, N, np, i + 1);
+        if (sub) {
+            const uint64_t d0 = (uint64_t)V[i] - q0 - bw;
+            V[i] = (uint32_t)d0;
+            const uint64_t d1 = (uint64_t)V[i + 1] - q1 - (uint32_t)(d0 >> 63);
+            V[i + 1] = (uint32_t)d1;
+            bw = (uint32_t)(d1 >> 63);
+        }
+    }
+    borrow = bw;
+    return mont_tail<S, 1>(r, X, Y, Z, N);
+}
+
+template <int S>
+__device__ __forceinline__ void mont_sqr(uint32_t (&r)[S], const uint32_t (&a)[S], const uint32_t (&N)[S],
+                                         uint32_t np) {
+    uint32_t V[S], bw;
+    bool fl;
+    mont_sqr_sub<S>(r, V, a, N, np, false, bw, fl);
+}
+
 // ---------------------------------------------------------------- global <-> lane limbs
 
 template <int S, int TPI>

@@ -45,8 +45,36 @@ __device__ __forceinline__ void p2_mul(uint32_t (&A)[s / TPI], uint32_t (&B)[s /
     uint32_t v[L], x[L];
     bool ge = false;
     uint32_t bw = 0;
+    if constexpr (TPI == 1) {
+        if (square) {
+            // pass 0: v = 2·MM(A, B)
+            stage_b<s, TPI>(st, B);
+            {
+                uint32_t r[L], b;
+                mont_mul_sub<s, TPI>(r, v, A, st.sB, st.inst, N, np, false, b);
+                mod_add<s, TPI>(v, r, r, N);
+            }
+            // pass 1 squares A' = min(A, p − A) (mont_sqr_sub): t is the same,
+            // and its quotient m' satisfies ge·R − m ≡ ge'·R − m' + 2A (mod p)
+            // [A² = A'² + 2pA − p²], so 2A joins v when A was flipped
+            {
+                uint32_t t[L];
+                if (sqr_operand<s>(t, A, N)) {
+                    mod_add<s, TPI>(v, v, A, N);
+                    mod_add<s, TPI>(v, v, A, N);
+                }
+            }
+            uint32_t r[L], b;
+            bool fl;
+            ge = mont_sqr_sub<s>(r, v, A, N, np, true, b, fl);
+            bw = b;
+#pragma unroll
+            for (int k = 0; k < L; ++k) A[k] = r[k];
+        }
+    }
+    const bool generic = TPI > 1 || !square;
 #pragma unroll 1
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < (generic ? 2 : 0); ++c) {
         if (c == 0 && !square) {
             {
                 uint32_t tmp[L];

@@ -86,6 +86,15 @@ bool inv_mod_fast(const Big &x, const Big &M, Big &out) {
 } // namespace sfxb
 
 struct sfxb_ctx : CtxState {};
+// Queue of precomputed blinding powers r^n mod n² (device, 4s-limb stride),
+// in the order their r were drawn.
+struct sfxb_blind {
+    int device = 0;
+    uint32_t s = 0, nw = 0;
+    uint64_t key_id = 0;
+    uint32_t *d = nullptr;
+    size_t cap = 0, head = 0, size = 0; // live entries [head, head + size)
+};
 struct sfxb_gh {
     sfxb_ctx *ctx = nullptr;
     uint32_t *d = nullptr;     // 2·n_samples × 4s limbs, Montgomery form
@@ -2208,6 +2217,143 @@ int sfxb_encode_batch(sfxb_ctx *c, const double *x, size_t count, uint32_t scale
             throw ApiError(SFXB_ERR_RANGE, w == 1   ? "encode_fixed: value must be finite"
                                            : w == 2 ? "encode_fixed: value too large for the fixed-point grid"
                                                     : "encode_fixed: |x|·2^scale_bits must stay below n/2");
+    });
+}
+
+int sfxb_ctx_set_low_priority(sfxb_ctx *c) {
+    return guard(c, [&] {
+        if (is_group(c)) throw ApiError(SFXB_ERR_UNSUPPORTED, "stream priority: single-device contexts only");
+        CK(cudaSetDevice(c->device));
+        int least = 0, greatest = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        CK(cudaStreamSynchronize(c->stream));
+        cudaStream_t st = nullptr;
+        CK(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, least));
+        CK(cudaStreamDestroy(c->stream));
+        c->stream = st;
+    });
+}
+
+int sfxb_blind_create(sfxb_ctx *c, size_t capacity, sfxb_blind **out) {
+    return guard(c, [&] {
+        if (is_group(c)) throw ApiError(SFXB_ERR_UNSUPPORTED, "blinding queue: single-device contexts only");
+        CK(cudaSetDevice(c->device));
+        auto b = std::make_unique<sfxb_blind>();
+        b->device = c->device;
+        b->s = (uint32_t)c->s;
+        b->nw = c->nw;
+        b->key_id = c->key_id;
+        b->cap = capacity;
+        CK(cudaMalloc(&b->d, std::max<size_t>(capacity, 1) * 4 * (size_t)c->s * 4));
+        *out = b.release();
+    });
+}
+
+void sfxb_blind_free(sfxb_blind *b) {
+    if (!b) return;
+    cudaSetDevice(b->device);
+    cudaFree(b->d);
+    delete b;
+}
+
+size_t sfxb_blind_size(const sfxb_blind *b) { return b ? b->size : 0; }
+
+int sfxb_blind_append(sfxb_ctx *c, sfxb_blind *b, const uint32_t *r, size_t count, uint8_t *r_flags) {
+    return guard(c, [&] {
+        if (!b || b->key_id != c->key_id || b->device != c->device || is_group(c))
+            throw ApiError(SFXB_ERR_ARG, "blinding queue: another key or device");
+        if (count == 0) return;
+        // compact: live entries to the front when the tail has no room
+        const size_t S4 = 4 * (size_t)c->s;
+        CK(cudaSetDevice(c->device));
+        if (b->head + b->size + count > b->cap) {
+            if (b->size + count > b->cap) throw ApiError(SFXB_ERR_ARG, "blinding queue: capacity exceeded");
+            if (b->size)
+                CK(cudaMemcpyAsync(b->d, b->d + b->head * S4, b->size * S4 * 4, cudaMemcpyDeviceToDevice, c->stream));
+            b->head = 0;
+        }
+        // r^n mod n² = Enc(0, r): the encryption pipeline with plaintext 0
+        IoBuf<int64_t> dq(c->io[0], count);
+        CK(cudaMemsetAsync(dq.p, 0, count * 8, c->stream));
+        const size_t Sn = 2 * (size_t)c->s;
+        IoBuf<uint32_t> dr(c->io[1], count * Sn);
+        IoBuf<uint8_t> dflags(c->io[3], count);
+        CK(cudaMemsetAsync(dflags.p, 0, count, c->stream));
+        h2d_padded(c, dr.p, r, count, c->nw, Sn);
+        int st = SFXB_OK;
+        try {
+            encrypt_dev(c, dq.p, dr.p, count, b->d + (b->head + b->size) * S4, dflags.p);
+        } catch (const ApiError &e) {
+            if (e.code != SFXB_ERR_COPRIME) throw;
+            st = e.code;
+            c->err = e.what();
+        }
+        if (r_flags) {
+            CK(cudaMemcpyAsync(r_flags, dflags.p, count, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+        }
+        if (st != SFXB_OK) throw ApiError(st, c->err); // nothing appended
+        b->size += count;
+    });
+}
+
+int sfxb_blind_pop(sfxb_blind *b, size_t count) {
+    if (!b || count > b->size) return SFXB_ERR_ARG;
+    b->head += count;
+    b->size -= count;
+    if (b->size == 0) b->head = 0;
+    return SFXB_OK;
+}
+
+int sfxb_encrypt_blind(sfxb_ctx *c, sfxb_blind *b, const int64_t *q_fixed, const uint32_t *m_words, size_t count,
+                       uint32_t *out_cts) {
+    return guard(c, [&] {
+        if (!b || b->key_id != c->key_id || b->device != c->device || is_group(c))
+            throw ApiError(SFXB_ERR_ARG, "blinding queue: another key or device");
+        if (count > b->size) throw ApiError(SFXB_ERR_ARG, "blinding queue: fewer precomputed powers than requested");
+        if (!q_fixed == !m_words) throw ApiError(SFXB_ERR_ARG, "encrypt: exactly one of q_fixed / m_words");
+        if (count == 0) return;
+        CK(cudaSetDevice(c->device));
+        const size_t Sn = 2 * (size_t)c->s, S4 = 4 * (size_t)c->s;
+        if (m_words) {
+            const std::vector<uint32_t> nw_words = host::pad(c->n, c->nw);
+            for (size_t i = 0; i < count; ++i) {
+                const uint32_t *x = m_words + i * c->nw;
+                bool lt = false;
+                for (uint32_t k = c->nw; k-- > 0;)
+                    if (x[k] != nw_words[k]) {
+                        lt = x[k] < nw_words[k];
+                        break;
+                    }
+                if (!lt) throw ApiError(SFXB_ERR_RANGE, "encrypt: plaintext out of range [0, n)");
+            }
+        }
+        IoBuf<int64_t> dq(c->io[0], m_words ? 1 : count);
+        IoBuf<uint32_t> dm(c->io[4], m_words ? count * Sn : 1), dout(c->io[2], count * S4);
+        if (m_words) h2d_padded(c, dm.p, m_words, count, c->nw, Sn);
+        else CK(cudaMemcpyAsync(dq.p, q_fixed, count * 8, cudaMemcpyHostToDevice, c->stream));
+        // online step: c = (1 + m·n)·Y mod n² with Y the queued r^n mod n²
+        dev::EncArgs a{};
+        a.qfix = m_words ? nullptr : dq.p;
+        a.mw = m_words ? dm.p : nullptr;
+        a.count = count;
+        a.mod_n2 = arg(c->mod_n2);
+        a.n4 = c->d_n4;
+        a.nR_n2 = c->d_nR_n2;
+        a.y = b->d + b->head * S4;
+        a.out = dout.p;
+        dispatch_class(c->s, [&](auto sc) {
+            constexpr int cs = decltype(sc)::value;
+            using C = Cls<cs>;
+            auto k = dev::k_enc_combine<cs, C::TC>;
+            constexpr int NI = dev::kBlock / C::TC;
+            k<<<occupancy_grid(*c, k, count, NI), dev::kBlock, 0, c->stream>>>(a, 0);
+            check_launch(*c);
+        });
+        d2h_padded(c, out_cts, dout.p, count, 2 * c->nw, S4);
+        b->head += count;
+        b->size -= count;
+        if (b->size == 0) b->head = 0;
     });
 }
 

@@ -289,6 +289,9 @@ public:
                          (unsigned long long)counters_.decryptions,
                          (unsigned long long)sfxb_ctx_tree_derived(ctx_), (unsigned long long)sfxb_ctx_dec_derived(ctx_),
                          (unsigned long long)sfxb_ctx_launches(ctx_), sfxb_ctx_n_shards(ctx_));
+        stop_precompute();
+        if (blind_) sfxb_blind_free(blind_);
+        if (bg_ctx_) sfxb_ctx_destroy(bg_ctx_);
         if (gh_) sfxb_gh_free(gh_);
         if (ctx_) sfxb_ctx_destroy(ctx_);
         gmp_randclear(rng_);
@@ -321,40 +324,63 @@ public:
         PhaseTimer pt("encrypt_gh");
         pt.lap("encode");
         const size_t nw = n_words_;
-        if (ok == count && has_priv_ && count >= 2 * enc_chunk()) {
-            encrypt_gh_pipelined(q, out, pt);
-            return out;
-        }
-        uint32_t *r = pin_r_.get<uint32_t>(ok * nw);
-        draw_blinding(r, ok);
-        pt.lap("draw_r");
+        // blinding powers precomputed since the previous call (offline phase)
+        stop_precompute();
+        const size_t have = blind_ ? sfxb_blind_size(blind_) : 0;
+        pt.lap("join_precompute");
         if (ok < count) {
+            // the reference drew one r per successful encryption before the failure
+            consume_draws(ok);
             counters_.encryptions += 2 * (ok / 2); // pairs completed before the failure
             throw Error(fail_msg);
         }
-        uint32_t *cts = pin_cts_.get<uint32_t>(count * ct_words_);
-        std::vector<uint8_t> flags(count, 0);
-        int rc = sfxb_encrypt(ctx_, q.data(), r, count, cts, flags.data());
-        if (rc == SFXB_ERR_COPRIME) {
-            // some r shares a factor with n (probability ~2^-1000): redo the
-            // draw with the reference's exact rejection rule from the saved state
-            gmp_randclear(rng_);
-            gmp_randinit_set(rng_, rng_snapshot_);
-            draw_blinding(r, ok, /*exact_gcd=*/true);
-            rc = sfxb_encrypt(ctx_, q.data(), r, count, cts, nullptr);
-        }
-        check(rc);
-        pt.lap("gpu");
-        const hostpar::TopPadScope pad(count * ct_words_ * 4);
         out.cts.resize(count);
-        parallel_for(count, [&](size_t lo, size_t hi) {
-            for (size_t i = lo; i < hi; ++i) {
-                from_words(out.cts[i].value, &cts[i * ct_words_], ct_words_);
-                out.cts[i].key_id = pub_.key_id;
+        const size_t take = std::min(have, count);
+        uint32_t *cts = pin_cts_.get<uint32_t>(count * ct_words_);
+        const hostpar::TopPadScope pad(count * ct_words_ * 4);
+        auto marshal = [&](size_t lo, size_t hi) {
+            parallel_for(hi - lo, [&](size_t a, size_t b) {
+                for (size_t i = lo + a; i < lo + b; ++i) {
+                    from_words(out.cts[i].value, &cts[i * ct_words_], ct_words_);
+                    out.cts[i].key_id = pub_.key_id;
+                }
+            });
+        };
+        if (take) {
+            // online phase: c = (1 + m·n)·r^n mod n² with the queued powers
+            check(sfxb_encrypt_blind(ctx_, blind_, q.data(), nullptr, take, cts));
+            pt.lap("online");
+        }
+        if (take < count && has_priv_ && count - take >= 2 * enc_chunk()) {
+            std::thread m0;
+            if (take) m0 = std::thread(marshal, 0, take);
+            encrypt_gh_pipelined(q, out, take, pt);
+            if (m0.joinable()) m0.join();
+        } else {
+            if (take < count) {
+                const size_t rest = count - take;
+                uint32_t *r = pin_r_.get<uint32_t>(rest * nw);
+                draw_blinding(r, rest);
+                pt.lap("draw_r");
+                std::vector<uint8_t> flags(rest, 0);
+                int rc = sfxb_encrypt(ctx_, q.data() + take, r, rest, cts + take * ct_words_, flags.data());
+                if (rc == SFXB_ERR_COPRIME) {
+                    // some r shares a factor with n (probability ~2^-1000): redo the
+                    // draw with the reference's exact rejection rule from the saved state
+                    gmp_randclear(rng_);
+                    gmp_randinit_set(rng_, rng_snapshot_);
+                    draw_blinding(r, rest, /*exact_gcd=*/true);
+                    rc = sfxb_encrypt(ctx_, q.data() + take, r, rest, cts + take * ct_words_, nullptr);
+                }
+                check(rc);
+                pt.lap("gpu");
             }
-        });
+            marshal(0, count);
+        }
         counters_.encryptions += count;
         pt.lap("marshal");
+        // offline phase for the next call (the next tree encrypts as many)
+        start_precompute(count);
         return out;
     }
 
@@ -618,22 +644,27 @@ public:
             }
         } catch (...) {
             // the reference encrypted (drew r for) every vector packed before the failure
-            std::vector<uint32_t> r(plains.size() * n_words_);
-            draw_blinding(r.data(), plains.size());
+            consume_draws(plains.size());
             counters_.encryptions += 2 * done_nodes;
             throw;
         }
         const size_t count = plains.size();
-        std::vector<uint32_t> m(count * n_words_), r(count * n_words_), cts(count * ct_words_);
+        std::vector<uint32_t> m(count * n_words_), cts(count * ct_words_);
         for (size_t i = 0; i < count; ++i) to_words(plains[i], &m[i * n_words_], n_words_);
-        draw_blinding(r.data(), count);
-        if (count) {
-            int rc = sfxb_encrypt_plain(ctx_, m.data(), r.data(), count, cts.data(), nullptr);
+        // queued blinding powers first (the stream order), then fresh draws
+        stop_precompute();
+        const size_t take = std::min(blind_ ? sfxb_blind_size(blind_) : 0, count);
+        if (take) check(sfxb_encrypt_blind(ctx_, blind_, nullptr, m.data(), take, cts.data()));
+        if (count > take) {
+            const size_t rest = count - take;
+            std::vector<uint32_t> r(rest * n_words_);
+            draw_blinding(r.data(), rest);
+            int rc = sfxb_encrypt_plain(ctx_, &m[take * n_words_], r.data(), rest, &cts[take * ct_words_], nullptr);
             if (rc == SFXB_ERR_COPRIME) {
                 gmp_randclear(rng_);
                 gmp_randinit_set(rng_, rng_snapshot_);
-                draw_blinding(r.data(), count, /*exact_gcd=*/true);
-                rc = sfxb_encrypt_plain(ctx_, m.data(), r.data(), count, cts.data(), nullptr);
+                draw_blinding(r.data(), rest, /*exact_gcd=*/true);
+                rc = sfxb_encrypt_plain(ctx_, &m[take * n_words_], r.data(), rest, &cts[take * ct_words_], nullptr);
             }
             check(rc);
         }
@@ -659,6 +690,7 @@ public:
             counters_.encryptions += 2; // vector granularity
             out.nodes.push_back(std::move(nh));
         }
+        start_precompute(count); // offline phase for the next call
         return out;
     }
 
@@ -781,14 +813,14 @@ private:
                                                              : (size_t)262144;
         return c;
     }
-    void encrypt_gh_pipelined(const std::vector<int64_t> &q, GhPayload &out, PhaseTimer &pt) {
+    void encrypt_gh_pipelined(const std::vector<int64_t> &q, GhPayload &out, size_t first, PhaseTimer &pt) {
+        // elements [first, count); out.cts already sized, pin_cts_ holds the
+        // ciphertexts before `first`
         const size_t kEncChunk = enc_chunk();
-        const size_t count = q.size(), nw = n_words_, nch = (count + kEncChunk - 1) / kEncChunk;
-        uint32_t *r = pin_r_.get<uint32_t>(count * nw);
+        const size_t count = q.size(), nw = n_words_, nch = (count - first + kEncChunk - 1) / kEncChunk;
+        uint32_t *r = pin_r_.get<uint32_t>(count * nw); // indexed by element
         uint32_t *cts = pin_cts_.get<uint32_t>(count * ct_words_);
         std::vector<uint8_t> flags(count, 0);
-        const hostpar::TopPadScope pad(count * ct_words_ * 4);
-        out.cts.resize(count);
         struct Snap {
             gmp_randstate_t s;
             Snap() { gmp_randinit_mt(s); }
@@ -805,7 +837,7 @@ private:
             for (size_t k = 0; k < nch && !stop; ++k) {
                 gmp_randclear(snap[k]->s);
                 gmp_randinit_set(snap[k]->s, rng_);
-                const size_t lo = k * kEncChunk, hi = std::min(count, lo + kEncChunk);
+                const size_t lo = first + k * kEncChunk, hi = std::min(count, lo + kEncChunk);
                 for (size_t i = lo; i < hi; ++i) {
                     do mpz_urandomm(rv.get_mpz_t(), rng_, pub_.n.get_mpz_t());
                     while (rv <= 1); // gcd(r, n) is tested on the device
@@ -834,7 +866,7 @@ private:
                     std::unique_lock<std::mutex> lk(mu);
                     cv.wait(lk, [&] { return drawn > k; });
                 }
-                const size_t lo = k * kEncChunk, n = std::min(count, lo + kEncChunk) - lo;
+                const size_t lo = first + k * kEncChunk, n = std::min(count, lo + kEncChunk) - lo;
                 int rc = sfxb_encrypt(ctx_, &q[lo], r + lo * nw, n, cts + lo * ct_words_, flags.data() + lo);
                 if (rc == SFXB_ERR_COPRIME) {
                     stop = true;
@@ -860,7 +892,132 @@ private:
         if (drawer.joinable()) drawer.join();
         join_marshal();
         pt.lap("pipelined");
-        counters_.encryptions += count;
+    }
+
+    // ---------------------------------------------------------------- offline phase
+    //
+    // Blinding powers r^n mod n² do not depend on the plaintexts: after a
+    // call that encrypted `target` values, a background thread keeps drawing
+    // the next r of the HeRng stream (he.cpp:11-28, same rejection rules) and
+    // has a low-priority context on the same GPU append r^n mod n² to a
+    // device queue, chunk by chunk, until the queue holds `target` powers or
+    // the next call arrives.  The next call joins the thread (at a chunk
+    // boundary: the stream position then matches the queue exactly), encrypts
+    // the first min(queued, needed) values by the online step only, and draws
+    // the rest as before.  Every consumer of the stream (encrypt_gh,
+    // encrypt_histogram, the draws of a failing call) takes queued powers
+    // first, so the r sequence — and every ciphertext — is the reference's.
+    // SFXB_ENC_PRECOMPUTE=0 disables it; SFXB_ENC_PRECOMPUTE_CHUNK sets the
+    // chunk (default 16384).
+    static bool precompute_enabled() {
+        static const bool on = [] {
+            const char *e = std::getenv("SFXB_ENC_PRECOMPUTE");
+            return !(e && std::atoi(e) == 0);
+        }();
+        return on;
+    }
+    static size_t precompute_chunk() {
+        static const size_t c = std::getenv("SFXB_ENC_PRECOMPUTE_CHUNK")
+                                    ? (size_t)std::max(1L, std::atol(std::getenv("SFXB_ENC_PRECOMPUTE_CHUNK")))
+                                    : (size_t)16384;
+        return c;
+    }
+
+    void start_precompute(size_t target) {
+        if (!precompute_enabled() || !has_priv_ || target == 0 || sfxb_ctx_n_shards(ctx_) != 1) return;
+        if (!bg_ctx_) {
+            // a second context of the same key on the same device, low priority
+            std::vector<uint32_t> n(n_words_);
+            to_words(pub_.n, n.data(), n_words_);
+            size_t pw = (std::max(mpz_sizeinbase(priv_.p.get_mpz_t(), 2), mpz_sizeinbase(priv_.q.get_mpz_t(), 2)) + 31) / 32;
+            std::vector<uint32_t> p(pw), qq(pw);
+            to_words(priv_.p, p.data(), pw);
+            to_words(priv_.q, qq.data(), pw);
+            if (sfxb_ctx_create(&bg_ctx_, sfxb_ctx_shard_device(ctx_, 0), n.data(), (uint32_t)n_words_, p.data(),
+                                qq.data(), (uint32_t)pw) != SFXB_OK) {
+                bg_ctx_ = nullptr;
+                return;
+            }
+            sfxb_ctx_set_low_priority(bg_ctx_);
+        }
+        if (blind_ && sfxb_blind_size(blind_) == 0 && target > blind_cap_) {
+            sfxb_blind_free(blind_);
+            blind_ = nullptr;
+        }
+        if (!blind_) {
+            if (sfxb_blind_create(bg_ctx_, target, &blind_) != SFXB_OK) {
+                blind_ = nullptr;
+                return;
+            }
+            blind_cap_ = target;
+        }
+        const size_t goal = std::min(target, blind_cap_);
+        if (sfxb_blind_size(blind_) >= goal) return;
+        bg_stop_ = false;
+        bg_ = std::thread([this, goal] { precompute_loop(goal); });
+    }
+
+    void stop_precompute() {
+        if (!bg_.joinable()) return;
+        bg_stop_ = true;
+        bg_.join();
+        bg_stop_ = false;
+    }
+
+    // background thread: owns rng_ until joined
+    void precompute_loop(size_t goal) {
+        const size_t chunk = precompute_chunk(), nw = n_words_;
+        std::vector<uint32_t> r(chunk * nw);
+        std::vector<uint8_t> flags(chunk);
+        gmp_randstate_t snap;
+        gmp_randinit_mt(snap);
+        mpz_class rv, g;
+        while (!bg_stop_) {
+            const size_t have = sfxb_blind_size(blind_);
+            if (have >= goal) break;
+            const size_t k = std::min(chunk, goal - have);
+            gmp_randclear(snap);
+            gmp_randinit_set(snap, rng_);
+            for (size_t i = 0; i < k; ++i) {
+                do mpz_urandomm(rv.get_mpz_t(), rng_, pub_.n.get_mpz_t());
+                while (rv <= 1); // gcd(r, n) on the device
+                to_words(rv, &r[i * nw], nw);
+            }
+            int rc = sfxb_blind_append(bg_ctx_, blind_, r.data(), k, flags.data());
+            if (rc == SFXB_ERR_COPRIME) {
+                // redraw the chunk with the reference's exact rejection rule
+                gmp_randclear(rng_);
+                gmp_randinit_set(rng_, snap);
+                for (size_t i = 0; i < k; ++i) {
+                    for (;;) {
+                        mpz_urandomm(rv.get_mpz_t(), rng_, pub_.n.get_mpz_t());
+                        if (rv <= 1) continue;
+                        mpz_gcd(g.get_mpz_t(), rv.get_mpz_t(), pub_.n.get_mpz_t());
+                        if (g == 1) break;
+                    }
+                    to_words(rv, &r[i * nw], nw);
+                }
+                rc = sfxb_blind_append(bg_ctx_, blind_, r.data(), k, nullptr);
+            }
+            if (rc != SFXB_OK) {
+                // leave the stream where the queue ends; the next call draws on
+                gmp_randclear(rng_);
+                gmp_randinit_set(rng_, snap);
+                break;
+            }
+        }
+        gmp_randclear(snap);
+    }
+
+    // `count` draws of the stream taken and discarded (queued powers first)
+    void consume_draws(size_t count) {
+        stop_precompute();
+        const size_t have = blind_ ? sfxb_blind_size(blind_) : 0, take = std::min(have, count);
+        if (take) sfxb_blind_pop(blind_, take);
+        if (count > take) {
+            std::vector<uint32_t> r((count - take) * n_words_);
+            draw_blinding(r.data(), count - take);
+        }
     }
 
     // `count` draws of HeRng::unit_below(n) (he.cpp:19-28).  With p, q the
@@ -1447,6 +1604,12 @@ private:
     size_t n_words_ = 0, ct_words_ = 0;
     sfxb_gh *gh_ = nullptr;
     PinnedBuf pin_r_, pin_cts_, pin_slots_, pin_limbs_, pin_bins_; // page-locked marshalling buffers
+    // offline phase: background context, queue of blinding powers, worker
+    sfxb_ctx *bg_ctx_ = nullptr;
+    sfxb_blind *blind_ = nullptr;
+    size_t blind_cap_ = 0;
+    std::thread bg_;
+    std::atomic<bool> bg_stop_{false};
     // previous accumulate call (sibling-subtraction parents)
     bool prev_valid_ = false;
     uint64_t prev_bins_key_ = 0;

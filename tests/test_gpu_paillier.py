@@ -325,3 +325,50 @@ def _encode_first_bad(ctx, y):
     rc = ctx.lib.sfxb_encode_batch(ctx.h, np.ascontiguousarray(y), len(y), 40, q, C.byref(bad))
     assert rc == _lib.SFXB_ERR_RANGE
     return q, bad.value
+
+
+@pytest.mark.parametrize("kname", ["k512_c0ffee", "k2048_7"])
+def test_offline_online_encryption_is_bit_identical(oracle, kname):
+    """Blinding powers queued ahead (sfxb_blind_append on a low-priority
+    second context of the key) and consumed by the online step
+    (sfxb_encrypt_blind: c = (1 + m·n)·r^n mod n²) give exactly the
+    ciphertexts of sfxb_encrypt with the same r, for fixed-point and word
+    plaintexts; the queue is FIFO across appends, pops and partial takes."""
+    import ctypes as C
+
+    n, p, q = key(kname)
+    ctx = _lib.Context(n, p, q)
+    bg = _lib.Context(n, p, q)
+    assert bg.lib.sfxb_ctx_set_low_priority(bg.h) == 0
+    rng = random.Random(9)
+    count = 3000
+    qf = np.array([rng.randrange(-(1 << 41), 1 << 41) for _ in range(count)], np.int64)
+    r = ints_to_words([rng.randrange(2, n) for _ in range(count)], ctx.nw)
+    want = ctx.encrypt(qf, r)
+    b = C.c_void_p()
+    assert ctx.lib.sfxb_blind_create(bg.h, 2048, C.byref(b)) == 0
+    try:
+        assert bg.lib.sfxb_blind_append(bg.h, b, np.ascontiguousarray(r[:1500]).reshape(-1), 1500, None) == 0
+        got = np.zeros((count, ctx.ct_words), np.uint32)
+        assert ctx.lib.sfxb_encrypt_blind(ctx.h, b, qf[:700].ctypes.data, None, 700,
+                                          got[:700].reshape(-1)) == 0
+        assert ctx.lib.sfxb_blind_size(b) == 800
+        # append past the tail (compaction), then take the rest in one go
+        assert bg.lib.sfxb_blind_append(bg.h, b, np.ascontiguousarray(r[1500:2700]).reshape(-1), 1200, None) == 0
+        assert ctx.lib.sfxb_encrypt_blind(ctx.h, b, qf[700:2700].ctypes.data, None, 2000,
+                                          got[700:2700].reshape(-1)) == 0
+        assert np.array_equal(got[:2700], want[:2700])
+        # capacity and underflow are errors, nothing consumed
+        assert bg.lib.sfxb_blind_append(bg.h, b, np.ascontiguousarray(r[:300]).reshape(-1), 2100, None) != 0
+        assert ctx.lib.sfxb_encrypt_blind(ctx.h, b, qf.ctypes.data, None, 1, got[:1].reshape(-1)) != 0
+        # word plaintexts (the packed path) and pop
+        m = ints_to_words([rng.randrange(0, n) for _ in range(200)], ctx.nw)
+        want_m = ctx.encrypt_plain(m, r[2700:2900])
+        assert bg.lib.sfxb_blind_append(bg.h, b, np.ascontiguousarray(r[2600:2900]).reshape(-1), 300, None) == 0
+        assert ctx.lib.sfxb_blind_pop(b, 100) == 0
+        got_m = np.zeros((200, ctx.ct_words), np.uint32)
+        assert ctx.lib.sfxb_encrypt_blind(ctx.h, b, None, np.ascontiguousarray(m).ctypes.data, 200,
+                                          got_m.reshape(-1)) == 0
+        assert np.array_equal(got_m, want_m) and ctx.lib.sfxb_blind_size(b) == 0
+    finally:
+        ctx.lib.sfxb_blind_free(b)

@@ -10,6 +10,10 @@
 //
 //   plugin_bench [rows=1000000] [features_per_party=14] [bins=256] [depth=6] [bits=2048] [parties=2] [trees=1]
 // (with trees > 1 the last tree is reported; every tree encrypts afresh)
+// tree_wall_s: the reported tree from encrypt_gh to its last decrypt,
+// including the untimed host copies of the gradient payload to the passive
+// parties (the Bus's share of the reference loop) — the GPU adapter's
+// offline phase for the next encrypt_gh runs in the background meanwhile.
 //
 // Prints one JSON object.  Synthetic inputs: gh on the 2^-40 grid
 // (g in (-1, 1), h in [0, 0.25]), uniform bins, a full binary tree whose
@@ -90,7 +94,7 @@ int main(int argc, char **argv) {
         (void)w;
     }
 
-    double enc_s = 0, acc = 0, dec = 0;
+    double enc_s = 0, acc = 0, dec = 0, tree_wall = 0;
     std::string la, ld;
     uint64_t adds = 0, decs = 0;
     for (int tree = 0; tree < trees; ++tree) {
@@ -131,13 +135,14 @@ int main(int argc, char **argv) {
     la += "]";
     ld += "]";
     enc_s = secs(t0, t1);
+    tree_wall = secs(t0, Clock::now());
     }
     std::printf("{\"plugin\": \"%s\", \"rows\": %u, \"features_per_party\": %d, \"parties\": %d, \"bins\": %d, "
                 "\"depth\": %d, \"bits\": %u, \"encrypt_gh_s\": %.6f, \"encryptions_per_s\": %.1f, "
                 "\"accumulate_rows_s\": %.6f, \"accumulate_rows_s_per_level\": %s, \"ciphertext_additions\": %llu, "
                 "\"decrypt_histogram_s\": %.6f, \"decrypt_histogram_s_per_level\": %s, \"decryptions\": %llu, "
-                "\"plugin_s_per_tree\": %.6f, \"trees\": %d}\n",
+                "\"plugin_s_per_tree\": %.6f, \"tree_wall_s\": %.6f, \"trees\": %d}\n",
                 plug[0]->name().c_str(), rows, J, parties, K, D, bits, enc_s, 2.0 * rows / enc_s, acc, la.c_str(),
-                (unsigned long long)adds, dec, ld.c_str(), (unsigned long long)decs, enc_s + acc + dec, trees);
+                (unsigned long long)adds, dec, ld.c_str(), (unsigned long long)decs, enc_s + acc + dec, tree_wall, trees);
     return 0;
 }
