@@ -87,6 +87,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-plugin-e2e", action="store_true", help="skip the reference-facing plugin timing")
     ap.add_argument("--no-tree", action="store_true", help="disable sibling subtraction (direct histograms)")
+    ap.add_argument("--check", dest="check", action="store_true", default=True, help="(default) the self-check")
     ap.add_argument("--no-check", dest="check", action="store_false",
                     help="skip the bit-exact self-check (N=1: direct histograms of every level + sampled big-integer "
                          "slot products; N>1: rank 0 recomputes the sharded result from all rows on one GPU)")
@@ -300,8 +301,11 @@ def plugin_e2e(a, devices=None, env_extra=None):
     reference's EncryptionPlugin calls of one tree (encrypt_gh, accumulate_rows
     per level and party, decrypt_histogram per level and party) with the GPU
     adapter LD_PRELOADed over the unmodified reference library — host
-    marshalling of the reference's mpz payloads included.  Two trees, the
-    second reported (the first grows buffers)."""
+    marshalling of the reference's mpz payloads included.  Four trees, the
+    last reported (steady state: the first grows buffers; with the offline
+    phase each tree's blinding powers are precomputed during the previous
+    tree).  tree_wall_s includes the untimed host copies of the gradient
+    payload between the calls (the Bus's share of the reference loop)."""
     import subprocess
 
     exe = os.path.join(ROOT, "oracle", "_ref", "plugin_bench")
@@ -315,8 +319,11 @@ def plugin_e2e(a, devices=None, env_extra=None):
         # row-sharded histograms reduced over NVLink peer memory in one kernel
         env["SFXB_CUDA_DEVICES"] = devices
     try:
+        # four trees, the last reported: with the offline phase of encryption
+        # the last tree is in steady state (each tree's blinding powers are
+        # computed during the previous tree, sharing the GPU with it)
         out = subprocess.run([exe, str(a.rows), str(a.feats), str(a.bins), str(a.depth), str(bits), str(a.parties),
-                              "2"], env=env, capture_output=True, text=True, timeout=600)
+                              "4"], env=env, capture_output=True, text=True, timeout=900)
         res = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     except Exception as e:  # noqa: BLE001
         return {"unavailable": f"plugin_bench failed: {e}"}

@@ -198,6 +198,16 @@ __device__ __forceinline__ void from_mont(uint32_t (&r)[S / TPI], const uint32_t
     mmul<S, TPI>(r, x, one, st, N, np);
 }
 
+// squarings by mont_sqr (one lane per instance); SFXB_NO_SQR builds the
+// plain mont_mul(x, x) path (A/B runs)
+#ifndef SFXB_NO_SQR
+template <int TPI>
+constexpr bool kSqrPow = TPI == 1;
+#else
+template <int TPI>
+constexpr bool kSqrPow = false;
+#endif
+
 // Fixed-window exponentiation in the Montgomery domain:
 //   x <- x^e, e given as `nd` window digits of `w` bits, most significant first.
 // `table` = this instance's 2^w·S-word scratch in global memory (L2-resident).
@@ -245,7 +255,7 @@ __device__ __forceinline__ void mont_pow(uint32_t (&x)[S / TPI], const uint8_t *
                 bsrc = table + d * S;
             }
         }
-        if constexpr (TPI == 1) {
+        if constexpr (kSqrPow<TPI>) {
             if (square) {
                 // symmetric products once (mont_sqr: 24% fewer at S = 32)
                 mont_sqr<S>(acc, acc, N, M.np);
@@ -317,7 +327,7 @@ __device__ __forceinline__ void mont_pow_ops(uint32_t (&x)[S / TPI], const uint8
                 bsrc = table + S * (d >> 1);
             }
         }
-        if constexpr (TPI == 1) {
+        if constexpr (kSqrPow<TPI>) {
             if (square) {
                 // symmetric products once (mont_sqr: 24% fewer at S = 32)
                 mont_sqr<S>(acc, acc, N, M.np);

@@ -45,7 +45,12 @@ __device__ __forceinline__ void p2_mul(uint32_t (&A)[s / TPI], uint32_t (&B)[s /
     uint32_t v[L], x[L];
     bool ge = false;
     uint32_t bw = 0;
-    if constexpr (TPI == 1) {
+#ifndef SFXB_NO_SQR
+    constexpr bool kSqr = TPI == 1;
+#else
+    constexpr bool kSqr = false;
+#endif
+    if constexpr (kSqr) {
         if (square) {
             // pass 0: v = 2·MM(A, B)
             stage_b<s, TPI>(st, B);
@@ -72,7 +77,7 @@ __device__ __forceinline__ void p2_mul(uint32_t (&A)[s / TPI], uint32_t (&B)[s /
             for (int k = 0; k < L; ++k) A[k] = r[k];
         }
     }
-    const bool generic = TPI > 1 || !square;
+    const bool generic = !kSqr || !square;
 #pragma unroll 1
     for (int c = 0; c < (generic ? 2 : 0); ++c) {
         if (c == 0 && !square) {
