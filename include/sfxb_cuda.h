@@ -225,6 +225,18 @@ int sfxb_accumulate_tree_gh(sfxb_ctx *ctx, const sfxb_gh *gh, const uint16_t *bi
                             uint32_t n_bins, const int32_t *parent, uint32_t *out_slots,
                             uint64_t *additions);
 int sfxb_tree_reset(sfxb_ctx *ctx);
+/* Device-resident bin columns (n_features × n_samples u16, column-major,
+ * dataset.hpp:55-57): the reference's bins are fixed for a whole training
+ * run, so the adapter uploads them once (keyed on their content) instead of
+ * once per accumulate_rows call.  sfxb_accumulate_tree_bins is
+ * sfxb_accumulate_tree_gh with the handle's columns (feature count =
+ * the handle's).  Single-device contexts only. */
+typedef struct sfxb_bins sfxb_bins;
+int sfxb_bins_upload(sfxb_ctx *ctx, const uint16_t *bins, uint32_t n_features, uint32_t n_samples, sfxb_bins **out);
+void sfxb_bins_free(sfxb_bins *b);
+int sfxb_accumulate_tree_bins(sfxb_ctx *ctx, const sfxb_gh *gh, const sfxb_bins *bins, const uint32_t *node_offsets,
+                              uint32_t n_nodes, const uint32_t *rows, uint32_t n_bins, const int32_t *parent,
+                              uint32_t *out_slots, uint64_t *additions);
 /* number of frontier nodes obtained by sibling subtraction on this context */
 uint64_t sfxb_ctx_tree_derived(const sfxb_ctx *ctx);
 

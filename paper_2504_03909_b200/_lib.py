@@ -83,6 +83,10 @@ def load() -> C.CDLL:
         "sfxb_blind_pop": (C.c_int, [vp, C.c_size_t]),
         "sfxb_encrypt_blind": (C.c_int, [vp, vp, vp, vp, C.c_size_t, _u32p]),
         "sfxb_ctx_set_low_priority": (C.c_int, [vp]),
+        "sfxb_bins_upload": (C.c_int, [vp, _u16p, C.c_uint32, C.c_uint32, C.POINTER(vp)]),
+        "sfxb_bins_free": (None, [vp]),
+        "sfxb_accumulate_tree_bins": (C.c_int, [vp, vp, vp, _u32p, C.c_uint32, _u32p, C.c_uint32, _i32p, _u32p,
+                                                C.POINTER(C.c_uint64)]),
         "sfxb_add": (C.c_int, [vp, _u32p, _u32p, sz, _u32p]),
         "sfxb_accumulate": (C.c_int, [vp, _u32p, C.c_uint32, _u16p, C.c_uint32, _u32p, C.c_uint32, _u32p,
                                       C.c_uint32, _u32p, C.POINTER(C.c_uint64)]),
@@ -405,6 +409,30 @@ class DeviceOps:
         adds = C.c_uint64(0)
         self.ctx._check(self.ctx.lib.sfxb_accumulate_tree_gh(
             self.ctx.h, gh.h, bins.reshape(-1), J, np.ascontiguousarray(node_offsets, dtype=np.uint32), n_nodes,
+            np.ascontiguousarray(rows, dtype=np.uint32), n_bins, np.ascontiguousarray(parent, dtype=np.int32),
+            out.reshape(-1), C.byref(adds)))
+        return out, adds.value
+
+    def bins_upload(self, bins):
+        """Device-resident bin columns (sfxb_bins_upload); free with bins_free."""
+        bins = np.ascontiguousarray(bins, dtype=np.uint16)
+        h = C.c_void_p()
+        self.ctx._check(self.ctx.lib.sfxb_bins_upload(self.ctx.h, bins.reshape(-1), bins.shape[0], bins.shape[1],
+                                                      C.byref(h)))
+        return h
+
+    def bins_free(self, h):
+        self.ctx.lib.sfxb_bins_free(h)
+
+    def accumulate_tree_bins(self, gh: GhHandle, bins_h, n_features: int, node_offsets, rows, n_bins: int, parent,
+                             out=None):
+        """Tree-mode accumulate over resident gh and bins, host frontier and output."""
+        n_nodes = len(node_offsets) - 1
+        if out is None:
+            out = np.zeros((n_nodes * n_features * n_bins * 2, self.ctx.ct_words), np.uint32)
+        adds = C.c_uint64(0)
+        self.ctx._check(self.ctx.lib.sfxb_accumulate_tree_bins(
+            self.ctx.h, gh.h, bins_h, np.ascontiguousarray(node_offsets, dtype=np.uint32), n_nodes,
             np.ascontiguousarray(rows, dtype=np.uint32), n_bins, np.ascontiguousarray(parent, dtype=np.int32),
             out.reshape(-1), C.byref(adds)))
         return out, adds.value

@@ -198,9 +198,10 @@ __device__ __forceinline__ void from_mont(uint32_t (&r)[S / TPI], const uint32_t
     mmul<S, TPI>(r, x, one, st, N, np);
 }
 
-// squarings by mont_sqr (one lane per instance); SFXB_NO_SQR builds the
-// plain mont_mul(x, x) path (A/B runs)
-#ifndef SFXB_NO_SQR
+// squarings by mont_sqr (one lane per instance) in an SFXB_SQR build; the
+// default build squares with mont_mul(x, x): measured faster on the B200
+// (fewer products, but lower occupancy and more code)
+#ifdef SFXB_SQR
 template <int TPI>
 constexpr bool kSqrPow = TPI == 1;
 #else

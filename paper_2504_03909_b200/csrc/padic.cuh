@@ -45,8 +45,8 @@ __device__ __forceinline__ void p2_mul(uint32_t (&A)[s / TPI], uint32_t (&B)[s /
     uint32_t v[L], x[L];
     bool ge = false;
     uint32_t bw = 0;
-#ifndef SFXB_NO_SQR
-    constexpr bool kSqr = TPI == 1;
+#ifdef SFXB_SQR
+    constexpr bool kSqr = TPI == 1; // mont_sqr for the digit squarings (opt-in build)
 #else
     constexpr bool kSqr = false;
 #endif

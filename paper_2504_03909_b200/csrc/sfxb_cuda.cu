@@ -95,6 +95,12 @@ struct sfxb_blind {
     uint32_t *d = nullptr;
     size_t cap = 0, head = 0, size = 0; // live entries [head, head + size)
 };
+// Device-resident bin columns (n_features × n_samples u16, column-major)
+struct sfxb_bins {
+    const sfxb_ctx *ctx = nullptr;
+    uint32_t J = 0, n = 0;
+    uint16_t *d = nullptr;
+};
 struct sfxb_gh {
     sfxb_ctx *ctx = nullptr;
     uint32_t *d = nullptr;     // 2·n_samples × 4s limbs, Montgomery form
@@ -2571,6 +2577,53 @@ int sfxb_accumulate_tree_gh(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *bins,
         CK(cudaMemcpyAsync(doff.p, node_offsets, ((size_t)N + 1) * 4, cudaMemcpyHostToDevice, c->stream));
         if (R) CK(cudaMemcpyAsync(drows.p, rows, (size_t)R * 4, cudaMemcpyHostToDevice, c->stream));
         accumulate_dev(c, g, db.p, J, doff.p, N, drows.p, R, K, dout.p, 0, additions, parent, node_offsets);
+        d2h_padded(c, out_slots, dout.p, nslots, 2 * c->nw, S4);
+    });
+}
+
+int sfxb_bins_upload(sfxb_ctx *c, const uint16_t *bins, uint32_t n_features, uint32_t n_samples, sfxb_bins **out) {
+    return guard(c, [&] {
+        if (is_group(c)) throw ApiError(SFXB_ERR_UNSUPPORTED, "bins handle: single-device contexts only");
+        CK(cudaSetDevice(c->device));
+        auto b = std::make_unique<sfxb_bins>();
+        b->ctx = c;
+        b->J = n_features;
+        b->n = n_samples;
+        const size_t bytes = (size_t)n_features * n_samples * 2;
+        CK(cudaMalloc(&b->d, bytes + 16));
+        if (bytes) {
+            CK(cudaMemcpyAsync(b->d, bins, bytes, cudaMemcpyHostToDevice, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+        }
+        *out = b.release();
+    });
+}
+
+void sfxb_bins_free(sfxb_bins *b) {
+    if (!b) return;
+    cudaSetDevice(b->ctx->device);
+    cudaFree(b->d);
+    delete b;
+}
+
+int sfxb_accumulate_tree_bins(sfxb_ctx *c, const sfxb_gh *g, const sfxb_bins *b, const uint32_t *node_offsets,
+                              uint32_t N, const uint32_t *rows, uint32_t K, const int32_t *parent,
+                              uint32_t *out_slots, uint64_t *additions) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (!g || g->ctx != c) throw ApiError(SFXB_ERR_ARG, "accumulate: gradient handle belongs to another context");
+        if (!b || b->ctx != c) throw ApiError(SFXB_ERR_ARG, "accumulate: bins handle belongs to another context");
+        if (b->n != g->n_samples) throw ApiError(SFXB_ERR_ARG, "row-count mismatch between bins and gradients");
+        if (!parent) throw ApiError(SFXB_ERR_ARG, "accumulate_tree: parent indices required");
+        for (uint32_t i = 0; i < N; ++i)
+            if (node_offsets[i + 1] < node_offsets[i]) throw ApiError(SFXB_ERR_ARG, "accumulate: node offsets decrease");
+        if (N && node_offsets[0] != 0) throw ApiError(SFXB_ERR_ARG, "accumulate: node offsets must start at 0");
+        const uint32_t R = N ? node_offsets[N] : 0, J = b->J;
+        const size_t S4 = 4 * (size_t)c->s, nslots = 2ull * N * J * K;
+        IoBuf<uint32_t> doff(c->io[1], (size_t)N + 1), drows(c->io[2], R ? R : 1), dout(c->io[3], nslots * S4);
+        CK(cudaMemcpyAsync(doff.p, node_offsets, ((size_t)N + 1) * 4, cudaMemcpyHostToDevice, c->stream));
+        if (R) CK(cudaMemcpyAsync(drows.p, rows, (size_t)R * 4, cudaMemcpyHostToDevice, c->stream));
+        accumulate_dev(c, g, b->d, J, doff.p, N, drows.p, R, K, dout.p, 0, additions, parent, node_offsets);
         d2h_padded(c, out_slots, dout.p, nslots, 2 * c->nw, S4);
     });
 }

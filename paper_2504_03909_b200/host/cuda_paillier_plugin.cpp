@@ -143,6 +143,22 @@ void from_words(mpz_class &z, const uint32_t *w, size_t words) {
 
 // the reference implementation, for the out-of-scope packed path
 
+// ------------------------------------------------------------ foreground calls
+//
+// Plugin calls in flight in this process (every instance: the parties'
+// plugins share the GPU).  The offline phase launches its next chunk only
+// while none is — it fills the host's gaps between calls (the reference's
+// Bus, gradients, splits) instead of competing with the histogram and
+// decrypt kernels for the SMs.
+std::atomic<int> g_foreground{0};
+
+struct ForegroundCall {
+    ForegroundCall() { g_foreground.fetch_add(1); }
+    ~ForegroundCall() { g_foreground.fetch_sub(1); }
+    ForegroundCall(const ForegroundCall &) = delete;
+    ForegroundCall &operator=(const ForegroundCall &) = delete;
+};
+
 // ------------------------------------------------------------ packed vectors
 //
 // The horizontal path's plaintext packing (he.cpp:145-213), restated so the
@@ -293,6 +309,7 @@ public:
         if (blind_) sfxb_blind_free(blind_);
         if (bg_ctx_) sfxb_ctx_destroy(bg_ctx_);
         if (gh_) sfxb_gh_free(gh_);
+        if (bins_h_) sfxb_bins_free(bins_h_);
         if (ctx_) sfxb_ctx_destroy(ctx_);
         gmp_randclear(rng_);
     }
@@ -304,6 +321,7 @@ public:
 
     // ---- encrypt_gh (secure_processor.cpp:574-585)
     GhPayload encrypt_gh(std::span<const GHPair> gh) override {
+        const ForegroundCall fg;
         GhPayload out;
         out.encrypted = true;
         out.n_samples = static_cast<std::uint32_t>(gh.size());
@@ -408,6 +426,7 @@ public:
     HistogramPayload accumulate_rows(const GhPayload &gh, const std::vector<std::vector<std::uint16_t>> &bins,
                                      const std::vector<int> &feature_ids, const std::vector<NodeRows> &nodes,
                                      int n_bins) override {
+        const ForegroundCall fg;
         if (!gh.encrypted) throw Error("paillier accumulate expects encrypted gradients");
         if (gh.cts.size() != 2ull * gh.n_samples)
             throw Error("row-count mismatch: ciphertext count is not 2·n_samples");
@@ -443,8 +462,27 @@ public:
         const bool candidate = gh_ && gh_scan_key_ == scan.key && gh_count_ == gh.cts.size();
         if (!candidate) upload_gh(gh, scan.key);
         pt.lap("ensure_gh");
-        uint16_t *flat = pin_bins_.get<uint16_t>(J * gh.n_samples);
-        const uint64_t bins_key = stage_bins(bins, J, gh.n_samples, feature_ids, n_bins, flat);
+        // bins: exact change detection against the previous call's staged copy
+        const size_t nb_elems = J * gh.n_samples;
+        const void *before = pin_bins_.peek<void>();
+        uint16_t *flat = pin_bins_.get<uint16_t>(nb_elems);
+        const bool same_layout = flat == before && staged_J_ == J && staged_n_ == gh.n_samples && nb_elems;
+        const bool bins_changed = stage_bins(bins, J, gh.n_samples, flat, same_layout);
+        staged_J_ = J;
+        staged_n_ = gh.n_samples;
+        const bool same_bins = !bins_changed && staged_fids_ == feature_ids && staged_K_ == n_bins;
+        staged_fids_ = feature_ids;
+        staged_K_ = n_bins;
+        // the columns stay on the device across calls (the reference's bins are
+        // fixed for a training run); re-uploaded only when they change
+        const bool use_bins_handle = sfxb_ctx_n_shards(ctx_) == 1 && nb_elems;
+        if (use_bins_handle && (!bins_h_ || bins_changed || bins_h_J_ != J || bins_h_n_ != gh.n_samples)) {
+            if (bins_h_) sfxb_bins_free(bins_h_);
+            bins_h_ = nullptr;
+            check(sfxb_bins_upload(ctx_, flat, (uint32_t)J, gh.n_samples, &bins_h_));
+            bins_h_J_ = J;
+            bins_h_n_ = gh.n_samples;
+        }
         std::vector<uint32_t> offs(N + 1, 0), rows;
         for (size_t i = 0; i < N; ++i) offs[i + 1] = offs[i] + (uint32_t)nodes[i].rows.size();
         rows.reserve(offs[N]);
@@ -459,7 +497,7 @@ public:
             // merged rows of the pair equal its rows exactly and the features,
             // bins and gradients are those of the previous call.
             std::vector<int32_t> parent(N, -1);
-            if (allow_parents && prev_valid_ && prev_bins_key_ == bins_key && prev_gh_ == gh_) {
+            if (allow_parents && prev_valid_ && same_bins && prev_gh_ == gh_) {
                 size_t p = 0;
                 for (size_t i = 0; i + 1 < N && p < prev_rows_.size();) {
                     const auto &ra = nodes[i].rows, &rb = nodes[i + 1].rows;
@@ -476,6 +514,9 @@ public:
             }
             adds = 0;
             if (!(N && J && K)) return SFXB_OK;
+            if (use_bins_handle)
+                return sfxb_accumulate_tree_bins(ctx_, gh_, bins_h_, offs.data(), (uint32_t)N, rows.data(),
+                                                 (uint32_t)K, parent.data(), slots, &adds);
             return sfxb_accumulate_tree_gh(ctx_, gh_, flat, (uint32_t)J, offs.data(), (uint32_t)N, rows.data(),
                                            (uint32_t)K, parent.data(), slots, &adds);
         };
@@ -501,7 +542,6 @@ public:
         }
         check(rc);
         prev_valid_ = N && J && K;
-        prev_bins_key_ = bins_key;
         prev_gh_ = gh_;
         prev_rows_.resize(N);
         for (size_t i = 0; i < N; ++i) prev_rows_[i] = nodes[i].rows;
@@ -534,6 +574,7 @@ public:
 
     // ---- decrypt_histogram (secure_processor.cpp:679-719)
     std::vector<std::pair<std::uint32_t, Histogram>> decrypt_histogram(const HistogramPayload &payload) override {
+        const ForegroundCall fg;
         if (!has_priv_) throw AuthorizationError("decrypt requested without private key material");
         if (payload.layout != HistLayout::enc_scalar) {
             if (payload.layout == HistLayout::enc_packed) return decrypt_packed(payload);
@@ -617,6 +658,7 @@ public:
     // batch of encrypt_with_r over every packed plaintext, r drawn in the
     // reference's order (node: G vector, then H vector).
     HistogramPayload encrypt_histogram(const std::vector<std::pair<std::uint32_t, Histogram>> &node_hists) override {
+        const ForegroundCall fg;
         packing::validate(layout_);
         HistogramPayload out;
         out.layout = HistLayout::enc_packed;
@@ -698,6 +740,7 @@ public:
     // rules and counters in the reference's order; the ciphertext products of
     // each part run as one GPU batch (sfxb_add).
     HistogramPayload add_histograms(const std::vector<HistogramPayload> &parts) override {
+        const ForegroundCall fg;
         if (parts.empty()) throw Error("add_histograms: no inputs");
         HistogramPayload acc = parts[0];
         for (std::size_t p = 1; p < parts.size(); ++p) {
@@ -916,6 +959,13 @@ private:
         }();
         return on;
     }
+    static bool precompute_always() {
+        static const bool on = [] {
+            const char *e = std::getenv("SFXB_ENC_PRECOMPUTE");
+            return e && std::string(e) == "always";
+        }();
+        return on;
+    }
     static size_t precompute_chunk() {
         static const size_t c = std::getenv("SFXB_ENC_PRECOMPUTE_CHUNK")
                                     ? (size_t)std::max(1L, std::atol(std::getenv("SFXB_ENC_PRECOMPUTE_CHUNK")))
@@ -975,6 +1025,10 @@ private:
         while (!bg_stop_) {
             const size_t have = sfxb_blind_size(blind_);
             if (have >= goal) break;
+            // only between plugin calls (SFXB_ENC_PRECOMPUTE=always: also during them)
+            while (!precompute_always() && g_foreground.load() > 0 && !bg_stop_)
+                std::this_thread::sleep_for(std::chrono::microseconds(500));
+            if (bg_stop_) break;
             const size_t k = std::min(chunk, goal - have);
             gmp_randclear(snap);
             gmp_randinit_set(snap, rng_);
@@ -1055,37 +1109,29 @@ private:
         return i == a.size() && j == b.size();
     }
 
-    // The call's bin columns (J × n u16, column-major) copied into the
-    // page-locked staging buffer on all host threads, and their content key:
-    // FNV-1a over the per-block FNV-1a digests (blocks of kBinsBlock rows of
-    // one feature, in order), each computed on its block's copy.
+    // The call's bin columns (J × n u16, column-major) staged in the
+    // page-locked buffer `flat`, which still holds the previous call's
+    // columns: each block of kBinsBlock rows of one feature is compared with
+    // its staged copy on all host threads and copied only where it differs.
+    // Returns whether anything differs (exact: no hash) — `same_layout` says
+    // whether `flat` holds a previous call of the same J × n.
     static constexpr size_t kBinsBlock = size_t(1) << 18;
-    static uint64_t stage_bins(const std::vector<std::vector<uint16_t>> &bins, size_t J, size_t n,
-                               const std::vector<int> &fids, int n_bins, uint16_t *flat) {
-        constexpr uint64_t kBasis = 14695981039346656037ULL, kPrime = 1099511628211ULL;
+    static bool stage_bins(const std::vector<std::vector<uint16_t>> &bins, size_t J, size_t n, uint16_t *flat,
+                           bool same_layout) {
         const size_t per_f = (n + kBinsBlock - 1) / kBinsBlock, nb = J * per_f;
-        std::vector<uint64_t> dig(nb);
+        std::atomic<bool> changed{!same_layout};
         parallel_for(nb, [&](size_t lo, size_t hi) {
             for (size_t b = lo; b < hi; ++b) {
                 const size_t f = b / per_f, i0 = (b % per_f) * kBinsBlock, cnt = std::min(kBinsBlock, n - i0);
                 const uint16_t *src = bins[f].data() + i0;
-                std::memcpy(flat + f * n + i0, src, cnt * 2);
-                uint64_t h = kBasis;
-                size_t k = 0;
-                for (; k + 4 <= cnt; k += 4) {
-                    uint64_t w;
-                    std::memcpy(&w, src + k, 8);
-                    h = (h ^ w) * kPrime;
+                uint16_t *dst = flat + f * n + i0;
+                if (!same_layout || std::memcmp(dst, src, cnt * 2) != 0) {
+                    std::memcpy(dst, src, cnt * 2);
+                    changed = true;
                 }
-                for (; k < cnt; ++k) h = (h ^ src[k]) * kPrime;
-                dig[b] = h;
             }
         }, /*grain=*/2);
-        uint64_t h = kBasis ^ (uint64_t)n_bins;
-        for (int f : fids) h = (h ^ (uint32_t)f) * kPrime;
-        h = (h ^ (uint64_t)n) * kPrime;
-        for (uint64_t d : dig) h = (h ^ d) * kPrime;
-        return h;
+        return changed;
     }
 
     // ---------------------------------------------------------------- gh residency
@@ -1612,7 +1658,12 @@ private:
     std::atomic<bool> bg_stop_{false};
     // previous accumulate call (sibling-subtraction parents)
     bool prev_valid_ = false;
-    uint64_t prev_bins_key_ = 0;
+    // staged bin columns (pin_bins_) and their device copy
+    size_t staged_J_ = 0, staged_n_ = 0;
+    std::vector<int> staged_fids_;
+    int staged_K_ = -1;
+    sfxb_bins *bins_h_ = nullptr;
+    size_t bins_h_J_ = 0, bins_h_n_ = 0;
     const sfxb_gh *prev_gh_ = nullptr;
     std::vector<std::vector<std::uint32_t>> prev_rows_;
     // resident gh: pre-filter key, count, and its irregular ciphertexts

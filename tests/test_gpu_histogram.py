@@ -183,6 +183,17 @@ def test_tree_mode_sibling_subtraction_is_bit_exact(kname, shape):
         ops.accumulate_tree(gh, d_bins, J, d_off, offs, len(nodes), d_rows, len(rows), K,
                             np.array(parents, np.int32), out)
         assert np.array_equal(out.cpu().numpy().view(np.uint32), want)
+    # resident bin columns (sfxb_bins_upload / sfxb_accumulate_tree_bins) on a fresh cache
+    ops.tree_reset()
+    bh = ops.bins_upload(bins)
+    try:
+        for nodes, parents in levels:
+            offs, rows = frontier(nodes)
+            want, want_adds = ctx.accumulate(cw, bins, offs, rows, K)
+            got, adds = ops.accumulate_tree_bins(gh, bh, J, offs, rows, K, np.array(parents, np.int32))
+            assert np.array_equal(got, want) and adds == want_adds
+    finally:
+        ops.bins_free(bh)
 
 
 @pytest.mark.parametrize("kname,shape", [("k512_c0ffee", (400, 3, 8, 4)), ("k2048_7", (300, 2, 16, 3))])
