@@ -955,7 +955,7 @@ private:
     static bool precompute_enabled() {
         static const bool on = [] {
             const char *e = std::getenv("SFXB_ENC_PRECOMPUTE");
-            return !(e && std::atoi(e) == 0);
+            return !(e && std::string(e) == "0");
         }();
         return on;
     }
