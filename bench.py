@@ -772,10 +772,12 @@ def run_ours(a):
                     "crt_kernel_ms": k3t[1],
                     "pattern": "sfxb_decrypt_tree per party per level, host buffers (slots up, doubles down)"}
 
+    if world > 1:
+        # every rank is done with the GPUs: the other ranks leave, so rank 0's
+        # device-group plugin arm below has all GPUs to itself
+        dist.barrier()
+        dist.destroy_process_group()
     if rank != 0:
-        if world > 1:
-            dist.barrier()  # rank 0 runs the device-group plugin arm meanwhile
-            dist.destroy_process_group()
         return
     enc_per_s = E / enc_s * world
     dec_per_s = decs / dec_s * world
@@ -862,7 +864,7 @@ def run_ours(a):
         line["wire"] = wire_codec(a)
     elif world > 1 and not a.no_plugin_e2e and os.environ.get("SFXB_DIST_BACKEND", "nccl") == "nccl":
         # the drop-in plugin's own multi-GPU path: one process, the N GPUs of
-        # this job as a device group (the other ranks wait at the barrier)
+        # this job as a device group (the other ranks have finished)
         torch.cuda.synchronize()
         line["plugin_e2e_group"] = plugin_e2e(a, devices=",".join(str(i) for i in range(world)))
     if world == 1 and not a.no_cpu:
@@ -876,9 +878,6 @@ def run_ours(a):
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"]["paillier_rates_all_threads"] = {"unavailable": str(e)}
     print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
 
 
 def main():

@@ -155,6 +155,16 @@ int sfxb_ctx_set_low_priority(sfxb_ctx *ctx);
  * SFXB_OK and q = llround(ldexp(x, scale)), or SFXB_ERR_RANGE with the
  * reference's message. */
 int sfxb_encode_check(sfxb_ctx *ctx, double x, uint32_t scale_bits, int64_t *q_out);
+/* Gradients on the device: compute_gradients (gbdt.cpp:
+ * 69-80) from probabilities and 0/1 labels, quantize_gradients (:82-87) and
+ * encode_fixed (he.cpp:125-136) — d_q: 2n fixed-point plaintexts (g, h
+ * interleaved) for sfxb_encrypt_dev; d_gh (optional): the 2n quantized
+ * doubles.  Bit-identical to the reference's host arithmetic (one IEEE
+ * operation per step).  *first_bad = the first value failing encode_fixed's
+ * checks (2n when none; the call then returns SFXB_ERR_RANGE with its
+ * message).  Device pointers; synchronous. */
+int sfxb_gradients_dev(sfxb_ctx *ctx, const double *d_prob, const uint8_t *d_labels, size_t n, uint32_t scale_bits,
+                       int64_t *d_q, double *d_gh, size_t *first_bad);
 /* The same for `count` values on all host threads (encrypt_gh's encode of a
  * whole GhPayload): q_out[i] for every value before the first failing one;
  * *first_bad = index of the first value that fails (count when none) and the

@@ -264,6 +264,8 @@ class Reference:
                                              C.POINTER(C.c_double)]
         lib.ref_decrypt_threaded.argtypes = [_u32p, _u32p, C.c_size_t, _u32p, C.c_uint32, C.c_int,
                                              C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+        lib.ref_gradients.argtypes = [_f64p, np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS"), C.c_size_t,
+                                      C.c_uint, _u32p, C.c_size_t, _i64p, _f64p, C.POINTER(C.c_size_t)]
         lib.ref_train.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t, C.c_char_p, C.c_size_t,
                                   C.POINTER(C.c_uint64 * 4), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                   C.POINTER(C.c_double * 6)]

@@ -128,6 +128,40 @@ int ref_encrypt_with_r(const std::uint32_t *n, std::size_t nw, const std::uint32
     });
 }
 
+// compute_gradients + quantize_gradients (gbdt.cpp:69-87) + encode_fixed
+// (he.cpp:125-136) for each row, as the reference's loop feeds encrypt_gh:
+// q_out[2i], q_out[2i+1] = the signed fixed-point plaintexts of g_i, h_i
+// (m − n when m > n/2), gh_out = the quantized doubles.  Stops at the first
+// value encode_fixed rejects: returns -1 with the message, *first_bad = its index.
+int ref_gradients(const double *prob, const std::uint8_t *labels, std::size_t n, unsigned scale,
+                  const std::uint32_t *nwords, std::size_t nw, std::int64_t *q_out, double *gh_out,
+                  std::size_t *first_bad) {
+    *first_bad = 2 * n;
+    return guarded([&] {
+        PaillierPublicKey pk;
+        pk.n = from_words(nwords, nw);
+        pk.n2 = pk.n * pk.n;
+        std::vector<std::uint8_t> lab(labels, labels + n);
+        std::vector<double> pr(prob, prob + n);
+        std::vector<GHPair> gh = compute_gradients(lab, pr);
+        quantize_gradients(gh, scale);
+        const mpz_class half = pk.n / 2;
+        for (std::size_t i = 0; i < 2 * n; ++i) {
+            const double x = (i & 1) ? gh[i / 2].h : gh[i / 2].g;
+            gh_out[i] = x;
+            mpz_class m;
+            try {
+                m = encode_fixed(pk, x, scale);
+            } catch (...) {
+                *first_bad = i;
+                throw;
+            }
+            if (m > half) m -= pk.n;
+            q_out[i] = mpz_get_si(m.get_mpz_t());
+        }
+    });
+}
+
 // make_paillier_plugin (secure_processor.cpp:754-762); p == nullptr -> public half only.
 void *ref_plugin_new(const std::uint32_t *n, const std::uint32_t *p, const std::uint32_t *q,
                      std::size_t nw, std::uint64_t rng_seed, unsigned scale_bits) {

@@ -76,6 +76,7 @@ def load() -> C.CDLL:
         "sfxb_encrypt_plain": (C.c_int, [vp, _u32p, _u32p, sz, _u32p, vp]),
         "sfxb_encode_check": (C.c_int, [vp, C.c_double, C.c_uint32, C.POINTER(C.c_int64)]),
         "sfxb_encode_batch": (C.c_int, [vp, _f64p, C.c_size_t, C.c_uint32, _i64p, C.POINTER(C.c_size_t)]),
+        "sfxb_gradients_dev": (C.c_int, [vp, vp, vp, C.c_size_t, C.c_uint32, vp, vp, C.POINTER(C.c_size_t)]),
         "sfxb_blind_create": (C.c_int, [vp, C.c_size_t, C.POINTER(vp)]),
         "sfxb_blind_free": (None, [vp]),
         "sfxb_blind_size": (C.c_size_t, [vp]),

@@ -277,6 +277,70 @@ __global__ void __launch_bounds__(kBlock) k_enc_combine(EncArgs a, int crt) {
     }
 }
 
+// ------------------------------------------------------------------ gradients on the device
+//
+// compute_gradients (gbdt.cpp:69-80): g = p − y, h = p·(1 − p); quantize_gradients
+// (:82-87) = fixed_round (fixed_point.hpp:22-24) on the 2^-scale grid; then
+// encode_fixed's checks (he.cpp:125-136) and q = llround(ldexp(x, scale)) —
+// the plaintexts sfxb_encrypt_dev takes, G and H interleaved.  Every step is
+// one correctly rounded IEEE operation (explicit _rn intrinsics: no FMA
+// contraction), ldexp and llround are exact, so q is bit-identical to the
+// reference's host arithmetic.  The sigmoid that turns margins into p stays
+// with the caller (the reference's federation loop, federation.cpp:460-461):
+// libm exp is not reproducible bit for bit on the device.
+// status[0]: lowest failing index (count when none); status[1]: failure kind
+// (1 non-finite, 2 off the grid, 3 |q| >= n/2).
+struct GradArgs {
+    const double *prob;
+    const uint8_t *label;
+    size_t n;
+    int scale;
+    double lim;        // 2^(62 − scale)
+    uint64_t n64;      // n when n < 2^64 (toy keys), else 0 (no bound reachable)
+    int64_t *q;        // 2n
+    double *gh;        // optional 2n quantized (g, h)
+    unsigned long long *status;
+};
+
+__device__ __forceinline__ int encode_one(const GradArgs &a, double x, int64_t &q) {
+    if (!isfinite(x)) return 1;
+    if (fabs(x) >= a.lim) return 2;
+    q = llround(ldexp(x, a.scale));
+    const uint64_t mag = q < 0 ? (uint64_t)(-(q + 1)) + 1u : (uint64_t)q;
+    if (a.n64 && 2 * mag >= a.n64) return 3;
+    return 0;
+}
+
+// fixed_round (fixed_point.hpp:22-24) = ldexp((double)llround(ldexp(x, s)), −s),
+// with the host's llround for values outside int64 (NaN, |x|·2^s ≥ 2^63: the
+// x86-64 conversion yields INT64_MIN) so even garbage inputs fail the same way
+__device__ __forceinline__ double fixed_round_dev(double x, int s) {
+    const double y = ldexp(x, s);
+    const long long q = (isfinite(y) && fabs(y) < 9.223372036854775808e18) ? llround(y) : (long long)(1ull << 63);
+    return ldexp((double)q, -s);
+}
+
+__global__ void k_gradients(GradArgs a) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < a.n; i += (size_t)gridDim.x * blockDim.x) {
+        const double p = a.prob[i];
+        const double g = __dsub_rn(p, (double)a.label[i]);
+        const double h = __dmul_rn(p, __dsub_rn(1.0, p));
+        const double gq = fixed_round_dev(g, a.scale), hq = fixed_round_dev(h, a.scale);
+        if (a.gh) {
+            a.gh[2 * i] = gq;
+            a.gh[2 * i + 1] = hq;
+        }
+        int64_t q0 = 0, q1 = 0;
+        const int e0 = encode_one(a, gq, q0), e1 = e0 ? 0 : encode_one(a, hq, q1);
+        if (e0 || e1) {
+            const unsigned long long idx = e0 ? 2 * i : 2 * i + 1;
+            if (atomicMin(&a.status[0], idx) > idx) a.status[1] = (unsigned long long)(e0 ? e0 : e1);
+        }
+        a.q[2 * i] = q0;
+        a.q[2 * i + 1] = q1;
+    }
+}
+
 // ------------------------------------------------------------------ K3 decrypt (CRT)
 
 // decode_fixed (he.cpp:138-143) before the final ldexp: v = m − n if 2m > n,

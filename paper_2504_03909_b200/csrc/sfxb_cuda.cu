@@ -2178,6 +2178,42 @@ int sfxb_encode_check(sfxb_ctx *c, double x, uint32_t scale, int64_t *q_out) {
     });
 }
 
+int sfxb_gradients_dev(sfxb_ctx *c, const double *d_prob, const uint8_t *d_labels, size_t n, uint32_t scale,
+                       int64_t *d_q, double *d_gh, size_t *first_bad) {
+    return guard(c, [&] {
+        if (scale > 62) throw ApiError(SFXB_ERR_ARG, "gradients: scale_bits above 62");
+        CK(cudaSetDevice(c->device));
+        dev::GradArgs a{};
+        a.prob = d_prob;
+        a.label = d_labels;
+        a.n = n;
+        a.scale = (int)scale;
+        a.lim = std::ldexp(1.0, (int)(62 - scale));
+        a.n64 = host::bit_length(c->n) > 64
+                    ? 0
+                    : (uint64_t)(c->n.size() > 0 ? c->n[0] : 0) | ((uint64_t)(c->n.size() > 1 ? c->n[1] : 0) << 32);
+        a.q = d_q;
+        a.gh = d_gh;
+        unsigned long long *st = (unsigned long long *)grow(c->tmp[3], 64);
+        const unsigned long long init[2] = {2ull * n, 0ull};
+        CK(cudaMemcpyAsync(st, init, 16, cudaMemcpyHostToDevice, c->stream));
+        a.status = st;
+        if (n) {
+            const int grid = (int)std::min<size_t>((n + 255) / 256, (size_t)c->sms * 8);
+            dev::k_gradients<<<grid, 256, 0, c->stream>>>(a);
+            check_launch(*c);
+        }
+        unsigned long long h[2];
+        CK(cudaMemcpyAsync(h, st, 16, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (first_bad) *first_bad = (size_t)h[0];
+        if (h[0] < 2ull * n)
+            throw ApiError(SFXB_ERR_RANGE, h[1] == 1   ? "encode_fixed: value must be finite"
+                                           : h[1] == 2 ? "encode_fixed: value too large for the fixed-point grid"
+                                                       : "encode_fixed: |x|·2^scale_bits must stay below n/2");
+    });
+}
+
 int sfxb_encode_batch(sfxb_ctx *c, const double *x, size_t count, uint32_t scale, int64_t *q_out,
                       size_t *first_bad) {
     return guard(c, [&] {

@@ -83,6 +83,7 @@ typedef __gmp_randstate_struct gmp_randstate_t[1];
 #define mpz_abs __gmpz_abs
 #define mpz_neg __gmpz_neg
 #define mpz_get_d __gmpz_get_d
+#define mpz_get_si __gmpz_get_si
 #define mpz_get_str __gmpz_get_str
 #define mpz_sizeinbase __gmpz_sizeinbase
 #define mpz_size __gmpz_size
@@ -143,6 +144,7 @@ void mpz_fdiv_r_2exp(mpz_ptr, mpz_srcptr, mp_bitcnt_t);
 void mpz_abs(mpz_ptr, mpz_srcptr);
 void mpz_neg(mpz_ptr, mpz_srcptr);
 double mpz_get_d(mpz_srcptr);
+long mpz_get_si(mpz_srcptr);
 char *mpz_get_str(char *, int, mpz_srcptr);
 size_t mpz_sizeinbase(mpz_srcptr, int);
 size_t mpz_size(mpz_srcptr);

@@ -372,3 +372,69 @@ def test_offline_online_encryption_is_bit_identical(oracle, kname):
         assert np.array_equal(got_m, want_m) and ctx.lib.sfxb_blind_size(b) == 0
     finally:
         ctx.lib.sfxb_blind_free(b)
+
+
+@pytest.mark.parametrize("kname", ["toy35", "k2048_7"])
+def test_device_gradients_equal_reference(kname):
+    """sfxb_gradients_dev (compute_gradients + quantize_gradients + encode_fixed
+    on the device) against the reference's own functions (oracle/_ref
+    ref_gradients): the quantized doubles and the fixed-point plaintexts are
+    bit-identical, including probabilities at 0 and 1, values on rounding
+    boundaries of the 2^-40 grid, and the first failing value with its message
+    (NaN, off the grid, |q| >= n/2 for the toy key)."""
+    import ctypes as C
+
+    import torch
+
+    import py_oracle as po
+
+    if not po.reference_available():
+        pytest.skip("oracle/_ref not built")
+    ref = po.Reference()
+    n, p, q = (35, 5, 7) if kname == "toy35" else key(kname)
+    nw = max(1, (n.bit_length() + 31) // 32)
+    ctx = _lib.Context(n, p, q)
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(4)
+    N = 20000 if kname != "toy35" else 64
+    prob = rng.uniform(0, 1, N)
+    prob[:6] = [0.0, 1.0, 0.5, 0.5 + 2.0 ** -41, 0.25 + 2.0 ** -42, 1 - 2.0 ** -53]
+    if kname == "toy35":
+        prob = rng.integers(0, 9, N) * 2.0 ** -40  # |q| tiny, below n/2 = 17
+    lab = rng.integers(0, 2, N).astype(np.uint8)
+    if kname == "toy35":
+        lab[:] = 0
+
+    def run_ref(pr):
+        qo, gh, bad = np.zeros(2 * N, np.int64), np.zeros(2 * N), C.c_size_t()
+        rc = ref.lib.ref_gradients(pr, lab, N, 40, po.to_words(n, nw), nw, qo, gh, C.byref(bad))
+        return rc, qo, gh, bad.value, ref.lib.ref_last_error().decode() if rc else ""
+
+    def run_dev(pr):
+        d_q = torch.zeros(2 * N, dtype=torch.int64, device=dev)
+        d_gh = torch.zeros(2 * N, dtype=torch.float64, device=dev)
+        bad = C.c_size_t()
+        rc = ctx.lib.sfxb_gradients_dev(ctx.h, torch.from_numpy(pr).to(dev).data_ptr(),
+                                        torch.from_numpy(lab).to(dev).data_ptr(), N, 40, d_q.data_ptr(),
+                                        d_gh.data_ptr(), C.byref(bad))
+        torch.cuda.synchronize()
+        return rc, d_q.cpu().numpy(), d_gh.cpu().numpy(), bad.value, (
+            ctx.lib.sfxb_last_error(ctx.h).decode() if rc else "")
+
+    rc, q_ref, gh_ref, bad_ref, _ = run_ref(prob)
+    rc2, q_dev, gh_dev, bad_dev, _ = run_dev(prob)
+    assert rc == 0 and rc2 == 0 and bad_ref == bad_dev == 2 * N
+    assert np.array_equal(gh_ref.view(np.uint64), gh_dev.view(np.uint64))
+    assert np.array_equal(q_ref, q_dev)
+    cases = [(N // 2, float("nan")), (N // 3, 1e30)]
+    if kname == "toy35":
+        cases.append((7, 18 * 2.0 ** -40))  # g = p: q = 18, 2|q| >= 35
+    for k, v in cases:
+        pr = prob.copy()
+        pr[k] = v
+        rc, q_ref, gh_ref, bad_ref, msg_ref = run_ref(pr)
+        rc2, q_dev, gh_dev, bad_dev, msg_dev = run_dev(pr)
+        assert bad_ref == bad_dev and (rc != 0) == (rc2 != 0), (k, v, bad_ref, bad_dev)
+        if rc:
+            assert msg_ref.split(":")[-1].strip() in msg_dev
+            assert np.array_equal(q_ref[:bad_ref], q_dev[:bad_ref])
