@@ -414,8 +414,9 @@ def test_device_gradients_equal_reference(kname):
         d_q = torch.zeros(2 * N, dtype=torch.int64, device=dev)
         d_gh = torch.zeros(2 * N, dtype=torch.float64, device=dev)
         bad = C.c_size_t()
-        rc = ctx.lib.sfxb_gradients_dev(ctx.h, torch.from_numpy(pr).to(dev).data_ptr(),
-                                        torch.from_numpy(lab).to(dev).data_ptr(), N, 40, d_q.data_ptr(),
+        d_p, d_l = torch.from_numpy(pr).to(dev), torch.from_numpy(lab).to(dev)  # kept alive over the call
+        torch.cuda.synchronize()
+        rc = ctx.lib.sfxb_gradients_dev(ctx.h, d_p.data_ptr(), d_l.data_ptr(), N, 40, d_q.data_ptr(),
                                         d_gh.data_ptr(), C.byref(bad))
         torch.cuda.synchronize()
         return rc, d_q.cpu().numpy(), d_gh.cpu().numpy(), bad.value, (
