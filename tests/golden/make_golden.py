@@ -109,6 +109,7 @@ TRAIN_CONFIGS = {
 # tests/test_oracle.py) under the recording wrapper (oracle/record_plugin.cpp).
 SCALE_CONFIGS = {
     "vertical_c2_2048": ("vertical_c2_2048.ini", 2048, 7),
+    "vertical_c3_2048": ("vertical_c3_2048.ini", 2048, 7),
 }
 
 

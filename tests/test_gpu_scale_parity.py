@@ -1,4 +1,5 @@
-"""Drop-in parity on the metric's own configuration (BASELINE configs[1]):
+"""Drop-in parity on the metric's own configuration (BASELINE configs[1], and
+configs[2]):
 the reference's run_training (report.cpp:132) on 1M rows × 28 features, 256
 bins, depth 6, 2048-bit keygen(2048, 7), two trees, with the GPU adapter
 interposed on make_paillier_plugin — against the same run with the
@@ -24,24 +25,27 @@ sys.path.insert(0, os.path.join(HERE, "golden"))
 
 
 @pytest.mark.gpu
-def test_c2_training_loop_matches_integer_sum_oracle():
+@pytest.mark.parametrize("name", ["vertical_c2_2048", "vertical_c3_2048"])
+def test_training_loop_at_scale_matches_integer_sum_oracle(name):
+    """configs[1] (1M × 28, two parties) and configs[2] (284,807 × 30, three
+    parties called concurrently, fraud-like labels), 2048-bit, two trees."""
     from make_golden import SCALE_CONFIGS, run_recorded
 
     for p in (PLUGIN, os.path.join(REF, "librecord_plugin.so"), os.path.join(REF, "libsfxb_refcapi.so")):
         if not os.path.exists(p):
             pytest.skip(f"{p} not built")
-    want = json.load(open(os.path.join(HERE, "golden", "train_vertical_c2_2048_intsum.json")))
-    ini, bits, seed = SCALE_CONFIGS["vertical_c2_2048"]
+    want = json.load(open(os.path.join(HERE, "golden", f"train_{name}_intsum.json")))
+    ini, bits, seed = SCALE_CONFIGS[name]
     got = run_recorded(ini, bits, seed, PLUGIN, env={"SFXB_PLUGIN_VERBOSE": "1"}, timeout=1800)
     assert got["forest"] == want["forest"]
     assert got["partials"] == want["partials"]
     assert got["counters"][:3] == want["counters"]
-    assert len(got["records"]) == len(want["records"]) == 2
+    assert len(got["records"]) == len(want["records"]) >= 2
     for g, w in zip(got["records"], want["records"]):
         assert g["key"] == w["key"] and g["private"] == w["private"]
         assert g["counters"] == w["counters"]
         assert g["decrypt_calls"] == w["decrypt_calls"] and g["slots"] == w["slots"]
         assert g["per_call"] == w["per_call"]  # every decrypted histogram, call by call
         assert g["fnv"] == w["fnv"]
-    # the active party decrypted 12 histograms per tree (2 parties × 6 levels)
-    assert [r["decrypt_calls"] for r in got["records"]] == [24, 0]
+    # only the active party decrypts
+    assert [r["decrypt_calls"] > 0 for r in got["records"]] == [r["private"] for r in got["records"]]

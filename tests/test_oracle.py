@@ -214,15 +214,17 @@ def test_intsum_plugin_equals_cpu_paillier(name):
             assert x[k] == y[k], k
 
 
-def test_intsum_golden_at_c2_reproduces():
-    """tests/golden/train_vertical_c2_2048_intsum.json is what the oracle
-    plugin produces now (1M × 28, 2048-bit, depth 6, two trees; ≈30 s)."""
+@pytest.mark.parametrize("name", ["vertical_c2_2048", "vertical_c3_2048"])
+def test_intsum_golden_at_scale_reproduces(name):
+    """tests/golden/train_<name>_intsum.json is what the oracle plugin
+    produces now (configs[1]: 1M × 28, depth 6; configs[2]: 284,807 × 30,
+    3 parties threaded, depth 5; 2048-bit, two trees)."""
     sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
     from make_golden import SCALE_CONFIGS, run_recorded
 
     intsum = _scale_libs()
-    want = json.load(open(os.path.join(ROOT, "tests", "golden", "train_vertical_c2_2048_intsum.json")))
-    ini, bits, seed = SCALE_CONFIGS["vertical_c2_2048"]
+    want = json.load(open(os.path.join(ROOT, "tests", "golden", f"train_{name}_intsum.json")))
+    ini, bits, seed = SCALE_CONFIGS[name]
     got = run_recorded(ini, bits, seed, intsum)
     assert got["forest"] == want["forest"] and got["partials"] == want["partials"]
     assert got["counters"][:3] == want["counters"]
