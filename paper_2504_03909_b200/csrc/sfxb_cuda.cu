@@ -16,6 +16,7 @@
 #include <exception>
 
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/sfxb_cuda.h"
 #include "bignum_host.hpp"
@@ -132,6 +133,15 @@ struct ApiError : std::runtime_error {
         if (e_ != cudaSuccess)                                                                     \
             throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));                      \
     } while (0)
+
+// NVTX range over one C ABI call (visible in Nsight Systems / ncu NVTX
+// filters; header-only NVTX 3, no cost without an attached tool)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 template <typename F>
 int guard(sfxb_ctx *ctx, F &&f) {
@@ -2180,6 +2190,7 @@ int sfxb_encode_check(sfxb_ctx *c, double x, uint32_t scale, int64_t *q_out) {
 
 int sfxb_gradients_dev(sfxb_ctx *c, const double *d_prob, const uint8_t *d_labels, size_t n, uint32_t scale,
                        int64_t *d_q, double *d_gh, size_t *first_bad) {
+    const NvtxRange nvtx_("sfxb_gradients_dev");
     return guard(c, [&] {
         if (scale > 62) throw ApiError(SFXB_ERR_ARG, "gradients: scale_bits above 62");
         CK(cudaSetDevice(c->device));
@@ -2216,6 +2227,7 @@ int sfxb_gradients_dev(sfxb_ctx *c, const double *d_prob, const uint8_t *d_label
 
 int sfxb_encode_batch(sfxb_ctx *c, const double *x, size_t count, uint32_t scale, int64_t *q_out,
                       size_t *first_bad) {
+    const NvtxRange nvtx_("sfxb_encode_batch");
     return guard(c, [&] {
         // encode_fixed's checks (he.cpp:125-136) per value, on all host
         // threads; |q| <= 2^62 after the grid check, so 2|q| fits 64 bits and
@@ -2301,6 +2313,7 @@ void sfxb_blind_free(sfxb_blind *b) {
 size_t sfxb_blind_size(const sfxb_blind *b) { return b ? b->size : 0; }
 
 int sfxb_blind_append(sfxb_ctx *c, sfxb_blind *b, const uint32_t *r, size_t count, uint8_t *r_flags) {
+    const NvtxRange nvtx_("sfxb_blind_append");
     return guard(c, [&] {
         if (!b || b->key_id != c->key_id || b->device != c->device || is_group(c))
             throw ApiError(SFXB_ERR_ARG, "blinding queue: another key or device");
@@ -2349,6 +2362,7 @@ int sfxb_blind_pop(sfxb_blind *b, size_t count) {
 
 int sfxb_encrypt_blind(sfxb_ctx *c, sfxb_blind *b, const int64_t *q_fixed, const uint32_t *m_words, size_t count,
                        uint32_t *out_cts) {
+    const NvtxRange nvtx_("sfxb_encrypt_blind");
     return guard(c, [&] {
         if (!b || b->key_id != c->key_id || b->device != c->device || is_group(c))
             throw ApiError(SFXB_ERR_ARG, "blinding queue: another key or device");
@@ -2401,6 +2415,7 @@ int sfxb_encrypt_blind(sfxb_ctx *c, sfxb_blind *b, const int64_t *q_fixed, const
 
 int sfxb_encrypt_dev(sfxb_ctx *c, const int64_t *d_q, const uint32_t *d_r, size_t count, uint32_t *d_out,
                      uint8_t *d_flags) {
+    const NvtxRange nvtx_("sfxb_encrypt_dev");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
         encrypt_dev(c, d_q, d_r, count, d_out, d_flags);
@@ -2410,6 +2425,7 @@ int sfxb_encrypt_dev(sfxb_ctx *c, const int64_t *d_q, const uint32_t *d_r, size_
 
 int sfxb_encrypt(sfxb_ctx *c, const int64_t *q_fixed, const uint32_t *r, size_t count, uint32_t *out_cts,
                  uint8_t *r_flags) {
+    const NvtxRange nvtx_("sfxb_encrypt");
     return guard(c, [&] {
         if (is_group(c)) encrypt_group(c, q_fixed, nullptr, r, count, out_cts, r_flags);
         else encrypt_host(c, q_fixed, nullptr, r, count, out_cts, r_flags);
@@ -2418,6 +2434,7 @@ int sfxb_encrypt(sfxb_ctx *c, const int64_t *q_fixed, const uint32_t *r, size_t 
 
 int sfxb_encrypt_plain(sfxb_ctx *c, const uint32_t *m_words, const uint32_t *r, size_t count, uint32_t *out_cts,
                        uint8_t *r_flags) {
+    const NvtxRange nvtx_("sfxb_encrypt_plain");
     return guard(c, [&] {
         if (is_group(c)) encrypt_group(c, nullptr, m_words, r, count, out_cts, r_flags);
         else encrypt_host(c, nullptr, m_words, r, count, out_cts, r_flags);
@@ -2425,6 +2442,7 @@ int sfxb_encrypt_plain(sfxb_ctx *c, const uint32_t *m_words, const uint32_t *r, 
 }
 
 int sfxb_add(sfxb_ctx *c, const uint32_t *a, const uint32_t *b, size_t count, uint32_t *out) {
+    const NvtxRange nvtx_("sfxb_add");
     return guard(c, [&] {
         if (is_group(c)) add_group(c, a, b, count, out);
         else add_host(c, a, b, count, out);
@@ -2433,6 +2451,7 @@ int sfxb_add(sfxb_ctx *c, const uint32_t *a, const uint32_t *b, size_t count, ui
 
 int sfxb_decrypt_dev(sfxb_ctx *c, const uint32_t *d_cts, size_t count, uint32_t scale, double *d_values,
                      uint32_t *d_plain, uint64_t *decryptions) {
+    const NvtxRange nvtx_("sfxb_decrypt_dev");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
         decrypt_dev(c, d_cts, count, scale, d_values, d_plain, decryptions);
@@ -2441,6 +2460,7 @@ int sfxb_decrypt_dev(sfxb_ctx *c, const uint32_t *d_cts, size_t count, uint32_t 
 
 int sfxb_decrypt_tree(sfxb_ctx *c, uint64_t tag, const uint32_t *cts, uint32_t n_nodes, uint32_t spn,
                       const int32_t *parent, uint32_t scale, double *out_values, uint64_t *decryptions) {
+    const NvtxRange nvtx_("sfxb_decrypt_tree");
     return guard(c, [&] {
         if (is_group(c)) decrypt_tree_group(c, tag, cts, n_nodes, spn, parent, scale, out_values, decryptions);
         else decrypt_tree_impl(c, tag, cts, n_nodes, spn, 0, spn, parent, scale, out_values, decryptions);
@@ -2449,6 +2469,7 @@ int sfxb_decrypt_tree(sfxb_ctx *c, uint64_t tag, const uint32_t *cts, uint32_t n
 
 int sfxb_decrypt(sfxb_ctx *c, const uint32_t *cts, size_t count, uint32_t scale, double *out_values,
                  uint32_t *out_plain, uint64_t *decryptions) {
+    const NvtxRange nvtx_("sfxb_decrypt");
     return guard(c, [&] {
         if (is_group(c)) decrypt_group(c, cts, count, scale, out_values, out_plain, decryptions);
         else decrypt_host(c, cts, count, scale, out_values, out_plain, decryptions);
@@ -2456,6 +2477,7 @@ int sfxb_decrypt(sfxb_ctx *c, const uint32_t *cts, size_t count, uint32_t scale,
 }
 
 int sfxb_gh_upload(sfxb_ctx *c, const uint32_t *gh_cts, uint32_t n_samples, sfxb_gh **out) {
+    const NvtxRange nvtx_("sfxb_gh_upload");
     return guard(c, [&] {
         if (is_group(c)) {
             *out = gh_upload_group(c, gh_cts, n_samples);
@@ -2470,6 +2492,7 @@ int sfxb_gh_upload(sfxb_ctx *c, const uint32_t *gh_cts, uint32_t n_samples, sfxb
 }
 
 int sfxb_gh_from_dev(sfxb_ctx *c, const uint32_t *d_gh, uint32_t n_samples, sfxb_gh **out) {
+    const NvtxRange nvtx_("sfxb_gh_from_dev");
     return guard(c, [&] {
         if (is_group(c)) throw ApiError(SFXB_ERR_UNSUPPORTED, "gh_from_dev: device-pointer entry points are single-device");
         CK(cudaSetDevice(c->device));
@@ -2510,6 +2533,7 @@ void sfxb_gh_free(sfxb_gh *g) {
 int sfxb_accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, uint32_t n_features,
                         const uint32_t *d_node_offsets, uint32_t n_nodes, const uint32_t *d_rows, uint32_t n_rows,
                         uint32_t n_bins, uint32_t *d_out, int mont_out, uint64_t *additions) {
+    const NvtxRange nvtx_("sfxb_accumulate_dev");
     return guard(c, [&] {
         if (g && !g->parts.empty())
             throw ApiError(SFXB_ERR_UNSUPPORTED, "accumulate: device-pointer entry points take a single-device handle");
@@ -2522,6 +2546,7 @@ int sfxb_accumulate_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bins, u
 int sfxb_accumulate(sfxb_ctx *c, const uint32_t *gh_cts, uint32_t n_samples, const uint16_t *bins, uint32_t J,
                     const uint32_t *node_offsets, uint32_t N, const uint32_t *rows, uint32_t K, uint32_t *out_slots,
                     uint64_t *additions) {
+    const NvtxRange nvtx_("sfxb_accumulate");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
         for (uint32_t i = 0; i < N; ++i)
@@ -2553,6 +2578,7 @@ int sfxb_accumulate(sfxb_ctx *c, const uint32_t *gh_cts, uint32_t n_samples, con
 
 int sfxb_accumulate_gh(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *bins, uint32_t J, const uint32_t *node_offsets,
                        uint32_t N, const uint32_t *rows, uint32_t K, uint32_t *out_slots, uint64_t *additions) {
+    const NvtxRange nvtx_("sfxb_accumulate_gh");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
         if (!g || g->ctx != c) throw ApiError(SFXB_ERR_ARG, "accumulate: gradient handle belongs to another context");
@@ -2580,6 +2606,7 @@ int sfxb_accumulate_tree_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bi
                              const uint32_t *d_node_offsets, const uint32_t *h_node_offsets, uint32_t n_nodes,
                              const uint32_t *d_rows, uint32_t n_rows, uint32_t n_bins, const int32_t *h_parent,
                              uint32_t *d_out, int mont_out, uint64_t *additions) {
+    const NvtxRange nvtx_("sfxb_accumulate_tree_dev");
     return guard(c, [&] {
         if (g && !g->parts.empty())
             throw ApiError(SFXB_ERR_UNSUPPORTED, "accumulate: device-pointer entry points take a single-device handle");
@@ -2593,6 +2620,7 @@ int sfxb_accumulate_tree_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bi
 int sfxb_accumulate_tree_gh(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *bins, uint32_t J,
                             const uint32_t *node_offsets, uint32_t N, const uint32_t *rows, uint32_t K,
                             const int32_t *parent, uint32_t *out_slots, uint64_t *additions) {
+    const NvtxRange nvtx_("sfxb_accumulate_tree_gh");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
         if (!g || g->ctx != c) throw ApiError(SFXB_ERR_ARG, "accumulate: gradient handle belongs to another context");
@@ -2618,6 +2646,7 @@ int sfxb_accumulate_tree_gh(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *bins,
 }
 
 int sfxb_bins_upload(sfxb_ctx *c, const uint16_t *bins, uint32_t n_features, uint32_t n_samples, sfxb_bins **out) {
+    const NvtxRange nvtx_("sfxb_bins_upload");
     return guard(c, [&] {
         if (is_group(c)) throw ApiError(SFXB_ERR_UNSUPPORTED, "bins handle: single-device contexts only");
         CK(cudaSetDevice(c->device));
@@ -2645,6 +2674,7 @@ void sfxb_bins_free(sfxb_bins *b) {
 int sfxb_accumulate_tree_bins(sfxb_ctx *c, const sfxb_gh *g, const sfxb_bins *b, const uint32_t *node_offsets,
                               uint32_t N, const uint32_t *rows, uint32_t K, const int32_t *parent,
                               uint32_t *out_slots, uint64_t *additions) {
+    const NvtxRange nvtx_("sfxb_accumulate_tree_bins");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
         if (!g || g->ctx != c) throw ApiError(SFXB_ERR_ARG, "accumulate: gradient handle belongs to another context");
@@ -2677,6 +2707,7 @@ int sfxb_accumulate_part_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bi
                              const uint32_t *d_node_offsets, const uint32_t *h_node_offsets, uint32_t n_nodes,
                              const uint32_t *d_rows, uint32_t n_rows, uint32_t n_bins, const int32_t *h_parent,
                              const uint32_t *h_node_sizes, uint32_t world, uint32_t *d_send, uint32_t *d_real) {
+    const NvtxRange nvtx_("sfxb_accumulate_part_dev");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
         if (!h_node_offsets) throw ApiError(SFXB_ERR_ARG, "accumulate_part: host node offsets required");
@@ -2689,6 +2720,7 @@ int sfxb_accumulate_part_dev(sfxb_ctx *c, const sfxb_gh *g, const uint16_t *d_bi
 int sfxb_combine_slices_dev(sfxb_ctx *c, const sfxb_gh *g, const uint32_t *d_recv, uint32_t world, uint32_t rank,
                             uint32_t n_nodes, uint32_t n_features, uint32_t n_bins, const int32_t *h_parent,
                             const uint32_t *h_node_sizes, uint32_t *d_out) {
+    const NvtxRange nvtx_("sfxb_combine_slices_dev");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
         if (h_parent && !h_node_sizes) throw ApiError(SFXB_ERR_ARG, "combine_slices: node sizes required");
@@ -2721,6 +2753,7 @@ int sfxb_count_additions_dev(sfxb_ctx *c, const uint32_t *d_real, size_t n, uint
 }
 
 int sfxb_reduce_partials_dev(sfxb_ctx *c, const uint32_t *d_parts, uint32_t parts, size_t n_slots, uint32_t *d_out) {
+    const NvtxRange nvtx_("sfxb_reduce_partials_dev");
     return guard(c, [&] {
         CK(cudaSetDevice(c->device));
         reduce_parts_dev(c, d_parts, parts, n_slots, d_out);

@@ -37,6 +37,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "sfxb/errors.hpp"
 #include "sfxb/secure_processor.hpp"
 #include "sfxb_cuda.h"
@@ -152,9 +154,16 @@ void from_words(mpz_class &z, const uint32_t *w, size_t words) {
 // decrypt kernels for the SMs.
 std::atomic<int> g_foreground{0};
 
+// (also one NVTX range per plugin call: the reference's call names in Nsight)
 struct ForegroundCall {
-    ForegroundCall() { g_foreground.fetch_add(1); }
-    ~ForegroundCall() { g_foreground.fetch_sub(1); }
+    explicit ForegroundCall(const char *name) {
+        g_foreground.fetch_add(1);
+        nvtxRangePushA(name);
+    }
+    ~ForegroundCall() {
+        nvtxRangePop();
+        g_foreground.fetch_sub(1);
+    }
     ForegroundCall(const ForegroundCall &) = delete;
     ForegroundCall &operator=(const ForegroundCall &) = delete;
 };
@@ -321,7 +330,7 @@ public:
 
     // ---- encrypt_gh (secure_processor.cpp:574-585)
     GhPayload encrypt_gh(std::span<const GHPair> gh) override {
-        const ForegroundCall fg;
+        const ForegroundCall fg("sfxb::encrypt_gh");
         GhPayload out;
         out.encrypted = true;
         out.n_samples = static_cast<std::uint32_t>(gh.size());
@@ -426,7 +435,7 @@ public:
     HistogramPayload accumulate_rows(const GhPayload &gh, const std::vector<std::vector<std::uint16_t>> &bins,
                                      const std::vector<int> &feature_ids, const std::vector<NodeRows> &nodes,
                                      int n_bins) override {
-        const ForegroundCall fg;
+        const ForegroundCall fg("sfxb::accumulate_rows");
         if (!gh.encrypted) throw Error("paillier accumulate expects encrypted gradients");
         if (gh.cts.size() != 2ull * gh.n_samples)
             throw Error("row-count mismatch: ciphertext count is not 2·n_samples");
@@ -527,8 +536,19 @@ public:
             // was uploaded.  A difference discards the result and reruns on a
             // fresh upload — the device copy is never trusted on a sampled key.
             bool same = false;
-            std::thread verify([&] { same = verify_gh(gh); });
-            rc = run_gpu(true);
+            std::thread verify([&] {
+                try {
+                    same = verify_gh(gh);
+                } catch (...) {
+                    same = false; // treated as a difference: fresh upload below
+                }
+            });
+            try {
+                rc = run_gpu(true);
+            } catch (...) {
+                verify.join();
+                throw;
+            }
             verify.join();
             pt.lap("gpu+verify");
             if (!same) {
@@ -574,7 +594,7 @@ public:
 
     // ---- decrypt_histogram (secure_processor.cpp:679-719)
     std::vector<std::pair<std::uint32_t, Histogram>> decrypt_histogram(const HistogramPayload &payload) override {
-        const ForegroundCall fg;
+        const ForegroundCall fg("sfxb::decrypt_histogram");
         if (!has_priv_) throw AuthorizationError("decrypt requested without private key material");
         if (payload.layout != HistLayout::enc_scalar) {
             if (payload.layout == HistLayout::enc_packed) return decrypt_packed(payload);
@@ -658,7 +678,7 @@ public:
     // batch of encrypt_with_r over every packed plaintext, r drawn in the
     // reference's order (node: G vector, then H vector).
     HistogramPayload encrypt_histogram(const std::vector<std::pair<std::uint32_t, Histogram>> &node_hists) override {
-        const ForegroundCall fg;
+        const ForegroundCall fg("sfxb::encrypt_histogram");
         packing::validate(layout_);
         HistogramPayload out;
         out.layout = HistLayout::enc_packed;
@@ -740,7 +760,7 @@ public:
     // rules and counters in the reference's order; the ciphertext products of
     // each part run as one GPU batch (sfxb_add).
     HistogramPayload add_histograms(const std::vector<HistogramPayload> &parts) override {
-        const ForegroundCall fg;
+        const ForegroundCall fg("sfxb::add_histograms");
         if (parts.empty()) throw Error("add_histograms: no inputs");
         HistogramPayload acc = parts[0];
         for (std::size_t p = 1; p < parts.size(); ++p) {
