@@ -256,7 +256,8 @@ struct P2Args {
     const uint32_t *in;       // per (item, prime): 2s words
     uint32_t *out;            // per (item or element, prime)
     const uint32_t *idx;      // decrypt: item -> element (compaction), else null
-    size_t count;
+    size_t count;             // items [first, first + count) of this launch
+    size_t first;
     uint32_t *status;         // decrypt: bit2 = not coprime
     uint32_t *scratch;        // tables
 };
@@ -285,7 +286,8 @@ __global__ void __launch_bounds__(kBlock, SFXB_P2_MINB) k_p2_pow(P2Args a) {
     const ModRef M = a.mod_p[which].ref();
     uint32_t N[L];
     load_const<s, TPI>(N, M, kMod);
-    SFXB_UNIFORM_LOOP(item, active, a.count) {
+    SFXB_UNIFORM_LOOP(local, active, a.count) {
+        const size_t item = a.first + local;
         const uint32_t *src = a.in + (item * 2 + which) * 2 * s;
         uint32_t A[L], B[L], x[L];
         if constexpr (MODE == 0) {

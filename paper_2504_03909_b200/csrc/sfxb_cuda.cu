@@ -516,42 +516,57 @@ void decrypt_dev(sfxb_ctx *c, const uint32_t *d_cts, size_t count, uint32_t scal
             pa.idx = a.idx;
             pa.count = n_items;
             pa.status = a.status;
-            auto launch = [&](auto tp) {
+            // items [first, first + cnt) at TPv lanes per instance
+            auto launch = [&](auto tp, size_t first, size_t cnt) {
                 constexpr int TPv = decltype(tp)::value;
+                if (cnt == 0) return;
                 auto k = dev::k_p2_pow<cs, TPv, kWindow, 1>;
                 constexpr int NI = dev::kBlock / TPv;
-                int grid = occupancy_grid(*c, k, 2 * (size_t)n_items, NI, 2);
+                int grid = occupancy_grid(*c, k, 2 * cnt, NI, 2);
                 pa.scratch =
                     (uint32_t *)grow(c->scratch_table, 2 * (size_t)grid * NI * ((size_t)(2 * cs) << kWindow) * 4);
+                pa.first = first;
+                pa.count = cnt;
                 k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(pa);
                 check_launch(*c);
             };
-            // Small batches (a tree's first levels: a few thousand slots)
-            // leave most SMs idle at one lane per instance, and the call
-            // takes one exponentiation's latency.  Spread each instance
-            // over 4 (or 2) lanes when that still fits in one wave: ~3x
-            // lower latency, same results (SFXB_DEC_SMALL_TPI=0 disables).
-            int tpi = C::TP;
+            // Whole waves of exponentiations at one lane per instance; what
+            // does not fill a wave — a small batch (a tree's first levels), or
+            // the last partial wave of a large one (a decrypt_tree call of
+            // 1.5, 3.03 or 6.05 waves leaves most SMs idle for a whole
+            // exponentiation) — spread over 4 or 2 lanes per instance when
+            // that finishes sooner: shorter latency, same results
+            // (SFXB_DEC_SMALL_TPI=0 disables).
+            bool split = false;
             if constexpr (C::TP == 1 && (cs == 16 || cs == 32)) {
                 const char *e = std::getenv("SFXB_DEC_SMALL_TPI");
                 if (!e || std::atoi(e) != 0) {
-                    const size_t inst = 2 * (size_t)n_items;
-                    auto lanes_cap = [&](auto k) {
+                    auto instances = [&](auto k, int tpv) { // concurrent instances of kernel k
                         int per_sm = 0;
                         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, dev::kBlock, 0));
-                        return (size_t)std::max(per_sm, 1) * c->sms * dev::kBlock;
+                        return (size_t)std::max(per_sm, 1) * c->sms * (dev::kBlock / tpv);
                     };
-                    if (4 * inst <= lanes_cap(dev::k_p2_pow<cs, 4, kWindow, 1>)) tpi = 4;
-                    else if (2 * inst <= lanes_cap(dev::k_p2_pow<cs, 2, kWindow, 1>)) tpi = 2;
+                    const size_t S1 = instances(dev::k_p2_pow<cs, 1, kWindow, 1>, 1);
+                    const size_t S2 = instances(dev::k_p2_pow<cs, 2, kWindow, 1>, 2);
+                    const size_t S4 = instances(dev::k_p2_pow<cs, 4, kWindow, 1>, 4);
+                    // jobs are (item, prime); full waves of one-lane instances first
+                    const size_t jobs = 2 * (size_t)n_items, full = jobs / S1 * S1;
+                    const size_t bulk = full / 2, tail = n_items - bulk;
+                    // time in units of one one-lane exponentiation: a wave of k-lane
+                    // instances takes ≈ 1.17/k (measured: 2 and 4 lanes run 13–19%
+                    // slower per product)
+                    const double t1 = tail ? 1.0 : 0.0;
+                    const double t2 = std::ceil(2.0 * tail / (double)S2) * (1.15 / 2);
+                    const double t4 = std::ceil(2.0 * tail / (double)S4) * (1.19 / 4);
+                    if (tail && (t4 < t1 || t2 < t1)) {
+                        split = true;
+                        launch(std::integral_constant<int, 1>{}, 0, bulk);
+                        if (t4 <= t2) launch(std::integral_constant<int, 4>{}, bulk, tail);
+                        else launch(std::integral_constant<int, 2>{}, bulk, tail);
+                    }
                 }
             }
-            if constexpr (C::TP == 1 && (cs == 16 || cs == 32)) {
-                if (tpi == 4) launch(std::integral_constant<int, 4>{});
-                else if (tpi == 2) launch(std::integral_constant<int, 2>{});
-                else launch(std::integral_constant<int, C::TP>{});
-            } else {
-                launch(std::integral_constant<int, C::TP>{});
-            }
+            if (!split) launch(std::integral_constant<int, C::TP>{}, 0, n_items);
         } else {
             auto k = dev::k_dec_step<cs, C::TD, kWindow>;
             constexpr int NI = dev::kBlock / C::TD;
