@@ -12,7 +12,9 @@ depend on the plaintexts).  The gradient ciphertexts (1 GB) exceed L2.
 
 Reported (one JSON line, rank 0):
   value       device-resident s/tree (CUDA events on the kernels' stream,
-              max over ranks); lower is better
+              max over ranks); lower is better.  Each step starts from the
+              tree's gradient ciphertexts in HBM and converts them to every
+              party's resident form (CRT / base-n digits) inside the step
   e2e         the same through the C ABI with HOST buffers: per tree the gh
               ciphertexts are uploaded once (sfxb_gh_upload), every level ×
               party uploads bins + frontier and downloads its slots
@@ -511,7 +513,6 @@ def run_ours(a):
     gh = [ops[pi].gh_from_dev(gh_dev, R) for pi in range(a.parties)]
     gh_host = torch.empty((2 * R, cw), dtype=torch.int32, pin_memory=True)
     gh_host.copy_(gh_dev)
-    del gh_dev
     n_slots = [(1 << d) * J * K * 2 for d in range(D)]
     pad = [pdist.padded_slots(s, world) for s in n_slots]
     outs = [[torch.empty((pad[d], cw), dtype=torch.int32, device=dev) for _ in range(a.parties)] for d in range(D)]
@@ -552,6 +553,11 @@ def run_ours(a):
 
     def one_tree(sync_each=True):
         adds = 0
+        # a new tree brings new gradient ciphertexts: every party converts them
+        # to its resident form (digits / Montgomery) inside the step
+        for pi in range(a.parties):
+            gh[pi].free()
+            gh[pi] = ops[pi].gh_from_dev(gh_dev, R)
         for d in range(D):
             offs, rows = d_front[d]
             N = offs.shape[0] - 1
