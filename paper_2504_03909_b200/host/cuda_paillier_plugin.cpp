@@ -993,7 +993,17 @@ private:
         return c;
     }
 
+    // queue capacity in blinding powers (SFXB_ENC_PRECOMPUTE_MAX, default 4M:
+    // 2 GB of device memory at 2048-bit n — two HIGGS trees' worth)
+    static size_t precompute_max() {
+        static const size_t m = std::getenv("SFXB_ENC_PRECOMPUTE_MAX")
+                                    ? (size_t)std::max(0L, std::atol(std::getenv("SFXB_ENC_PRECOMPUTE_MAX")))
+                                    : (size_t)4 << 20;
+        return m;
+    }
+
     void start_precompute(size_t target) {
+        target = std::min(target, precompute_max());
         if (!precompute_enabled() || !has_priv_ || target == 0 || sfxb_ctx_n_shards(ctx_) != 1) return;
         if (!bg_ctx_) {
             // a second context of the same key on the same device, low priority
