@@ -83,7 +83,7 @@ def parse():
     ap.add_argument("--key", default="k2048_7")
     ap.add_argument("--enc-sample", type=int, default=1 << 18)
     ap.add_argument("--dec-sample", type=int, default=1 << 18)
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-sample-rows", type=int, default=12000, help="per host thread (reference arm)")
     ap.add_argument("--cpu-rows", type=int, default=40000, help="single-core cpu_baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
@@ -672,9 +672,13 @@ def run_ours(a):
                 e2e_phase[f"level{d}"] += time.perf_counter() - ta
                 d2h_p += h_out[pi][d].nbytes
             h2d_p += offs.nbytes + rows.nbytes + (0 if bh is not None else h_bins[pi].nbytes)
+        tf = time.perf_counter()
         if bh is not None:
             ops[pi].bins_free(bh)
+        tf2 = time.perf_counter()
         g.free()
+        e2e_phase["bins_free"] += tf2 - tf
+        e2e_phase["gh_free"] += time.perf_counter() - tf2
         counters[pi] = (h2d_p, d2h_p)
 
     e2e_phase = collections.defaultdict(float)
@@ -814,6 +818,7 @@ def run_ours(a):
                            if world == 1 else
                            "per party gh up, device histograms, all_to_all + K4, slots gathered to rank 0"},
         "e2e_phase_s": {k: v / max(1, len(e2e_times)) for k, v in e2e_phase.items()},
+        "e2e_steps_s": e2e_times,
         "gpu_launches": int(launches),
         "roofline": {
             "bound": "imad", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tproducts/s",
