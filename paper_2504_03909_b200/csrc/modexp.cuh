@@ -198,10 +198,11 @@ __device__ __forceinline__ void from_mont(uint32_t (&r)[S / TPI], const uint32_t
     mmul<S, TPI>(r, x, one, st, N, np);
 }
 
-// squarings by mont_sqr (one lane per instance) in an SFXB_SQR build; the
-// default build squares with mont_mul(x, x): measured faster on the B200
-// (fewer products, but lower occupancy and more code)
-#ifdef SFXB_SQR
+// squarings of the mod-p exponentiation (encrypt step 1) by mont_sqr (one
+// lane per instance) in an SFXB_SQR / SFXB_SQR_POW build; the default build
+// squares with mont_mul(x, x): measured faster on the B200.
+// The digit squarings of k_p2_pow do use mont_sqr (padic.cuh p2_mul).
+#if defined(SFXB_SQR) || defined(SFXB_SQR_POW)
 template <int TPI>
 constexpr bool kSqrPow = TPI == 1;
 #else

@@ -29,6 +29,14 @@ __device__ __forceinline__ void stage_regs(const Stage &st, const uint32_t (&v)[
     stage_b<S, TPI>(st, v);
 }
 
+// mont_sqr for the digit squarings at one lane per instance (
+// -DSFXB_NO_SQR_P2 builds the two-CIOS-pass squaring instead)
+#if !defined(SFXB_NO_SQR_P2) || defined(SFXB_SQR)
+constexpr bool kSqrP2 = true;
+#else
+constexpr bool kSqrP2 = false;
+#endif
+
 // One Montgomery product mod p² on digits: (A, B) <- (A, B) ⊛ (A2, B2),
 // or the square when `square` (A2, B2 unused).  Two CIOS passes:
 //   pass 0: square:   v = 2·MM(A, B)
@@ -45,11 +53,7 @@ __device__ __forceinline__ void p2_mul(uint32_t (&A)[s / TPI], uint32_t (&B)[s /
     uint32_t v[L], x[L];
     bool ge = false;
     uint32_t bw = 0;
-#ifdef SFXB_SQR
-    constexpr bool kSqr = TPI == 1; // mont_sqr for the digit squarings (opt-in build)
-#else
-    constexpr bool kSqr = false;
-#endif
+    constexpr bool kSqr = kSqrP2 && TPI == 1;
     if constexpr (kSqr) {
         if (square) {
             // pass 0: v = 2·MM(A, B)
@@ -187,8 +191,12 @@ __device__ __forceinline__ void p2_pow(uint32_t (&A)[s / TPI], uint32_t (&B)[s /
 
 // 32×32 products of p2_pow for a sliding-window program at s limbs
 // (p2_mul: square 2·(2s²+s), multiply (3s²+s) + (2s²+s)).
-inline unsigned long long p2_pow_products(const uint8_t *ops, int n_ops, int w, int s) {
-    const unsigned long long sq = 2ull * (2ull * s * s + s), mul = (3ull * s * s + s) + (2ull * s * s + s);
+// `sqr`: squarings by mont_sqr (one lane per instance, kSqrP2): the pass
+// v = 2·MM(A, B) plus s(s+1)/2 + s² + s for A², instead of 2·(2s²+s)
+inline unsigned long long p2_pow_products(const uint8_t *ops, int n_ops, int w, int s, bool sqr) {
+    const unsigned long long sq = sqr ? (2ull * s * s + s) + (s * (s + 1ull) / 2 + 1ull * s * s + s)
+                                      : 2ull * (2ull * s * s + s),
+                             mul = (3ull * s * s + s) + (2ull * s * s + s);
     unsigned long long prod = sq + mul * ((1ull << (w - 1)) - 1);
     for (int i = 1; i < n_ops; ++i) prod += sq * ops[2 * i] + (ops[2 * i + 1] ? mul : 0ull);
     return prod;

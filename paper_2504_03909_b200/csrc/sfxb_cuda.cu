@@ -327,6 +327,19 @@ struct ProfScope {
 
 // --------------------------------------------------------------- encrypt
 
+// Items per k_p2_pow launch: SFXB_P2_WAVES whole waves (default 1; a wave =
+// the items one launch of `grid` resident blocks holds at once; 0 = a single
+// launch).  Every warp of a launch then runs the same exponentiation program
+// once, in step: with many items per thread the warps of an SM drift apart
+// into different parts of the (fully unrolled, ~100 KB) program, and the
+// instruction cache no longer holds what they execute — one launch over 4M
+// encryptions ran 14% slower per item than one-wave launches
+// (profiles/r02_ab_chunk.jsonl).
+size_t p2_chunk(size_t count, size_t wave) {
+    static const long v = std::getenv("SFXB_P2_WAVES") ? std::atol(std::getenv("SFXB_P2_WAVES")) : 1;
+    return v > 0 ? (size_t)v * std::max<size_t>(wave, 1) : std::max<size_t>(count, 1);
+}
+
 void encrypt_dev(sfxb_ctx *c, const int64_t *d_q, const uint32_t *d_r, size_t count,
                  uint32_t *d_out, uint8_t *d_flags, const uint32_t *d_m = nullptr) {
     if (count == 0) return;
@@ -375,8 +388,19 @@ void encrypt_dev(sfxb_ctx *c, const int64_t *d_q, const uint32_t *d_r, size_t co
                 int grid = occupancy_grid(*c, k, 2 * count, NI, 2);
                 a.scratch = (uint32_t *)grow(c->scratch_table, 2 * (size_t)grid * NI * ((size_t)cs << kWindow) * 4);
                 ProfScope prof_(*c, 1, c->prod_enc * count);
-                k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(a);
-                check_launch(*c);
+                // whole waves per launch as for k_p2_pow (SFXB_STEP1_WAVES)
+                static const long waves1 =
+                    std::getenv("SFXB_STEP1_WAVES") ? std::atol(std::getenv("SFXB_STEP1_WAVES")) : 0;
+                const size_t chunk = waves1 > 0 ? (size_t)waves1 * grid * NI : count;
+                for (size_t f = 0; f < count; f += chunk) {
+                    dev::EncArgs ac = a;
+                    ac.r = a.r + f * S2;
+                    ac.x = a.x + f * 2 * S2;
+                    ac.flags = a.flags ? a.flags + f : nullptr;
+                    ac.count = std::min(chunk, count - f);
+                    k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(ac);
+                    check_launch(*c);
+                }
             }
             if (c->p2_digits) {
                 // y = x^prime mod prime² on base-prime digits (padic.cuh), then plain
@@ -398,8 +422,13 @@ void encrypt_dev(sfxb_ctx *c, const int64_t *d_q, const uint32_t *d_r, size_t co
                     pa.scratch = (uint32_t *)grow(c->scratch_table,
                                                   2 * (size_t)grid * NI * ((size_t)(2 * cs) << kWindow) * 4);
                     ProfScope prof_(*c, 1);
-                    k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(pa);
-                    check_launch(*c);
+                    const size_t chunk = p2_chunk(count, (size_t)grid * NI);
+                    for (size_t f = 0; f < count; f += chunk) {
+                        pa.first = f;
+                        pa.count = std::min(chunk, count - f);
+                        k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(pa);
+                        check_launch(*c);
+                    }
                 }
                 {
                     auto k = dev::k_enc_post<cs, C::TQ>;
@@ -525,10 +554,13 @@ void decrypt_dev(sfxb_ctx *c, const uint32_t *d_cts, size_t count, uint32_t scal
                 int grid = occupancy_grid(*c, k, 2 * cnt, NI, 2);
                 pa.scratch =
                     (uint32_t *)grow(c->scratch_table, 2 * (size_t)grid * NI * ((size_t)(2 * cs) << kWindow) * 4);
-                pa.first = first;
-                pa.count = cnt;
-                k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(pa);
-                check_launch(*c);
+                const size_t chunk = p2_chunk(cnt, (size_t)grid * NI);
+                for (size_t f = 0; f < cnt; f += chunk) {
+                    pa.first = first + f;
+                    pa.count = std::min(chunk, cnt - f);
+                    k<<<dim3(grid, 2), dev::kBlock, 0, c->stream>>>(pa);
+                    check_launch(*c);
+                }
             };
             // Whole waves of exponentiations at one lane per instance; what
             // does not fill a wave — a small batch (a tree's first levels), or
@@ -1949,12 +1981,15 @@ int sfxb_ctx_create(sfxb_ctx **out, int device, const uint32_t *n, uint32_t n_wo
             }
             // profiling units: 32×32 products per item of the exponentiation kernels
             const uint64_t pp = 2ull * s * s + s, pp2 = 2ull * (2 * s) * (2 * s) + 2 * s;
+            int p2_tp = 0;
+            dispatch_class(s, [&](auto sc) { p2_tp = Cls<decltype(sc)::value>::TP; });
+            const bool sqr = dev::kSqrP2 && p2_tp == 1;
             for (int i = 0; i < 2; ++i) {
                 const Win &w = host_window[i];
                 c->prod_enc += w.e1 * pp; // step 1 mod p
                 if (c->p2_digits) {
-                    c->prod_enc += dev::p2_pow_products(w.dig_pr.data(), (int)w.dig_pr.size() / 2, kWindow, s) + 2 * pp;
-                    c->prod_dec += dev::p2_pow_products(w.dig_pm1.data(), (int)w.dig_pm1.size() / 2, kWindow, s) + 2 * pp;
+                    c->prod_enc += dev::p2_pow_products(w.dig_pr.data(), (int)w.dig_pr.size() / 2, kWindow, s, sqr) + 2 * pp;
+                    c->prod_dec += dev::p2_pow_products(w.dig_pm1.data(), (int)w.dig_pm1.size() / 2, kWindow, s, sqr) + 2 * pp;
                 } else {
                     c->prod_enc += w.pr * pp2;
                     c->prod_dec += w.pm1 * pp2;
