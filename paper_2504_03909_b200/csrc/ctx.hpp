@@ -109,6 +109,7 @@ struct CtxState {
     bool n_digits = false;
     uint32_t *d_negR_n = nullptr; // n − R mod n, R = 2^(64s)   (2s)
     uint32_t *d_one_nd = nullptr; // digits of 1̃ [R mod n | R mod n]  (4s)
+    uint32_t *d_r4_nd = nullptr;  // digits of R⁴ mod n² (k_gh_nd_direct)  (4s)
 
     // scratch (grown on demand, freed with the context)
     Buf scratch_table, tmp[4], host_pinned[2], io[6]; // io: host-API staging (grow-only)

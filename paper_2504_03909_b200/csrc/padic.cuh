@@ -652,6 +652,7 @@ struct NdArgs {
     const uint32_t *negR;    // n − R mod n              (2s)
     const uint32_t *one;     // digits of 1̃: [R mod n | R mod n]   (4s)
     const uint32_t *n4;      // n zero-extended           (4s)
+    const uint32_t *r4;      // digits of R⁴ mod n² (the representative of R² mod n²)  (4s)
 };
 
 template <int S, int TPI>
@@ -668,6 +669,35 @@ __global__ void __launch_bounds__(kBlock) k_gh_split_n(NdArgs a, uint32_t *gh, s
         load_lane<S, TPI>(lo, c);
         load_lane<S, TPI>(hi, c + S);
         p2_split<S, TPI>(A, B, lo, hi, st, N, M.np, M.w + kOne * S);
+        if (active) { // each lane rewrites exactly the limbs it read
+            store_lane<S, TPI>(c, A);
+            store_lane<S, TPI>(c + S, B);
+        }
+    }
+}
+
+// Plain ciphertexts X < n² (2S words each, in place) -> digits of X̃ = X·R² mod
+// n² in one kernel: the digits (A0, B0) of X itself (p2_split; as a
+// representative X stands for X·R⁻²) times the digits of R⁴ mod n² give
+// X·R⁴·R⁻² = X̃ — a split plus one digit multiplication, 2·S² + 5·S² + … fewer
+// products than a mod-n² Montgomery conversion (2(2S)² + 2S) followed by the
+// split (k_to_mont + k_gh_split_n).
+template <int S, int TPI>
+__global__ void __launch_bounds__(kBlock) k_gh_nd_direct(NdArgs a, uint32_t *gh, size_t count) {
+    constexpr int L = S / TPI, NI = kBlock / TPI;
+    __shared__ uint2 sB[S / 2 * NI], sD[S / 2 * NI];
+    const Stage st = make_stage<TPI>(sB);
+    const ModRef M = a.mod_n.ref();
+    uint32_t N[L];
+    load_const<S, TPI>(N, M, kMod);
+    SFXB_UNIFORM_LOOP(e, active, count) {
+        uint32_t *c = gh + e * 2 * S;
+        uint32_t lo[L], hi[L], A[L], B[L];
+        load_lane<S, TPI>(lo, c);
+        load_lane<S, TPI>(hi, c + S);
+        p2_split<S, TPI>(A, B, lo, hi, st, N, M.np, M.w + kOne * S);
+        __syncwarp();
+        p2_mul<S, TPI>(A, B, a.r4, false, st, sD, N, M.np, M.w + kOne * S, a.negR);
         if (active) { // each lane rewrites exactly the limbs it read
             store_lane<S, TPI>(c, A);
             store_lane<S, TPI>(c + S, B);

@@ -699,6 +699,7 @@ dev::NdArgs nd_args(const sfxb_ctx *c) {
     a.mod_n2 = arg(c->mod_n2);
     a.negR = c->d_negR_n;
     a.one = c->d_one_nd;
+    a.r4 = c->d_r4_nd;
     a.n4 = c->d_n4;
     return a;
 }
@@ -724,6 +725,15 @@ void gh_prepare_range(sfxb_ctx *c, sfxb_gh *g, size_t lo, size_t hi) {
             k<<<occupancy_grid(*c, k, n2, NI), dev::kBlock, 0, c->stream>>>(crt_args(c), d, n2);
             check_launch(*c);
         } else {
+            static const bool two_step = std::getenv("SFXB_GH_ND_DIRECT") && std::atoi(std::getenv("SFXB_GH_ND_DIRECT")) == 0;
+            if (g->digits_n && !two_step) {
+                // digits of X̃ straight from X (padic.cuh k_gh_nd_direct)
+                auto kd = dev::k_gh_nd_direct<2 * cs, C::TND>;
+                constexpr int NId = dev::kBlock / C::TND;
+                kd<<<occupancy_grid(*c, kd, n2, NId), dev::kBlock, 0, c->stream>>>(nd_args(c), d, n2);
+                check_launch(*c);
+                return;
+            }
             auto k = dev::k_to_mont<4 * cs, C::TH>;
             constexpr int NI = dev::kBlock / C::TH;
             k<<<occupancy_grid(*c, k, n2, NI), dev::kBlock, 0, c->stream>>>(arg(c->mod_n2), d, n2);
@@ -1918,6 +1928,27 @@ int sfxb_ctx_create(sfxb_ctx **out, int device, const uint32_t *n, uint32_t n_wo
             std::copy(mnn.r1.begin(), mnn.r1.end(), one.begin());
             std::copy(mnn.r1.begin(), mnn.r1.end(), one.begin() + 2 * s);
             c->d_one_nd = dev_upload(*c, one.data(), one.size());
+            // digits (A, B) of V = R⁴ mod n² (R = 2^(32·2s); mn2's R² is R⁴):
+            // V ≡ A·R + B·n (mod n²), A = V·R⁻¹ mod n, B = (V − A·R mod n²)/n
+            // (exact, by the 2-adic inverse of n)
+            const Big V = mn2.r2;
+            const Big A = host::mod(mnn.mont_mul(host::mod(V, N), host::from_u64(1)), N);
+            Big AR(4 * (size_t)s + 1, 0);
+            for (size_t i = 0; i < A.size() && i < 2 * (size_t)s; ++i) AR[2 * s + i] = A[i];
+            const Big x = host::mod(AR, c->n2);
+            const Big T = host::cmp(V, x) >= 0 ? host::sub(V, x) : host::sub(host::add(V, c->n2), x);
+            const Big B = host::low(host::mul(host::low(T, 2 * s), host::inv_pow2(N, 2 * s)), 2 * s);
+            Big chk = host::mod(host::add(AR, host::mul(B, N)), c->n2);
+            host::trim(chk);
+            Big Vt = V;
+            host::trim(Vt);
+            if (host::cmp(chk, Vt) != 0 || host::cmp(B, N) >= 0)
+                throw ApiError(SFXB_ERR_ARG, "base-n digits of R^4 mod n^2 (modulus outside the digit class)");
+            std::vector<uint32_t> r4(4 * (size_t)s, 0u);
+            const Big Ap = host::pad(A, 2 * s), Bp = host::pad(B, 2 * s);
+            std::copy(Ap.begin(), Ap.begin() + 2 * s, r4.begin());
+            std::copy(Bp.begin(), Bp.begin() + 2 * s, r4.begin() + 2 * s);
+            c->d_r4_nd = dev_upload(*c, r4.data(), r4.size());
         }
         if (p && q && pq_words) {
             Big P = host::from_words(p, pq_words), Q = host::from_words(q, pq_words);

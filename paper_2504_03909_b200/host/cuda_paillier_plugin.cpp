@@ -149,21 +149,28 @@ void from_words(mpz_class &z, const uint32_t *w, size_t words) {
 //
 // Plugin calls in flight in this process (every instance: the parties'
 // plugins share the GPU).  The offline phase launches its next chunk only
-// while none is — it fills the host's gaps between calls (the reference's
-// Bus, gradients, splits) instead of competing with the histogram and
-// decrypt kernels for the SMs.
+// when precompute_may_run(): by default not while a decrypt_histogram call
+// (exponentiations competing for the same SMs) is in flight — it fills the
+// host's gaps between calls (the reference's Bus, gradients, splits) and the
+// idle SMs of accumulate_rows' host phases and transfers.
 std::atomic<int> g_foreground{0};
+// decrypt_histogram calls in flight (SFXB_ENC_PRECOMPUTE=nodecrypt pauses
+// the offline phase only for these: they are exponentiations themselves)
+std::atomic<int> g_exclusive{0};
 
 // (also one NVTX range per plugin call: the reference's call names in Nsight)
 struct ForegroundCall {
-    explicit ForegroundCall(const char *name) {
+    explicit ForegroundCall(const char *name, bool exclusive = false) : excl(exclusive) {
         g_foreground.fetch_add(1);
+        if (excl) g_exclusive.fetch_add(1);
         nvtxRangePushA(name);
     }
     ~ForegroundCall() {
         nvtxRangePop();
+        if (excl) g_exclusive.fetch_sub(1);
         g_foreground.fetch_sub(1);
     }
+    const bool excl;
     ForegroundCall(const ForegroundCall &) = delete;
     ForegroundCall &operator=(const ForegroundCall &) = delete;
 };
@@ -594,7 +601,7 @@ public:
 
     // ---- decrypt_histogram (secure_processor.cpp:679-719)
     std::vector<std::pair<std::uint32_t, Histogram>> decrypt_histogram(const HistogramPayload &payload) override {
-        const ForegroundCall fg("sfxb::decrypt_histogram");
+        const ForegroundCall fg("sfxb::decrypt_histogram", true);
         if (!has_priv_) throw AuthorizationError("decrypt requested without private key material");
         if (payload.layout != HistLayout::enc_scalar) {
             if (payload.layout == HistLayout::enc_packed) return decrypt_packed(payload);
@@ -979,12 +986,26 @@ private:
         }();
         return on;
     }
-    static bool precompute_always() {
-        static const bool on = [] {
+    // when the next chunk may launch: 2 = except during decrypt_histogram
+    // (default, "nodecrypt": between calls and under accumulate_rows, whose
+    // host phases and transfers leave SMs idle), 0 = between plugin calls
+    // only ("between"), 1 = also during decrypt ("always").  Measured through
+    // the plugin (profiles/r02_precompute_policy.md): 4.46–4.58 s/tree vs
+    // 4.70 between calls only, 4.54–4.63 always.
+    static int precompute_mode() {
+        static const int m = [] {
             const char *e = std::getenv("SFXB_ENC_PRECOMPUTE");
-            return e && std::string(e) == "always";
+            const std::string v = e ? e : "";
+            return v == "always" ? 1 : v == "between" ? 0 : 2;
         }();
-        return on;
+        return m;
+    }
+    static bool precompute_may_run() {
+        switch (precompute_mode()) {
+        case 1: return true;
+        case 2: return g_exclusive.load() == 0;
+        default: return g_foreground.load() == 0;
+        }
     }
     static size_t precompute_chunk() {
         static const size_t c = std::getenv("SFXB_ENC_PRECOMPUTE_CHUNK")
@@ -1055,8 +1076,8 @@ private:
         while (!bg_stop_) {
             const size_t have = sfxb_blind_size(blind_);
             if (have >= goal) break;
-            // only between plugin calls (SFXB_ENC_PRECOMPUTE=always: also during them)
-            while (!precompute_always() && g_foreground.load() > 0 && !bg_stop_)
+            // SFXB_ENC_PRECOMPUTE policy (precompute_mode)
+            while (!precompute_may_run() && !bg_stop_)
                 std::this_thread::sleep_for(std::chrono::microseconds(500));
             if (bg_stop_) break;
             const size_t k = std::min(chunk, goal - have);

@@ -102,21 +102,25 @@ def test_training_loop_with_pipelined_encrypt_gh(name, chunk):
         assert got[k] == want[k], k
 
 
-@pytest.mark.parametrize("pre_chunk,enc_chunk", [("97", "61"), ("5000", None), ("0", None)])
+@pytest.mark.parametrize("pre_chunk,enc_chunk,policy", [("97", "61", None), ("5000", None, None), ("0", None, None),
+                                                        ("97", "61", "always"), ("97", None, "between")])
 @pytest.mark.parametrize("name", ["vertical_c1_1024", "vertical_threaded_3p", "horizontal_toy1024"])
-def test_training_loop_with_precomputed_blinding(name, pre_chunk, enc_chunk):
+def test_training_loop_with_precomputed_blinding(name, pre_chunk, enc_chunk, policy):
     """The offline phase (blinding powers of the next encrypt_gh drawn and
     exponentiated in the background, consumed by the online step) in small
     chunks, so later calls find partly filled queues and draw the rest
     (pipelined with a 61-value encrypt chunk), in whole chunks, and switched
-    off (SFXB_ENC_PRECOMPUTE=0): the same r stream, ciphertexts and
-    transcript bytes."""
+    off (SFXB_ENC_PRECOMPUTE=0); launched except during decrypt calls
+    (default), also during them (always) or between calls only (between):
+    the same r stream, ciphertexts and transcript bytes."""
     _need(PLUGIN)
     _need(os.path.join(REF, "libsfxb_refcapi.so"))
     gpath = os.path.join(HERE, "golden", f"train_{name}.json")
     _need(gpath)
     want = json.load(open(gpath))
     env = {"SFXB_ENC_PRECOMPUTE_CHUNK": pre_chunk} if pre_chunk != "0" else {"SFXB_ENC_PRECOMPUTE": "0"}
+    if policy:
+        env["SFXB_ENC_PRECOMPUTE"] = policy
     if enc_chunk:
         env["SFXB_ENC_CHUNK"] = enc_chunk
     got, _ = _train_with_plugin(name, extra_env=env)

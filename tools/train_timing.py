@@ -1,7 +1,8 @@
 """Wall time of whole reference training runs (run_training, report.cpp:132)
-with the GPU plugin interposed, per variant: the offline phase of encryption
-between plugin calls (default), also during them (SFXB_ENC_PRECOMPUTE=always)
-or off (SFXB_ENC_PRECOMPUTE=0).  The recording
+with the GPU plugin interposed, per variant of the offline phase of
+encryption: except during decrypt calls (default), also during them
+(SFXB_ENC_PRECOMPUTE=always), between plugin calls only (=between; listed
+as "nodecrypt" before it became the default) or off (=0).  The recording
 wrapper (oracle/record_plugin.cpp) adds the plugin's own per-call seconds, so
 the host-only share of a tree (the reference's Bus, gradients, splits) is
 visible next to it.  Forests and counters must agree across variants.
@@ -47,7 +48,7 @@ def main():
         import re
 
         text = re.sub(r"num_trees = \d+", f"num_trees = {sys.argv[4]}", text)
-    variants = [{}, {"SFXB_ENC_PRECOMPUTE": "always"}, {"SFXB_ENC_PRECOMPUTE": "0"}]
+    variants = [{}, {"SFXB_ENC_PRECOMPUTE": "always"}, {"SFXB_ENC_PRECOMPUTE": "between"}, {"SFXB_ENC_PRECOMPUTE": "0"}]
     runs = [run(text, bits, seed, v) for v in variants]
     forests = {r.get("forest") for r in runs}
     for r in runs:
