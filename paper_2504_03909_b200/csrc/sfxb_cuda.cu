@@ -271,9 +271,19 @@ struct Cls<32> { // 2048-bit keys (tuned on B200, profiles/)
     static constexpr int T1 = SFXB_T1_32, T2 = SFXB_T2_32, TC = 8, TD = SFXB_TD_32, TE = 4, TH = SFXB_TH_32, TN = 8,
                          TP = SFXB_TP_32, TQ = 4, TND = SFXB_TND_32, TK = SFXB_TK_32;
 };
+// 3072-bit: encrypt step 1 at one lane and the digit exponentiation at two
+// lanes per instance — 123K → 142K enc/s and 176K → 197K dec/s against 2 / 4
+// lanes (profiles/r02_ab_3072.jsonl)
+#ifndef SFXB_T1_48
+#define SFXB_T1_48 1
+#endif
+#ifndef SFXB_TP_48
+#define SFXB_TP_48 2
+#endif
 template <>
-struct Cls<48> {
-    static constexpr int T1 = 2, T2 = 4, TC = 8, TD = 4, TE = 8, TH = 8, TN = 8, TP = 4, TQ = 8, TND = 4, TK = 4;
+struct Cls<48> { // 3072-bit keys
+    static constexpr int T1 = SFXB_T1_48, T2 = 4, TC = 8, TD = 4, TE = 8, TH = 8, TN = 8, TP = SFXB_TP_48, TQ = 8,
+                         TND = 4, TK = 4;
 };
 
 // grid.x for `items` work items spread over `rows` block rows (grid.y)
