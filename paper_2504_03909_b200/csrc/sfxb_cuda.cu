@@ -848,11 +848,46 @@ bool derive_siblings(sfxb_ctx *c, HistBufs &B, uint32_t *hist, const uint32_t *p
         dev::k_gather_small<<<gg, 256, 0, st>>>(hist, d_pairs, n_pairs, spn, S4, tr);
         check_launch(*c);
     }
-    auto kup = dev::k_pair_up<S4, C::TH>;
+    // Lanes per instance per tree level: the product tree's upper levels are
+    // a few hundred to a few thousand multiplications each, one after the
+    // other — latency, not throughput.  Where the level's instances would
+    // not fill a wave at C::TH lanes, more lanes per instance (up to 32)
+    // shorten each multiplication's dependent chain (same products, same
+    // residues); the big bottom levels keep C::TH.
+    size_t wave_threads = 0;
+    {
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_pair_up<S4, C::TH>, dev::kBlock, 0));
+        wave_threads = (size_t)std::max(per_sm, 1) * c->sms * dev::kBlock;
+    }
+    static const bool wide = !(std::getenv("SFXB_PAIR_WIDE") && std::atoi(std::getenv("SFXB_PAIR_WIDE")) == 0);
+    auto lanes_for = [&](size_t instances) {
+        int t = C::TH;
+        while (wide && t < 32 && S4 / (2 * t) >= 2 && instances * 2 * t <= wave_threads) t *= 2;
+        return t;
+    };
+    // f(std::integral_constant<int, TPI>) for the runtime lane count t
+    auto with_lanes = [&](int t, auto f) {
+        auto one = [&](auto tp) {
+            constexpr int T = decltype(tp)::value;
+            if constexpr (T >= C::TH && S4 % T == 0 && S4 / T >= 2 && (S4 / T) % 2 == 0) f(tp);
+        };
+        switch (t) {
+        case 32: one(std::integral_constant<int, 32>{}); break;
+        case 16: one(std::integral_constant<int, 16>{}); break;
+        case 8: one(std::integral_constant<int, 8>{}); break;
+        default: one(std::integral_constant<int, C::TH>{}); break;
+        }
+    };
     for (size_t l = 0; l + 1 < lvl_n.size(); ++l) {
-        const int gu = occupancy_grid(*c, kup, lvl_n[l + 1], NI);
         ProfScope prof_(*c, 3, lvl_n[l] / 2);
-        kup<<<gu, dev::kBlock, 0, st>>>(arg(c->mod_n2), tr + lvl_off[l] * S4, lvl_n[l], tr + lvl_off[l + 1] * S4);
+        with_lanes(lanes_for(lvl_n[l + 1]), [&](auto tp) {
+            constexpr int T = decltype(tp)::value;
+            auto kup = dev::k_pair_up<S4, T>;
+            const int gu = occupancy_grid(*c, kup, lvl_n[l + 1], dev::kBlock / T);
+            kup<<<gu, dev::kBlock, 0, st>>>(arg(c->mod_n2), tr + lvl_off[l] * S4, lvl_n[l],
+                                            tr + lvl_off[l + 1] * S4);
+        });
         check_launch(*c);
     }
     // invert the root on the host (GMP mpz_invert, or binary extended Euclid)
@@ -863,12 +898,15 @@ bool derive_siblings(sfxb_ctx *c, HistBufs &B, uint32_t *hist, const uint32_t *p
     if (!host::inv_mod_fast(plain, c->n2, rinv)) return false;
     host::Big rinv_m = host::pad(c->mh_n2->to_mont(rinv), S4);
     CK(cudaMemcpyAsync(inv + lvl_off.back() * S4, rinv_m.data(), S4 * 4, cudaMemcpyHostToDevice, st));
-    auto kdn = dev::k_pair_down<S4, C::TH>;
     for (size_t l = lvl_n.size() - 1; l-- > 0;) {
-        const int gd = occupancy_grid(*c, kdn, lvl_n[l], NI);
         ProfScope prof_(*c, 3, lvl_n[l]);
-        kdn<<<gd, dev::kBlock, 0, st>>>(arg(c->mod_n2), inv + lvl_off[l + 1] * S4, tr + lvl_off[l] * S4, lvl_n[l],
-                                        inv + lvl_off[l] * S4);
+        with_lanes(lanes_for(lvl_n[l]), [&](auto tp) {
+            constexpr int T = decltype(tp)::value;
+            auto kdn = dev::k_pair_down<S4, T>;
+            const int gd = occupancy_grid(*c, kdn, lvl_n[l], dev::kBlock / T);
+            kdn<<<gd, dev::kBlock, 0, st>>>(arg(c->mod_n2), inv + lvl_off[l + 1] * S4, tr + lvl_off[l] * S4,
+                                            lvl_n[l], inv + lvl_off[l] * S4);
+        });
         check_launch(*c);
     }
     CK(cudaStreamSynchronize(st)); // rinv_m is a host temporary
