@@ -824,10 +824,12 @@ def run_ours(a):
             "bound": "imad", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tproducts/s",
             "frac": achieved / peak if peak else None,
             # dram__bytes_read.sum + dram__bytes_write.sum of one K2 launch from the round's
-            # ncu --set full capture (profiles/r01_nd.raw.csv, k_seg_prod_nd pass 1 at 200k rows):
-            # read 0.486 GB + wrote 0.023 GB against <= 0.23 GB of unique gh rows + partials (each
-            # row's ciphertexts are gathered once per feature; L2 hit rate 56%)
-            "traffic": 0.509e9, "traffic_algorithmic": 0.23e9,
+            # ncu --set full capture at the bench size (profiles/r02_nd.raw.csv: k_seg_prod_nd,
+            # level 0 pass 1, 1M rows): read 14.204 GB + wrote 0.231 GB, against the launch's
+            # algorithmic bytes — every (row, feature) gathers its G and H digits once
+            # (1M x 14 x 2 x 512 B = 14.336 GB) and writes one partial per piece (0.224 GB)
+            "traffic": 14.435e9, "traffic_algorithmic": 14.56e9,
+            "traffic_launch": "k_seg_prod_nd<64,4,64> level 0 pass 1 at 1M rows (ncu, profiles/r02_nd.raw.csv)",
             "kernel": "K2 segmented product: k_seg_prod_nd (passive party) + k_seg_prod_p2 (key holder)",
             "work": f"K2 executed {k2_modmuls:.4g} 32x32->64 products in the timed steps: passive party "
                     f"5S^2+2S = {5 * (cw // 2) ** 2 + 2 * (cw // 2)} per ciphertext multiplication (base-n "

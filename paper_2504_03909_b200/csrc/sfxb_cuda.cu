@@ -286,6 +286,24 @@ struct Cls<48> { // 3072-bit keys
                          TND = 4, TK = 4;
 };
 
+// lanes per instance of the gh conversions (key holder's CRT digits, passive
+// party's base-n digits): the class's TQ / TND, 2 at 2048 bits (bench A/B,
+// 0.4579 -> 0.4554 / 0.4562 s/tree: fewer lanes, fewer shuffles, some spills)
+template <typename C>
+constexpr int kTG = C::TQ;
+template <typename C>
+constexpr int kTGN = C::TND;
+#ifndef SFXB_TG_32
+#define SFXB_TG_32 2
+#endif
+#ifndef SFXB_TGN_32
+#define SFXB_TGN_32 2
+#endif
+template <>
+constexpr int kTG<Cls<32>> = SFXB_TG_32;
+template <>
+constexpr int kTGN<Cls<32>> = SFXB_TGN_32;
+
 // grid.x for `items` work items spread over `rows` block rows (grid.y)
 template <typename K>
 int occupancy_grid(CtxState &c, K kernel, size_t items, int NI, int rows = 1) {
@@ -730,16 +748,16 @@ void gh_prepare_range(sfxb_ctx *c, sfxb_gh *g, size_t lo, size_t hi) {
         check_launch(*c);
         if (g->digits) {
             // key holder: CRT digits mod p², q² (padic.cuh "K2 at the key holder")
-            auto k = dev::k_gh_digits<cs, C::TQ>;
-            constexpr int NI = dev::kBlock / C::TQ;
+            auto k = dev::k_gh_digits<cs, kTG<C>>;
+            constexpr int NI = dev::kBlock / kTG<C>;
             k<<<occupancy_grid(*c, k, n2, NI), dev::kBlock, 0, c->stream>>>(crt_args(c), d, n2);
             check_launch(*c);
         } else {
             static const bool two_step = std::getenv("SFXB_GH_ND_DIRECT") && std::atoi(std::getenv("SFXB_GH_ND_DIRECT")) == 0;
             if (g->digits_n && !two_step) {
                 // digits of X̃ straight from X (padic.cuh k_gh_nd_direct)
-                auto kd = dev::k_gh_nd_direct<2 * cs, C::TND>;
-                constexpr int NId = dev::kBlock / C::TND;
+                auto kd = dev::k_gh_nd_direct<2 * cs, kTGN<C>>;
+                constexpr int NId = dev::kBlock / kTGN<C>;
                 kd<<<occupancy_grid(*c, kd, n2, NId), dev::kBlock, 0, c->stream>>>(nd_args(c), d, n2);
                 check_launch(*c);
                 return;
