@@ -592,16 +592,23 @@ void decrypt_dev(sfxb_ctx *c, const uint32_t *d_cts, size_t count, uint32_t scal
             };
             // Whole waves of exponentiations at one lane per instance; what
             // does not fill a wave — a small batch (a tree's first levels), or
-            // the last partial wave of a large one (a decrypt_tree call of
-            // 1.5, 3.03 or 6.05 waves leaves most SMs idle for a whole
-            // exponentiation) — spread over 4 or 2 lanes per instance when
-            // that finishes sooner: shorter latency, same results
-            // (SFXB_DEC_SMALL_TPI=0 disables).
+            // the last partial wave of a large one — may finish sooner at 2 or
+            // 4 lanes per instance.  A one-lane wave takes ≈0.75–1.1 of a full
+            // wave's time however few its jobs (latency); at 4 lanes time
+            // follows the job count (≈1.15 µs per job at 2048 bits); at 2
+            // lanes a wave holds half as many jobs and takes ≈0.66 of a
+            // one-lane wave.  Measured at 2048 bits (tools/dec_latency.py,
+            // profiles/r02_dec_latency.jsonl): 3,584 / 7,168 / 14,336 items
+            // take 9.2 / 15.5 / 22.7 ms with this choice against 17.3 / 17.7 /
+            // 22.7 at one lane, 9.2 / 19.7 / 32.5 at 4 lanes and 11.4 / 15.5 /
+            // 30.9 at 2 lanes; 28,672 items (a wave + 51% of one) 46 ms with
+            // the tail at 4 lanes against 49.5 at one and 50.9 at two.  Same
+            // results in every case (SFXB_DEC_SMALL_TPI=0: one lane for all).
             bool split = false;
             if constexpr (C::TP == 1 && (cs == 16 || cs == 32)) {
                 const char *e = std::getenv("SFXB_DEC_SMALL_TPI");
                 if (!e || std::atoi(e) != 0) {
-                    auto instances = [&](auto k, int tpv) { // concurrent instances of kernel k
+                    auto instances = [&](auto k, int tpv) { // concurrent (item, prime) jobs of kernel k
                         int per_sm = 0;
                         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, dev::kBlock, 0));
                         return (size_t)std::max(per_sm, 1) * c->sms * (dev::kBlock / tpv);
@@ -611,17 +618,17 @@ void decrypt_dev(sfxb_ctx *c, const uint32_t *d_cts, size_t count, uint32_t scal
                     const size_t S4 = instances(dev::k_p2_pow<cs, 4, kWindow, 1>, 4);
                     // jobs are (item, prime); full waves of one-lane instances first
                     const size_t jobs = 2 * (size_t)n_items, full = jobs / S1 * S1;
-                    const size_t bulk = full / 2, tail = n_items - bulk;
-                    // time in units of one one-lane exponentiation: a wave of k-lane
-                    // instances takes ≈ 1.17/k (measured: 2 and 4 lanes run 13–19%
-                    // slower per product)
-                    const double t1 = tail ? 1.0 : 0.0;
-                    const double t2 = std::ceil(2.0 * tail / (double)S2) * (1.15 / 2);
-                    const double t4 = std::ceil(2.0 * tail / (double)S4) * (1.19 / 4);
-                    if (tail && (t4 < t1 || t2 < t1)) {
+                    const size_t bulk = full / 2, tail = n_items - bulk, J = 2 * tail;
+                    int lanes = 1;
+                    if (tail) {
+                        if (4 * J <= 3 * S4) lanes = 4;             // a small batch: 4 lanes
+                        else if (5 * J <= 4 * S2) lanes = 2;        // within one 2-lane wave
+                        else if (5 * J <= 3 * S1) lanes = 4;        // up to 60% of a one-lane wave
+                    }
+                    if (lanes > 1) {
                         split = true;
                         launch(std::integral_constant<int, 1>{}, 0, bulk);
-                        if (t4 <= t2) launch(std::integral_constant<int, 4>{}, bulk, tail);
+                        if (lanes == 4) launch(std::integral_constant<int, 4>{}, bulk, tail);
                         else launch(std::integral_constant<int, 2>{}, bulk, tail);
                     }
                 }
