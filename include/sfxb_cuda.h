@@ -86,6 +86,10 @@ void sfxb_host_free(void *p);
 int sfxb_device_count(void);
 /* shards of a context (1 for sfxb_ctx_create) and the device of shard k */
 uint32_t sfxb_ctx_n_shards(const sfxb_ctx *ctx);
+/* Encryptions whose exponentiations run concurrently on the context's GPU(s)
+ * (one wave of the encrypt kernels; summed over shards): batches that are
+ * whole multiples of it leave no partial last wave.  0 on error. */
+size_t sfxb_ctx_enc_wave(const sfxb_ctx *ctx);
 int sfxb_ctx_shard_device(const sfxb_ctx *ctx, uint32_t k);
 void sfxb_ctx_destroy(sfxb_ctx *ctx);
 const char *sfxb_last_error(const sfxb_ctx *ctx);

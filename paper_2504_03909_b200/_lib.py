@@ -58,6 +58,7 @@ def load() -> C.CDLL:
         "sfxb_ctx_create_multi": (C.c_int, [C.POINTER(vp), _i32p, C.c_uint32, _u32p, C.c_uint32, vp, vp,
                                             C.c_uint32]),
         "sfxb_ctx_n_shards": (C.c_uint32, [vp]),
+        "sfxb_ctx_enc_wave": (C.c_size_t, [vp]),
         "sfxb_device_count": (C.c_int, []),
         "sfxb_ctx_shard_device": (C.c_int, [vp, C.c_uint32]),
         "sfxb_ctx_destroy": (None, [vp]),

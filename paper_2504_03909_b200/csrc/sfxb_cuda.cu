@@ -2201,6 +2201,39 @@ int sfxb_device_count(void) {
 }
 
 uint32_t sfxb_ctx_n_shards(const sfxb_ctx *c) { return c->shards.empty() ? 1u : (uint32_t)c->shards.size(); }
+
+// encryptions per wave on one shard's device (shards[0] is the group itself)
+static size_t enc_wave_one(const sfxb_ctx *c) {
+    size_t items = 0;
+    try {
+        CK(cudaSetDevice(c->device));
+        dispatch_class(c->s, [&](auto sc) {
+            constexpr int cs = decltype(sc)::value;
+            using C = Cls<cs>;
+            // the widest exponentiation of the path encrypt_dev takes; one
+            // block row per prime, so a wave holds per_sm·SMs/2 blocks per prime
+            auto wave = [&](auto k, int tpi, int rows) {
+                int per_sm = 0;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, dev::kBlock, 0));
+                return (size_t)std::max(per_sm, 1) * c->sms * (dev::kBlock / tpi) / rows;
+            };
+            if (!c->has_priv) items = wave(dev::k_pow_n2<4 * cs, C::TN, kWindowN>, C::TN, 1);
+            else if (c->p2_digits) items = wave(dev::k_p2_pow<cs, C::TP, kWindow, 0>, C::TP, 2);
+            else items = wave(dev::k_enc_step2<2 * cs, C::T2, kWindow>, C::T2, 2);
+        });
+    } catch (...) {
+        return 0;
+    }
+    return items;
+}
+
+size_t sfxb_ctx_enc_wave(const sfxb_ctx *c) {
+    if (!c) return 0;
+    if (c->shards.empty()) return enc_wave_one(c);
+    size_t t = 0;
+    for (const sfxb_ctx *sh : c->shards) t += enc_wave_one(sh);
+    return t;
+}
 int sfxb_ctx_shard_device(const sfxb_ctx *c, uint32_t k) {
     if (c->shards.empty()) return k == 0 ? c->device : -1;
     return k < c->shards.size() ? c->shards[k]->device : -1;

@@ -858,6 +858,7 @@ private:
         }
         if (rc != SFXB_OK) throw Error(std::string("CUDA Paillier plugin: ") + sfxb_create_error());
         ct_words_ = sfxb_ctx_ct_words(ctx_);
+        enc_wave_ = sfxb_ctx_enc_wave(ctx_);
     }
 
     // HeRng(seed) (he.cpp:11-15)
@@ -878,10 +879,17 @@ private:
     // k and the rest is redrawn with the reference's exact rejection rule.
     // chunk size (SFXB_ENC_CHUNK overrides; the tests shrink it to exercise
     // the pipeline on small runs)
-    static size_t enc_chunk() {
-        static const size_t c = std::getenv("SFXB_ENC_CHUNK") ? (size_t)std::max(1L, std::atol(std::getenv("SFXB_ENC_CHUNK")))
-                                                             : (size_t)262144;
-        return c;
+    // (default: the multiple of the GPU's encryption wave nearest 256K, so no
+    // chunk but a call's last ends in a partial wave)
+    size_t enc_chunk() const {
+        static const long env = std::getenv("SFXB_ENC_CHUNK") ? std::max(1L, std::atol(std::getenv("SFXB_ENC_CHUNK"))) : 0;
+        return env ? (size_t)env : wave_multiple(262144);
+    }
+    // the multiple of sfxb_ctx_enc_wave nearest `target` (at least one wave)
+    size_t wave_multiple(size_t target) const {
+        const size_t w = enc_wave_;
+        if (w == 0) return target;
+        return std::max<size_t>(1, (target + w / 2) / w) * w;
     }
     void encrypt_gh_pipelined(const std::vector<int64_t> &q, GhPayload &out, size_t first, PhaseTimer &pt) {
         // elements [first, count); out.cts already sized, pin_cts_ holds the
@@ -1007,11 +1015,13 @@ private:
         default: return g_foreground.load() == 0;
         }
     }
-    static size_t precompute_chunk() {
-        static const size_t c = std::getenv("SFXB_ENC_PRECOMPUTE_CHUNK")
-                                    ? (size_t)std::max(1L, std::atol(std::getenv("SFXB_ENC_PRECOMPUTE_CHUNK")))
-                                    : (size_t)16384;
-        return c;
+    // (default: one encryption wave — 18,944 at 2048 bits on a B200 — so each
+    // background launch fills the GPU once)
+    size_t precompute_chunk() const {
+        static const long env = std::getenv("SFXB_ENC_PRECOMPUTE_CHUNK")
+                                    ? std::max(1L, std::atol(std::getenv("SFXB_ENC_PRECOMPUTE_CHUNK")))
+                                    : 0;
+        return env ? (size_t)env : wave_multiple(16384);
     }
 
     // queue capacity in blinding powers (SFXB_ENC_PRECOMPUTE_MAX, default 4M:
@@ -1699,6 +1709,7 @@ private:
     gmp_randstate_t rng_, rng_snapshot_;
     sfxb_ctx *ctx_ = nullptr;
     size_t n_words_ = 0, ct_words_ = 0;
+    size_t enc_wave_ = 0; // sfxb_ctx_enc_wave: encryptions per GPU wave
     sfxb_gh *gh_ = nullptr;
     PinnedBuf pin_r_, pin_cts_, pin_slots_, pin_limbs_, pin_bins_; // page-locked marshalling buffers
     // offline phase: background context, queue of blinding powers, worker

@@ -35,3 +35,32 @@ def test_switches_give_identical_results(kname):
     base = _run(kname, {})
     for sw in SWITCHES:
         assert _run(kname, sw) == base, sw
+
+
+@pytest.mark.parametrize("kname", ["k1024_7", "k2048_7", "k3072_7"])
+def test_encryption_wave_is_a_whole_number_of_blocks(kname):
+    """sfxb_ctx_enc_wave (the adapter sizes its encrypt and offline-phase
+    chunks by it): positive, a whole number of blocks' instances per prime row,
+    the public-key context's wave its own."""
+    sys.path.insert(0, os.path.dirname(HERE))
+    from keys import key
+    from paper_2504_03909_b200 import _lib
+
+    n, p, q = key(kname)
+    priv, pub = _lib.Context(n, p, q), _lib.Context(n)
+    w, wp = priv.lib.sfxb_ctx_enc_wave(priv.h), pub.lib.sfxb_ctx_enc_wave(pub.h)
+    assert w > 0 and wp > 0
+    assert w % 16 == 0 and wp % 4 == 0
+
+
+def test_encryption_wave_of_a_device_group_sums_its_shards():
+    """A device group (device 0 listed twice) reports the sum of its shards'
+    waves (the group context is its own shard 0)."""
+    sys.path.insert(0, os.path.dirname(HERE))
+    from keys import key
+    from paper_2504_03909_b200 import _lib
+
+    n, p, q = key("k2048_7")
+    one = _lib.Context(n, p, q)
+    grp = _lib.Context(n, p, q, devices=[0, 0])
+    assert grp.lib.sfxb_ctx_enc_wave(grp.h) == 2 * one.lib.sfxb_ctx_enc_wave(one.h)
