@@ -37,6 +37,28 @@ constexpr bool kSqrP2 = true;
 constexpr bool kSqrP2 = false;
 #endif
 
+// K2 job claiming: the block takes 4·NIW jobs at once from the global
+// counter between two barriers, so the warps of a block start every job batch
+// in step (they then run the same fully unrolled multiply body together:
+// fewer instruction-fetch stalls) — K2 399.8 -> 396 ms/tree at the bench
+// size, frac 0.883 -> 0.89 (profiles/r02_ab_blockjobs.jsonl).  Built with
+// -DSFXB_K2_WARPJOBS, each warp claims its own NIW jobs instead.
+#ifndef SFXB_K2_WARPJOBS
+#define SFXB_K2_JOB_STATE __shared__ unsigned long long sfxb_jb_
+#define SFXB_K2_CLAIM(base, NIW, total)                                                                      \
+    __syncthreads();                                                                                         \
+    if (threadIdx.x == 0) sfxb_jb_ = atomicAdd(next_job, (unsigned long long)(NIW) * (kBlock / 32));        \
+    __syncthreads();                                                                                         \
+    if (sfxb_jb_ >= (total)) break;                                                                          \
+    base = sfxb_jb_ + (unsigned long long)(threadIdx.x >> 5) * (NIW)
+#else
+#define SFXB_K2_JOB_STATE (void)0
+#define SFXB_K2_CLAIM(base, NIW, total)                                                                      \
+    if ((threadIdx.x & 31) == 0) base = atomicAdd(next_job, (unsigned long long)(NIW));                     \
+    base = __shfl_sync(0xffffffffu, base, 0);                                                                \
+    if (base >= (total)) break
+#endif
+
 // One Montgomery product mod p² on digits: (A, B) <- (A, B) ⊛ (A2, B2),
 // or the square when `square` (A2, B2 unused).  Two CIOS passes:
 //   pass 0: square:   v = 2·MM(A, B)
@@ -515,11 +537,10 @@ __global__ void __launch_bounds__(kBlock, (TPI > 1 ? SFXB_K_MINB : 1)) k_seg_pro
     __shared__ uint2 sB[s / 2 * NI], sD[s / 2 * NI];
     const Stage st = make_stage<TPI>(sB);
     const size_t total = 4 * n_pieces;
+    SFXB_K2_JOB_STATE;
     for (;;) {
         unsigned long long base = 0;
-        if ((threadIdx.x & 31) == 0) base = atomicAdd(next_job, (unsigned long long)NIW);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (base >= total) break;
+        SFXB_K2_CLAIM(base, NIW, total);
         const size_t mine = base + (threadIdx.x & 31) / TPI;
         const bool active = mine < total;
         const size_t job = active ? mine : total - 1;
@@ -719,11 +740,10 @@ __global__ void __launch_bounds__(kBlock, SFXB_ND_MINB) k_seg_prod_nd(NdArgs a, 
     uint32_t N[L];
     load_const<S, TPI>(N, M, kMod);
     const size_t total = 2 * n_pieces;
+    SFXB_K2_JOB_STATE;
     for (;;) {
         unsigned long long base = 0;
-        if ((threadIdx.x & 31) == 0) base = atomicAdd(next_job, (unsigned long long)NIW);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (base >= total) break;
+        SFXB_K2_CLAIM(base, NIW, total);
         const size_t mine = base + (threadIdx.x & 31) / TPI;
         const bool active = mine < total;
         const size_t job = active ? mine : total - 1;
