@@ -676,7 +676,13 @@ void add_dev(sfxb_ctx *c, const uint32_t *d_a, const uint32_t *d_b, size_t count
 
 // items per segmented-product piece: long segments use kPieceLong (fewer
 // partials / passes), short ones kPiece (less tail work)
-constexpr int kPiece = 16, kPieceLong = 64;
+#ifndef SFXB_PIECE_LONG
+#define SFXB_PIECE_LONG 64
+#endif
+#ifndef SFXB_PIECE
+#define SFXB_PIECE 16
+#endif
+constexpr int kPiece = SFXB_PIECE, kPieceLong = SFXB_PIECE_LONG;
 
 struct HistBufs {
     Buf node_of, count, ones, cursor, seg_start, sorted, np, piece_start, pieces, part[2], cub, misc, plen, pord,
