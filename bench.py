@@ -15,10 +15,12 @@ Reported (one JSON line, rank 0):
               max over ranks); lower is better.  Each step starts from the
               tree's gradient ciphertexts in HBM and converts them to every
               party's resident form (CRT / base-n digits) inside the step
-  e2e         the same through the C ABI with HOST buffers: per tree the gh
-              ciphertexts are uploaded once (sfxb_gh_upload), every level ×
-              party uploads bins + frontier and downloads its slots
-              (sfxb_accumulate_gh) — the C++ adapter's call pattern
+  e2e         the same through the C ABI with HOST buffers: per tree and party
+              the gh ciphertexts and the bin columns are uploaded once
+              (sfxb_gh_upload, sfxb_bins_upload), every level uploads its
+              frontier and downloads its slots (sfxb_accumulate_tree_bins) —
+              the C++ adapter's call pattern; median of --e2e-steps (5) trees
+              after one warm-up tree, per-step times in `e2e_steps_s`
   enc_per_s / dec_per_s / adds_per_s: Paillier encrypt (CRT), decrypt (CRT)
               and ciphertext-add throughput, each from its own timed sample
   roofline    dominant kernel K2 (segmented Montgomery product): `achieved` =
